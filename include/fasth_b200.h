@@ -1,0 +1,160 @@
+/*
+ * fasth_b200 — C ABI of the B200-native FastH path (arXiv 2009.13977).
+ *
+ * This is the drop-in boundary for the reference's header-only C++ API in
+ * /root/reference/proj/include/fasth/.  Each entry point below names the
+ * reference function it replaces (file:line).  The C++ mirror of the
+ * reference API (same names, types and exceptions) is include/fasth_b200.hpp,
+ * a header-only layer over these functions.
+ *
+ * Conventions
+ *   - All float* arguments are DEVICE pointers (except the *_host entry).
+ *   - A Householder chain is a column-major d x n fp32 matrix V with leading
+ *     dimension ldv >= d; column k is v_k, in chain order: applying the chain
+ *     to X computes H_1 (H_2 (... (H_n X))) (householder.hpp:44-45).  This is
+ *     also the payload order of the reference's OSVD checkpoint
+ *     (svd_layer.hpp:250-251).
+ *   - Activations X, Y, G, dX are column-major d x m fp32 (sample-contiguous,
+ *     so batch shards are contiguous column ranges).
+ *   - Gradients of a chain, dV, come back column-major d x n (column k is
+ *     dL/dv_k), summed over the batch as in Eq. (5) (householder.hpp:145-147).
+ *   - block_width is the reference's b / --k; it is clamped to [1, n] exactly
+ *     like fasth_forward (fasth.hpp:52).
+ *   - Calls are asynchronous on the context's stream.  In FASTH_CHECK_SYNC
+ *     mode (the default) every call that can raise a data-dependent error
+ *     (degenerate vector, singular sigma, Cayley pole, non-finite input)
+ *     synchronises once before returning so that the status matches the
+ *     reference's exception; in FASTH_CHECK_DEFERRED mode such errors are
+ *     latched on the device and reported by fasth_ctx_check().
+ *   - No exceptions cross this boundary; the status maps 1:1 onto the
+ *     reference's exception hierarchy (matrix.hpp:12-30).
+ *
+ * Build: paper_2009_13977_b200/lib/libfasth_b200.so (sm_100a).
+ */
+#ifndef FASTH_B200_H
+#define FASTH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fasth_status {
+    FASTH_OK = 0,
+    FASTH_ERR_DIMENSION = 1,  /* fasth::DimensionError       (matrix.hpp:17) */
+    FASTH_ERR_DEGENERATE = 2, /* fasth::DegenerateVectorError (matrix.hpp:22) */
+    FASTH_ERR_SINGULAR = 3,   /* fasth::SingularMatrixError   (matrix.hpp:27) */
+    FASTH_ERR_INVALID = 4,    /* fasth::Error                 (matrix.hpp:12) */
+    FASTH_ERR_CUDA = 5,
+    FASTH_ERR_NCCL = 6
+} fasth_status;
+
+typedef struct fasth_ctx_s* fasth_ctx;
+typedef struct fasth_tape_s* fasth_tape;         /* TapeForward  (fasth.hpp:22-29)     */
+typedef struct fasth_svd_tape_s* fasth_svd_tape; /* SvdTape      (svd_layer.hpp:83-86) */
+
+enum { FASTH_CHECK_SYNC = 0, FASTH_CHECK_DEFERRED = 1 };
+
+/* Message of the last non-OK status returned on this host thread. */
+const char* fasth_last_error(void);
+int fasth_version(void);
+
+/* Context: one per (device, stream).  stream == NULL -> the legacy default
+ * stream.  Replaces the reference's process-global worker count
+ * (parallel.hpp:12-30): parallelism here is the grid. */
+fasth_status fasth_ctx_create(int device, void* stream, fasth_ctx* out);
+fasth_status fasth_ctx_destroy(fasth_ctx ctx);
+fasth_status fasth_ctx_set_stream(fasth_ctx ctx, void* stream);
+fasth_status fasth_ctx_set_check(fasth_ctx ctx, int mode);
+/* Synchronise the stream and report (then clear) latched device errors. */
+fasth_status fasth_ctx_check(fasth_ctx ctx);
+/* Number of CUDA kernels this context has launched so far. */
+int64_t fasth_ctx_launch_count(fasth_ctx ctx);
+/* Release cached device memory held by the context's pool. */
+fasth_status fasth_ctx_trim(fasth_ctx ctx);
+
+/* ---- FastH ---------------------------------------------------------------
+ * fasth_forward  replaces  TapeForward fasth_forward(const HouseholderChain&,
+ *                          const Matrix& X, size_t block_width)   fasth.hpp:40
+ *   Y = H_1 ... H_n X.  tape may be NULL (forward only, nothing recorded);
+ *   otherwise *tape receives the record backward needs (the compacted WY
+ *   blocks and per-block activations).  The tape does not reference V after
+ *   this call returns.  d >= 1, n >= 0, m >= 0.
+ * fasth_backward replaces  BackwardResult fasth_backward(const TapeForward&,
+ *                          const Matrix& grad_output)              fasth.hpp:69
+ *   dX = (H_1 ... H_n)^T G and dV (d x n).  dV may be NULL (dX only).
+ *   A tape may be used for several backward calls. */
+fasth_status fasth_forward(fasth_ctx ctx, const float* V, int64_t ldv, int d, int n,
+                           const float* X, int64_t ldx, int m, int block_width, float* Y,
+                           int64_t ldy, fasth_tape* tape);
+fasth_status fasth_backward(fasth_ctx ctx, fasth_tape tape, const float* G, int64_t ldg,
+                            float* dX, int64_t lddx, float* dV, int64_t lddv);
+fasth_status fasth_tape_destroy(fasth_tape tape);
+/* Shape of a tape: any pointer may be NULL. q = number of WY blocks. */
+fasth_status fasth_tape_info(fasth_tape tape, int* d, int* n, int* m, int* block_width, int* q);
+
+/* Host-buffer form of the reference's call pair fasth_forward + fasth_backward
+ * (fasth.hpp:40, :69): all pointers are HOST memory (pinned for full copy
+ * bandwidth), column-major with leading dimension d.  Copies in, runs, copies
+ * out and synchronises. */
+fasth_status fasth_forward_backward_host(fasth_ctx ctx, const float* V, int d, int n,
+                                         const float* X, const float* G, int m, int block_width,
+                                         float* Y, float* dX, float* dV);
+
+/* ---- SVD-reparameterised layer W = U Sigma V^T ---------------------------
+ * SvdParam (svd_layer.hpp:25-72): U chain of nu vectors in dimension out_dim,
+ * V chain of nv vectors in dimension in_dim, sigma of min(out_dim, in_dim). */
+typedef struct fasth_svd_param {
+    int out_dim, in_dim, nu, nv;
+    const float* U; /* out_dim x nu, column-major */
+    int64_t ldu;
+    const float* V; /* in_dim x nv, column-major */
+    int64_t ldv;
+    const float* sigma; /* min(out_dim, in_dim) */
+} fasth_svd_param;
+
+/* svd_forward  (svd_layer.hpp:106): Y = U (Sigma (V^T X)), X in_dim x m.
+ * The tape keeps T1 = V^T X and both legs' records; it reads p->sigma again
+ * in backward, so sigma must stay valid until then. */
+fasth_status fasth_svd_forward(fasth_ctx ctx, const fasth_svd_param* p, const float* X,
+                               int64_t ldx, int m, int block_width, float* Y, int64_t ldy,
+                               fasth_svd_tape* tape);
+/* svd_backward (svd_layer.hpp:122): dX (in_dim x m), dU (out_dim x nu),
+ * dV (in_dim x nv, chain order), dsigma (min dim).  Any output may be NULL. */
+fasth_status fasth_svd_backward(fasth_ctx ctx, const fasth_svd_param* p, fasth_svd_tape tape,
+                                const float* G, int64_t ldg, float* dX, int64_t lddx, float* dU,
+                                int64_t lddu, float* dV, int64_t lddv, float* dsigma);
+fasth_status fasth_svd_tape_destroy(fasth_svd_tape tape);
+
+/* svd_step (svd_layer.hpp:158) fused with clamp_sigma (svd_layer.hpp:196)
+ * when clamp_eps >= 0: v <- v - eta dv, sigma <- sigma - eta dsigma.
+ * Outputs may alias the inputs (in-place update).  A vector whose updated
+ * ||v||^2 <= 1e-30 raises FASTH_ERR_DEGENERATE naming the chain and index
+ * (svd_layer.hpp:174-179); the outputs are then unspecified. */
+fasth_status fasth_svd_step(fasth_ctx ctx, const fasth_svd_param* p, const float* dU,
+                            int64_t lddu, const float* dV, int64_t lddv, const float* dsigma,
+                            float eta, float clamp_eps, float* U_out, int64_t ldou,
+                            float* V_out, int64_t ldov, float* sigma_out);
+/* clamp_sigma (svd_layer.hpp:196-202); epsilon in [0, 1). */
+fasth_status fasth_clamp_sigma(fasth_ctx ctx, const float* sigma, int k, float epsilon,
+                               float* sigma_out);
+
+/* Sigma-ops (matops.hpp).  Square parameters only.
+ *   apply_inverse      W^{-1} X = V Sigma^{-1} U^T X          matops.hpp:69
+ *   apply_exponential  e^W X = U e^Sigma U^T X   (nv == 0)    matops.hpp:98
+ *   apply_cayley       (I-W)(I+W)^{-1} X         (nv == 0)    matops.hpp:107
+ *   log_abs_det        sum ln|sigma_i|                         matops.hpp:57 */
+fasth_status fasth_apply_inverse(fasth_ctx ctx, const fasth_svd_param* p, const float* X,
+                                 int64_t ldx, int m, int block_width, float* Y, int64_t ldy);
+fasth_status fasth_apply_exponential(fasth_ctx ctx, const fasth_svd_param* p, const float* X,
+                                     int64_t ldx, int m, int block_width, float* Y, int64_t ldy);
+fasth_status fasth_apply_cayley(fasth_ctx ctx, const fasth_svd_param* p, const float* X,
+                                int64_t ldx, int m, int block_width, float* Y, int64_t ldy);
+fasth_status fasth_log_abs_det(fasth_ctx ctx, const fasth_svd_param* p, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTH_B200_H */

@@ -1,0 +1,798 @@
+// Host side of the C ABI (include/fasth_b200.h): argument validation with the
+// reference's error semantics, the device memory pool, WY plan construction
+// and the launch sequence of each reference operation.  No compute happens
+// here and there is no CPU fallback: every operation is a sequence of the
+// sm_100a kernels in this directory, and the library fails loudly when no
+// CUDA device is usable.
+#include "fasth_b200.h"
+#include "fasth_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+using namespace fasthb;
+
+namespace {
+
+thread_local std::string g_err;
+
+fasth_status fail(fasth_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define CU(call)                                                                       \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess)                                                         \
+            return fail(FASTH_ERR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                           \
+    } while (0)
+
+#define TRY(call)                          \
+    do {                                   \
+        fasth_status s_ = (call);          \
+        if (s_ != FASTH_OK) return s_;     \
+    } while (0)
+
+size_t size_class(size_t bytes) {
+    size_t c = 512;
+    while (c < bytes) c <<= 1;
+    return c;
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------
+struct fasth_ctx_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int check_mode = FASTH_CHECK_SYNC;
+    int num_sms = 148;
+    ErrWord* err_h = nullptr;  // host-mapped
+    ErrWord* err_d = nullptr;
+    unsigned* counters = nullptr;  // build tickets, self-resetting
+    int counters_len = 0;
+    double* logdet_d = nullptr;
+    int64_t launches = 0;
+    int last_chain = 0, last_index = -1;
+    std::mutex mu;
+    std::map<size_t, std::vector<void*>> free_list;
+    std::map<void*, size_t> live;
+
+    fasth_status alloc(size_t bytes, void** out) {
+        const size_t c = size_class(bytes ? bytes : 1);
+        std::lock_guard<std::mutex> lk(mu);
+        auto& fl = free_list[c];
+        if (!fl.empty()) {
+            *out = fl.back();
+            fl.pop_back();
+        } else {
+            cudaError_t e = cudaMalloc(out, c);
+            if (e != cudaSuccess)
+                return fail(FASTH_ERR_CUDA, "cudaMalloc(%zu): %s", c, cudaGetErrorString(e));
+        }
+        live[*out] = c;
+        return FASTH_OK;
+    }
+    void release(void* p) {
+        if (!p) return;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = live.find(p);
+        if (it == live.end()) return;
+        free_list[it->second].push_back(p);
+        live.erase(it);
+    }
+    template <typename T>
+    fasth_status alloc_n(size_t n, T** out) {
+        void* p = nullptr;
+        TRY(alloc(n * sizeof(T), &p));
+        *out = static_cast<T*>(p);
+        return FASTH_OK;
+    }
+    fasth_status ensure_counters(int q) {
+        if (q <= counters_len) return FASTH_OK;
+        if (counters) cudaFree(counters);
+        const int len = std::max(q, 1024);
+        CU(cudaMalloc(&counters, len * sizeof(unsigned)));
+        CU(cudaMemset(counters, 0, len * sizeof(unsigned)));
+        counters_len = len;
+        return FASTH_OK;
+    }
+    fasth_status launched(cudaError_t e, const char* what) {
+        if (e != cudaSuccess)
+            return fail(FASTH_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
+        ++launches;
+        return FASTH_OK;
+    }
+    // Report latched device errors (after a stream sync) and clear them.
+    fasth_status harvest() {
+        CU(cudaStreamSynchronize(stream));
+        ErrWord w = *err_h;
+        err_h->flags = 0;
+        err_h->index = 0x7fffffff;
+        err_h->chain = 0;
+        if (!w.flags) return FASTH_OK;
+        const char* chain = w.chain == 1 ? "V" : "U";
+        last_chain = w.chain;
+        last_index = w.index;
+        if (w.flags & kErrNonFinite)
+            return fail(FASTH_ERR_INVALID, "non-finite entry in chain %s vector %d", chain, w.index);
+        if (w.flags & kErrDegenerate)
+            return fail(FASTH_ERR_DEGENERATE,
+                        "HouseholderVector: ||v||^2 below degeneracy threshold 1e-30 "
+                        "(chain %s vector %d)",
+                        chain, w.index);
+        if (w.flags & kErrSingular) return fail(FASTH_ERR_SINGULAR, "zero singular value");
+        if (w.flags & kErrPole) return fail(FASTH_ERR_INVALID, "apply_cayley: sigma = -1 pole");
+        return fail(FASTH_ERR_INVALID, "device error flags 0x%x", w.flags);
+    }
+    fasth_status finish() { return check_mode == FASTH_CHECK_SYNC ? harvest() : FASTH_OK; }
+};
+
+struct fasth_tape_s {
+    fasth_ctx ctx = nullptr;
+    Plan plan;
+    int m = 0, b_user = 0;
+    int C = 0, WC = 0, ngroups = 0;
+    float* tapeA = nullptr;  // activations per block
+    float* zf = nullptr;
+    float* tapeG = nullptr;  // gradient per block (backward scratch)
+    float* zb = nullptr;
+    const float* scale = nullptr;  // Sigma-scaled input rows (SVD U leg)
+    int n_valid = 0;
+};
+
+struct fasth_svd_tape_s {
+    fasth_ctx ctx = nullptr;
+    int out_dim = 0, in_dim = 0, m = 0, k = 0;
+    fasth_tape v = nullptr;  // V^T leg (reversed V chain); null if nv == 0
+    fasth_tape u = nullptr;  // U leg; null if nu == 0
+    float* T1 = nullptr;     // V^T X, in_dim x m
+};
+
+namespace {
+
+void free_plan(fasth_ctx c, Plan& p) {
+    c->release(p.Vbl);
+    c->release(p.Tt);
+    c->release(p.gram);
+    p.Vbl = p.Tt = nullptr;
+    p.gram = nullptr;
+}
+
+void free_tape(fasth_tape t) {
+    if (!t) return;
+    fasth_ctx c = t->ctx;
+    free_plan(c, t->plan);
+    c->release(t->tapeA);
+    c->release(t->zf);
+    c->release(t->tapeG);
+    c->release(t->zb);
+    delete t;
+}
+
+int next_pow2_min8(int x) {
+    int p = 8;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Build the compacted chain (Alg. 1 step 1) on the device.
+fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int b_user,
+                        int reversed, int tag, Plan* out) {
+    Plan p;
+    p.d = d;
+    p.n = n;
+    const int b = std::min(std::max(b_user, 1), n);  // fasth.hpp:52
+    p.b = std::min(b, kMaxBS);  // wider blocks run as 64-wide sub-blocks (same product)
+    p.BS = next_pow2_min8(p.b);
+    p.q = (n + p.b - 1) / p.b;
+    p.d_pad = (d + 15) / 16 * 16;
+    p.reversed = reversed;
+    p.tag = tag;
+    const int cap = p.BS >= 64 ? 64 : 128;
+    int RS = std::max(1, (2 * c->num_sms + p.q - 1) / p.q);
+    RS = std::min(RS, p.d_pad / 16);
+    int rps = (p.d_pad + RS - 1) / RS;
+    rps = std::min((rps + 15) / 16 * 16, cap);
+    p.rps = rps;
+    p.RS = (p.d_pad + rps - 1) / rps;
+    TRY(c->alloc_n((size_t)p.q * p.d_pad * p.BS, &p.Vbl));
+    TRY(c->alloc_n((size_t)p.q * p.BS * p.BS, &p.Tt));
+    TRY(c->alloc_n((size_t)p.q * p.RS * p.BS * p.BS, &p.gram));
+    TRY(c->ensure_counters(p.q));
+    p.counter = c->counters;
+    TRY(c->launched(launch_build(p, V, ldv, c->err_d, c->stream), "wy_build"));
+    *out = p;
+    return FASTH_OK;
+}
+
+fasth_status check_mat(const char* what, const float* ptr, int64_t ld, int rows, int cols) {
+    if (rows < 0 || cols < 0) return fail(FASTH_ERR_DIMENSION, "%s: negative shape", what);
+    if ((int64_t)rows * cols > 0 && !ptr) return fail(FASTH_ERR_INVALID, "%s: null pointer", what);
+    if (cols > 0 && ld < std::max(rows, 1))
+        return fail(FASTH_ERR_DIMENSION, "%s: leading dimension %lld < rows %d", what,
+                    (long long)ld, rows);
+    return FASTH_OK;
+}
+
+fasth_status copy_cols(fasth_ctx c, const float* src, int64_t lds, float* dst, int64_t ldd,
+                       int rows, int cols) {
+    if ((int64_t)rows * cols == 0) return FASTH_OK;
+    CU(cudaMemcpy2DAsync(dst, ldd * sizeof(float), src, lds * sizeof(float), rows * sizeof(float),
+                         cols, cudaMemcpyDeviceToDevice, c->stream));
+    return FASTH_OK;
+}
+
+// Forward sweep through a built plan (Alg. 1 step 2).
+fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx, float* Y,
+                         int64_t ldy, bool record) {
+    const Plan& p = t->plan;
+    if (record) {
+        if (!t->tapeA) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeA));
+        if (!t->zf) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zf));
+    }
+    SweepArgs a{};
+    a.Vbl = p.Vbl;
+    a.Tt = p.Tt;
+    a.d = p.d;
+    a.d_pad = p.d_pad;
+    a.m = t->m;
+    a.q = p.q;
+    a.BS = p.BS;
+    a.forward = 1;
+    a.x_in = X;
+    a.ldx = ldx;
+    a.n_valid = t->n_valid;
+    a.scale = t->scale;
+    a.x_out = Y;
+    a.ldo = ldy;
+    a.tape = record ? t->tapeA : nullptr;
+    a.zhat = record ? t->zf : nullptr;
+    return c->launched(launch_sweep(a, t->C, t->WC, c->num_sms, c->stream), "sweep(forward)");
+}
+
+// Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
+fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, int g_valid,
+                          const float* g_scale, float* dX, int64_t lddx, float* dV,
+                          int64_t lddv) {
+    const Plan& p = t->plan;
+    if (!t->tapeA || !t->zf)
+        return fail(FASTH_ERR_INVALID, "fasth_backward: tape was recorded without activations");
+    const bool want_dv = dV != nullptr;
+    if (want_dv) {
+        if (!t->tapeG) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeG));
+        if (!t->zb) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zb));
+    }
+    float* dx = dX;
+    if (!dx) {
+        TRY(c->alloc_n((size_t)p.d * std::max(t->m, 1), &dx));
+        lddx = p.d;
+    }
+    SweepArgs a{};
+    a.Vbl = p.Vbl;
+    a.Tt = p.Tt;
+    a.d = p.d;
+    a.d_pad = p.d_pad;
+    a.m = t->m;
+    a.q = p.q;
+    a.BS = p.BS;
+    a.forward = 0;
+    a.x_in = G;
+    a.ldx = ldg;
+    a.n_valid = g_valid;
+    a.scale = g_scale;
+    a.x_out = dx;
+    a.ldo = lddx;
+    a.tape = want_dv ? t->tapeG : nullptr;
+    a.zhat = want_dv ? t->zb : nullptr;
+    fasth_status s = c->launched(launch_sweep(a, t->C, t->WC, c->num_sms, c->stream),
+                                 "sweep(backward)");
+    if (dx != dX) c->release(dx);
+    TRY(s);
+    if (!want_dv) return FASTH_OK;
+    DvArgs v{};
+    v.Vbl = p.Vbl;
+    v.d = p.d;
+    v.d_pad = p.d_pad;
+    v.n = p.n;
+    v.b = p.b;
+    v.q = p.q;
+    v.BS = p.BS;
+    v.m = t->m;
+    v.WC = t->WC;
+    v.ngroups = t->ngroups;
+    v.reversed = p.reversed;
+    v.tapeA = t->tapeA;
+    v.tapeG = t->tapeG;
+    v.zf = t->zf;
+    v.zb = t->zb;
+    v.dV = dV;
+    v.lddv = lddv;
+    return c->launched(launch_dv(v, c->stream), "dv");
+}
+
+fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
+                      int reversed, int tag, fasth_tape* out) {
+    fasth_tape t = new fasth_tape_s;
+    t->ctx = c;
+    t->m = m;
+    t->b_user = b;
+    t->n_valid = d;
+    fasth_status s = build_plan(c, V, ldv, d, n, b, reversed, tag, &t->plan);
+    if (s != FASTH_OK) {
+        delete t;
+        return s;
+    }
+    t->C = pick_cluster(t->plan.d_pad, m, t->plan.BS, c->num_sms, &t->WC);
+    t->ngroups = (m + t->WC - 1) / t->WC;
+    *out = t;
+    return FASTH_OK;
+}
+
+// Empty chain (n == 0): tape carries only the shape; output = input.
+fasth_tape empty_tape(fasth_ctx c, int d, int m, int b) {
+    fasth_tape t = new fasth_tape_s;
+    t->ctx = c;
+    t->m = m;
+    t->b_user = b;
+    t->plan.d = d;
+    t->plan.n = 0;
+    t->plan.q = 0;
+    t->n_valid = d;
+    return t;
+}
+
+// One chain application y = chain(x) (optionally Sigma-scaled input rows),
+// forward only, used by the Sigma-ops.
+fasth_status apply_chain(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int reversed,
+                         int tag, const float* X, int64_t ldx, int n_valid, const float* scale,
+                         int m, int b, float* Y, int64_t ldy) {
+    if (n == 0) {
+        if (scale || n_valid < d)
+            return c->launched(launch_scale_rows(X, ldx, n_valid, scale, d, m, Y, ldy, 0, c->stream),
+                               "scale_rows");
+        return copy_cols(c, X, ldx, Y, ldy, d, m);
+    }
+    fasth_tape t = nullptr;
+    TRY(new_tape(c, V, ldv, d, n, m, b, reversed, tag, &t));
+    t->scale = scale;
+    t->n_valid = n_valid;
+    fasth_status s = run_forward(c, t, X, ldx, Y, ldy, false);
+    free_tape(t);  // pool reuse is stream ordered: safe to recycle immediately
+    return s;
+}
+
+fasth_status check_param(const char* op, const fasth_svd_param* p) {
+    if (!p) return fail(FASTH_ERR_INVALID, "%s: null parameter", op);
+    if (p->out_dim < 1 || p->in_dim < 1 || p->nu < 0 || p->nv < 0)
+        return fail(FASTH_ERR_DIMENSION, "%s: SvdParam: chain dims inconsistent", op);
+    TRY(check_mat(op, p->U, p->ldu, p->out_dim, p->nu));
+    TRY(check_mat(op, p->V, p->ldv, p->in_dim, p->nv));
+    if (!p->sigma) return fail(FASTH_ERR_INVALID, "%s: null sigma", op);
+    return FASTH_OK;
+}
+
+}  // namespace
+
+// ==========================================================================
+extern "C" {
+
+const char* fasth_last_error(void) { return g_err.c_str(); }
+int fasth_version(void) { return 10000; }
+
+fasth_status fasth_ctx_create(int device, void* stream, fasth_ctx* out) {
+    if (!out) return fail(FASTH_ERR_INVALID, "null out");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(FASTH_ERR_CUDA, "fasth_b200 needs a CUDA device (sm_100a): %s",
+                    e != cudaSuccess ? cudaGetErrorString(e) : "none found");
+    if (device < 0 || device >= ndev) return fail(FASTH_ERR_INVALID, "bad device %d", device);
+    CU(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(FASTH_ERR_CUDA, "fasth_b200 is built for sm_100a (B200); device %d is sm_%d%d",
+                    device, prop.major, prop.minor);
+    fasth_ctx c = new fasth_ctx_s;
+    c->device = device;
+    c->stream = static_cast<cudaStream_t>(stream);
+    c->num_sms = prop.multiProcessorCount;
+    e = cudaHostAlloc(&c->err_h, sizeof(ErrWord), cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(FASTH_ERR_CUDA, "cudaHostAlloc: %s", cudaGetErrorString(e));
+    }
+    c->err_h->flags = 0;
+    c->err_h->index = 0x7fffffff;
+    c->err_h->chain = 0;
+    cudaHostGetDevicePointer(&c->err_d, c->err_h, 0);
+    cudaMalloc(&c->logdet_d, sizeof(double));
+    *out = c;
+    return FASTH_OK;
+}
+
+fasth_status fasth_ctx_destroy(fasth_ctx c) {
+    if (!c) return FASTH_OK;
+    cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->free_list)
+        for (void* p : kv.second) cudaFree(p);
+    for (auto& kv : c->live) cudaFree(kv.first);
+    if (c->counters) cudaFree(c->counters);
+    if (c->logdet_d) cudaFree(c->logdet_d);
+    if (c->err_h) cudaFreeHost(c->err_h);
+    delete c;
+    return FASTH_OK;
+}
+
+fasth_status fasth_ctx_set_stream(fasth_ctx c, void* stream) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    c->stream = static_cast<cudaStream_t>(stream);
+    return FASTH_OK;
+}
+
+fasth_status fasth_ctx_set_check(fasth_ctx c, int mode) {
+    if (!c || (mode != FASTH_CHECK_SYNC && mode != FASTH_CHECK_DEFERRED))
+        return fail(FASTH_ERR_INVALID, "bad check mode");
+    c->check_mode = mode;
+    return FASTH_OK;
+}
+
+fasth_status fasth_ctx_check(fasth_ctx c) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    return c->harvest();
+}
+
+int64_t fasth_ctx_launch_count(fasth_ctx c) { return c ? c->launches : 0; }
+
+fasth_status fasth_ctx_trim(fasth_ctx c) {
+    if (!c) return FASTH_OK;
+    CU(cudaStreamSynchronize(c->stream));
+    std::lock_guard<std::mutex> lk(c->mu);
+    for (auto& kv : c->free_list)
+        for (void* p : kv.second) cudaFree(p);
+    c->free_list.clear();
+    return FASTH_OK;
+}
+
+fasth_status fasth_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X,
+                           int64_t ldx, int m, int block_width, float* Y, int64_t ldy,
+                           fasth_tape* tape) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (d < 1) return fail(FASTH_ERR_DIMENSION, "fasth_forward: chain dim must be >= 1");
+    if (n < 0 || m < 0) return fail(FASTH_ERR_DIMENSION, "fasth_forward: negative shape");
+    TRY(check_mat("fasth_forward: V", V, ldv, d, n));
+    TRY(check_mat("fasth_forward: X", X, ldx, d, m));
+    TRY(check_mat("fasth_forward: Y", Y, ldy, d, m));
+    if (tape) *tape = nullptr;
+    if (n == 0 || m == 0) {  // fasth.hpp:46-51
+        if (n == 0) TRY(copy_cols(c, X, ldx, Y, ldy, d, m));
+        fasth_tape t = nullptr;
+        if (n == 0) {
+            t = empty_tape(c, d, m, block_width);
+        } else {
+            TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t));
+        }
+        fasth_status s = c->finish();
+        if (tape && s == FASTH_OK) *tape = t;
+        else free_tape(t);
+        return s;
+    }
+    fasth_tape t = nullptr;
+    TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t));
+    fasth_status s = run_forward(c, t, X, ldx, Y, ldy, tape != nullptr);
+    if (s == FASTH_OK) s = c->finish();
+    if (s == FASTH_OK && tape)
+        *tape = t;
+    else
+        free_tape(t);
+    return s;
+}
+
+fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, float* dX,
+                            int64_t lddx, float* dV, int64_t lddv) {
+    if (!c || !t) return fail(FASTH_ERR_INVALID, "fasth_backward: null ctx or tape");
+    const int d = t->plan.d, n = t->plan.n, m = t->m;
+    TRY(check_mat("fasth_backward: G", G, ldg, d, m));
+    if (dX) TRY(check_mat("fasth_backward: dX", dX, lddx, d, m));
+    if (dV) TRY(check_mat("fasth_backward: dV", dV, lddv, d, n));
+    if (n == 0) {
+        if (dX) TRY(copy_cols(c, G, ldg, dX, lddx, d, m));
+        return c->finish();
+    }
+    if (m == 0) {
+        if (dV) CU(cudaMemset2DAsync(dV, lddv * sizeof(float), 0, d * sizeof(float), n, c->stream));
+        return c->finish();
+    }
+    TRY(run_backward(c, t, G, ldg, d, nullptr, dX, lddx, dV, lddv));
+    return c->finish();
+}
+
+fasth_status fasth_tape_destroy(fasth_tape t) {
+    free_tape(t);
+    return FASTH_OK;
+}
+
+fasth_status fasth_tape_info(fasth_tape t, int* d, int* n, int* m, int* block_width, int* q) {
+    if (!t) return fail(FASTH_ERR_INVALID, "null tape");
+    if (d) *d = t->plan.d;
+    if (n) *n = t->plan.n;
+    if (m) *m = t->m;
+    if (block_width) *block_width = t->plan.n ? std::min(std::max(t->b_user, 1), t->plan.n) : t->b_user;
+    if (q) *q = t->plan.q;
+    return FASTH_OK;
+}
+
+fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int n,
+                                         const float* X, const float* G, int m, int block_width,
+                                         float* Y, float* dX, float* dV) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (d < 1 || n < 0 || m < 0) return fail(FASTH_ERR_DIMENSION, "bad shape");
+    float *v = nullptr, *x = nullptr, *g = nullptr, *y = nullptr, *dx = nullptr, *dv = nullptr;
+    const size_t nv = (size_t)d * n, nx = (size_t)d * m;
+    TRY(c->alloc_n(std::max<size_t>(nv, 1), &v));
+    TRY(c->alloc_n(std::max<size_t>(nx, 1), &x));
+    TRY(c->alloc_n(std::max<size_t>(nx, 1), &g));
+    TRY(c->alloc_n(std::max<size_t>(nx, 1), &y));
+    TRY(c->alloc_n(std::max<size_t>(nx, 1), &dx));
+    TRY(c->alloc_n(std::max<size_t>(nv, 1), &dv));
+    fasth_status s = FASTH_OK;
+    const int saved = c->check_mode;
+    c->check_mode = FASTH_CHECK_DEFERRED;
+    fasth_tape t = nullptr;
+    do {
+        if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
+        if (nx) CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
+        if (nx) CU(cudaMemcpyAsync(g, G, nx * 4, cudaMemcpyHostToDevice, c->stream));
+        s = fasth_forward(c, v, d, d, n, x, d, m, block_width, y, d, &t);
+        if (s != FASTH_OK) break;
+        s = fasth_backward(c, t, g, d, dx, d, n ? dv : nullptr, d);
+        if (s != FASTH_OK) break;
+        if (nx) CU(cudaMemcpyAsync(Y, y, nx * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (nx) CU(cudaMemcpyAsync(dX, dx, nx * 4, cudaMemcpyDeviceToHost, c->stream));
+        if (nv) CU(cudaMemcpyAsync(dV, dv, nv * 4, cudaMemcpyDeviceToHost, c->stream));
+    } while (0);
+    c->check_mode = saved;
+    fasth_tape_destroy(t);
+    fasth_status h = c->harvest();
+    if (s == FASTH_OK) s = h;
+    for (float* p : {v, x, g, y, dx, dv}) c->release(p);
+    return s;
+}
+
+// ---- SVD layer -------------------------------------------------------------
+fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx,
+                               int m, int block_width, float* Y, int64_t ldy,
+                               fasth_svd_tape* tape) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    TRY(check_param("svd_forward", p));
+    TRY(check_mat("svd_forward: X", X, ldx, p->in_dim, m));
+    TRY(check_mat("svd_forward: Y", Y, ldy, p->out_dim, m));
+    if (tape) *tape = nullptr;
+    fasth_svd_tape st = new fasth_svd_tape_s;
+    st->ctx = c;
+    st->out_dim = p->out_dim;
+    st->in_dim = p->in_dim;
+    st->m = m;
+    st->k = std::min(p->out_dim, p->in_dim);
+    fasth_status s = FASTH_OK;
+    do {
+        s = c->alloc_n((size_t)p->in_dim * std::max(m, 1), &st->T1);
+        if (s) break;
+        // V^T leg: the reversed V chain (svd_layer.hpp:113)
+        if (p->nv > 0 && m > 0) {
+            s = new_tape(c, p->V, p->ldv, p->in_dim, p->nv, m, block_width, 1, 1, &st->v);
+            if (s) break;
+            s = run_forward(c, st->v, X, ldx, st->T1, p->in_dim, tape != nullptr);
+        } else {
+            s = copy_cols(c, X, ldx, st->T1, p->in_dim, p->in_dim, m);
+        }
+        if (s) break;
+        // U leg on T2 = Sigma T1 (svd_layer.hpp:114-115), Sigma fused into the load
+        if (p->nu > 0 && m > 0) {
+            s = new_tape(c, p->U, p->ldu, p->out_dim, p->nu, m, block_width, 0, 0, &st->u);
+            if (s) break;
+            st->u->scale = p->sigma;
+            st->u->n_valid = st->k;
+            s = run_forward(c, st->u, st->T1, p->in_dim, Y, ldy, tape != nullptr);
+        } else {
+            s = c->launched(launch_scale_rows(st->T1, p->in_dim, st->k, p->sigma, p->out_dim, m, Y,
+                                              ldy, 0, c->stream),
+                            "scale_rows");
+        }
+        if (s) break;
+        s = c->finish();
+    } while (0);
+    if (s == FASTH_OK && tape) {
+        *tape = st;
+    } else {
+        fasth_svd_tape_destroy(st);
+    }
+    return s;
+}
+
+fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd_tape st,
+                                const float* G, int64_t ldg, float* dX, int64_t lddx, float* dU,
+                                int64_t lddu, float* dV, int64_t lddv, float* dsigma) {
+    if (!c || !st) return fail(FASTH_ERR_INVALID, "svd_backward: null ctx or tape");
+    TRY(check_param("svd_backward", p));
+    if (p->out_dim != st->out_dim || p->in_dim != st->in_dim)
+        return fail(FASTH_ERR_DIMENSION, "svd_backward: parameter does not match tape");
+    const int m = st->m, k = st->k;
+    TRY(check_mat("svd_backward: G", G, ldg, p->out_dim, m));
+    if (dX) TRY(check_mat("svd_backward: dX", dX, lddx, p->in_dim, m));
+    if (dU) TRY(check_mat("svd_backward: dU", dU, lddu, p->out_dim, p->nu));
+    if (dV) TRY(check_mat("svd_backward: dV", dV, lddv, p->in_dim, p->nv));
+    float* dT2 = nullptr;
+    TRY(c->alloc_n((size_t)p->out_dim * std::max(m, 1), &dT2));
+    fasth_status s = FASTH_OK;
+    do {
+        if (m == 0) {
+            if (dU && p->nu)
+                CU(cudaMemset2DAsync(dU, lddu * 4, 0, p->out_dim * 4, p->nu, c->stream));
+            if (dV && p->nv)
+                CU(cudaMemset2DAsync(dV, lddv * 4, 0, p->in_dim * 4, p->nv, c->stream));
+            if (dsigma && k) CU(cudaMemsetAsync(dsigma, 0, k * 4, c->stream));
+            break;
+        }
+        // U leg (svd_layer.hpp:124)
+        if (st->u) {
+            s = run_backward(c, st->u, G, ldg, p->out_dim, nullptr, dT2, p->out_dim, dU, lddu);
+        } else {
+            s = copy_cols(c, G, ldg, dT2, p->out_dim, p->out_dim, m);
+        }
+        if (s) break;
+        // dSigma (svd_layer.hpp:131-137)
+        if (dsigma) {
+            s = c->launched(launch_dsigma(dT2, p->out_dim, st->T1, p->in_dim, k, m, dsigma,
+                                          c->stream),
+                            "dsigma");
+            if (s) break;
+        }
+        // V^T leg on dT1 = Sigma dT2 (svd_layer.hpp:139-147), Sigma fused into the load
+        if (st->v) {
+            s = run_backward(c, st->v, dT2, p->out_dim, k, p->sigma, dX, lddx, dV, lddv);
+        } else if (dX) {
+            s = c->launched(launch_scale_rows(dT2, p->out_dim, k, p->sigma, p->in_dim, m, dX, lddx,
+                                              0, c->stream),
+                            "scale_rows");
+        }
+        if (s) break;
+    } while (0);
+    c->release(dT2);
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
+fasth_status fasth_svd_tape_destroy(fasth_svd_tape st) {
+    if (!st) return FASTH_OK;
+    free_tape(st->u);
+    free_tape(st->v);
+    st->ctx->release(st->T1);
+    delete st;
+    return FASTH_OK;
+}
+
+fasth_status fasth_svd_step(fasth_ctx c, const fasth_svd_param* p, const float* dU, int64_t lddu,
+                            const float* dV, int64_t lddv, const float* dsigma, float eta,
+                            float clamp_eps, float* U_out, int64_t ldou, float* V_out,
+                            int64_t ldov, float* sigma_out) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    TRY(check_param("svd_step", p));
+    if (!std::isfinite(eta)) return fail(FASTH_ERR_INVALID, "svd_step: eta not finite");
+    if (clamp_eps >= 1.f) return fail(FASTH_ERR_INVALID, "clamp_sigma: epsilon outside [0, 1)");
+    TRY(check_mat("svd_step: dU", dU, lddu, p->out_dim, p->nu));
+    TRY(check_mat("svd_step: dV", dV, lddv, p->in_dim, p->nv));
+    TRY(check_mat("svd_step: U_out", U_out, ldou, p->out_dim, p->nu));
+    TRY(check_mat("svd_step: V_out", V_out, ldov, p->in_dim, p->nv));
+    const int k = std::min(p->out_dim, p->in_dim);
+    if (k && (!dsigma || !sigma_out)) return fail(FASTH_ERR_INVALID, "svd_step: null sigma");
+    TRY(c->launched(launch_step(p->U, p->ldu, dU, lddu, p->out_dim, p->nu, eta, U_out, ldou,
+                                c->err_d, 0, c->stream),
+                    "step(U)"));
+    TRY(c->launched(launch_step(p->V, p->ldv, dV, lddv, p->in_dim, p->nv, eta, V_out, ldov,
+                                c->err_d, 1, c->stream),
+                    "step(V)"));
+    TRY(c->launched(launch_sigma_step(p->sigma, dsigma, k, eta, clamp_eps, sigma_out, c->stream),
+                    "sigma_step"));
+    fasth_status s = c->finish();
+    if (s == FASTH_ERR_DEGENERATE)  // svd_layer.hpp:177-178 wording
+        return fail(s, "svd_step: update degenerates %s vector %d", c->last_chain == 1 ? "V" : "U",
+                    c->last_index);
+    return s;
+}
+
+fasth_status fasth_clamp_sigma(fasth_ctx c, const float* sigma, int k, float epsilon,
+                               float* sigma_out) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (!(epsilon >= 0.f && epsilon < 1.f))
+        return fail(FASTH_ERR_INVALID, "clamp_sigma: epsilon outside [0, 1)");
+    TRY(c->launched(launch_sigma_step(sigma, nullptr, k, 0.f, epsilon, sigma_out, c->stream),
+                    "clamp_sigma"));
+    return c->finish();
+}
+
+namespace {
+// U f(Sigma) U^T X (symmetric form) or V Sigma^{-1} U^T X (inverse).
+fasth_status sigma_op(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx, int m,
+                      int b, float* Y, int64_t ldy, int kind, const char* op) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    TRY(check_param(op, p));
+    if (p->out_dim != p->in_dim) return fail(FASTH_ERR_DIMENSION, "%s: requires a square parameter", op);
+    if (kind != 1 && p->nv != 0)
+        return fail(FASTH_ERR_INVALID, "%s: expects symmetric form (empty V chain)", op);
+    const int d = p->out_dim;
+    TRY(check_mat(op, X, ldx, d, m));
+    TRY(check_mat(op, Y, ldy, d, m));
+    float* f = nullptr;
+    float* t = nullptr;
+    TRY(c->alloc_n((size_t)d, &f));
+    fasth_status s = c->alloc_n((size_t)d * std::max(m, 1), &t);
+    do {
+        if (s) break;
+        s = c->launched(launch_sigma_map(p->sigma, d, kind, f, c->err_d, c->stream), "sigma_map");
+        if (s) break;
+        if (c->check_mode == FASTH_CHECK_SYNC) {  // reference checks before any chain work
+            s = c->harvest();
+            if (s == FASTH_ERR_SINGULAR) s = fail(s, "%s: zero singular value", op);
+            if (s) break;
+        }
+        if (m == 0) break;
+        // U^T X: the reversed U chain (matops.hpp:77, :44)
+        s = apply_chain(c, p->U, p->ldu, d, p->nu, 1, 0, X, ldx, d, nullptr, m, b, t, d);
+        if (s) break;
+        if (kind == 1)  // V (Sigma^{-1} t)      matops.hpp:84
+            s = apply_chain(c, p->V, p->ldv, d, p->nv, 0, 1, t, d, d, f, m, b, Y, ldy);
+        else  // U (f(Sigma) t)                   matops.hpp:51
+            s = apply_chain(c, p->U, p->ldu, d, p->nu, 0, 0, t, d, d, f, m, b, Y, ldy);
+    } while (0);
+    c->release(f);
+    c->release(t);
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+}  // namespace
+
+fasth_status fasth_apply_inverse(fasth_ctx c, const fasth_svd_param* p, const float* X,
+                                 int64_t ldx, int m, int b, float* Y, int64_t ldy) {
+    return sigma_op(c, p, X, ldx, m, b, Y, ldy, 1, "apply_inverse");
+}
+
+fasth_status fasth_apply_exponential(fasth_ctx c, const fasth_svd_param* p, const float* X,
+                                     int64_t ldx, int m, int b, float* Y, int64_t ldy) {
+    return sigma_op(c, p, X, ldx, m, b, Y, ldy, 2, "apply_exponential");
+}
+
+fasth_status fasth_apply_cayley(fasth_ctx c, const fasth_svd_param* p, const float* X,
+                                int64_t ldx, int m, int b, float* Y, int64_t ldy) {
+    return sigma_op(c, p, X, ldx, m, b, Y, ldy, 3, "apply_cayley");
+}
+
+fasth_status fasth_log_abs_det(fasth_ctx c, const fasth_svd_param* p, double* out) {
+    if (!c || !out) return fail(FASTH_ERR_INVALID, "null argument");
+    TRY(check_param("log_abs_det", p));
+    if (p->out_dim != p->in_dim)
+        return fail(FASTH_ERR_DIMENSION, "log_abs_det: requires a square parameter");
+    TRY(c->launched(launch_logdet(p->sigma, p->out_dim, c->logdet_d, c->err_d, c->stream),
+                    "logdet"));
+    CU(cudaMemcpyAsync(out, c->logdet_d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    fasth_status s = c->harvest();  // the value is host-visible: always synchronise
+    if (s == FASTH_ERR_SINGULAR) return fail(s, "log_abs_det: zero singular value");
+    return s;
+}
+
+}  // extern "C"

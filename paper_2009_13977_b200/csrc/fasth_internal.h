@@ -1,0 +1,105 @@
+// Internal (non-ABI) declarations shared by the FastH CUDA translation units.
+//
+// Device layout of one compacted chain ("plan"), built once per call from the
+// caller's column-major V (d x n, column k = v_k):
+//
+//   Vbl [q][d_pad][BS]  f32   block i holds v_{i*bi .. i*bi+w_i-1} (chain
+//                             order, or reversed chain when plan.reversed),
+//                             row-major so that the rows a cluster CTA owns
+//                             are one contiguous bulk copy; zero padded rows
+//                             (d..d_pad) and columns (w_i..BS).
+//   Tt  [q][BS][BS]     f32   T~_i = (diag(V_i^T V_i) + 2 striu(V_i^T V_i))^{-1},
+//                             upper triangular, so that the block product is
+//                             P_i = H.. H.. = I - 2 V_i T~_i V_i^T
+//                             (the UT form of wy.hpp:50-55's W,Y: W = V T~ D,
+//                             Y = V D^{-1}).
+//
+// Per-block tapes written by the sweeps (ngroups = ceil(m / WC)):
+//   tape [q][ngroups][d_pad][WC]  forward: A_i (activations[i], fasth.hpp:28)
+//                                 backward: dA[i] (fasth.hpp:82-86)
+//   zhat [q][BS][m]               forward: Z'f_i = T~_i V_i^T A_{i+1}
+//                                 backward: Z'b_i = T~_i^T V_i^T dA[i]
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fasthb {
+
+constexpr int kThreads = 256;
+constexpr int kMaxBS = 64;
+
+struct ErrWord {  // host-mapped pinned memory, written by kernels
+    int flags;    // bit0 degenerate ||v||^2 <= 1e-30, bit1 non-finite
+    int index;    // smallest offending chain index (atomicMin)
+    int chain;    // which chain (caller tag) raised it
+    int pad;
+};
+
+enum : int { kErrDegenerate = 1, kErrNonFinite = 2, kErrSingular = 4, kErrPole = 8 };
+
+struct Plan {
+    int d = 0, n = 0, b = 0;  // b: internal block width (<= kMaxBS)
+    int q = 0, BS = 0, d_pad = 0;
+    int reversed = 0;
+    int tag = 0;  // error-report tag (0 = U / plain chain, 1 = V)
+    float* Vbl = nullptr;
+    float* Tt = nullptr;
+    double* gram = nullptr;      // [q][RS][BS][BS] partial Gram
+    unsigned* counter = nullptr; // [q], self-resetting
+    int RS = 0, rps = 0;         // row splits of the build, rows per split
+};
+
+struct SweepArgs {
+    const float* Vbl;
+    const float* Tt;
+    int d, d_pad, m, q, BS;
+    int forward;          // 1: Alg 1 step 2 (blocks q-1..0, T~), 0: Alg 2 step 1 (0..q-1, T~^T)
+    const float* x_in;    // column-major, rows < n_valid are read
+    int64_t ldx;
+    int n_valid;          // rows of x_in that exist (rest are zero)
+    const float* scale;   // optional per-row scale applied on load (Sigma)
+    float* x_out;         // column-major d x m
+    int64_t ldo;
+    float* tape;          // optional, see header comment
+    float* zhat;          // optional [q][BS][m]
+};
+
+struct DvArgs {
+    const float* Vbl;
+    int d, d_pad, n, b, q, BS, m, WC, ngroups;
+    int reversed;
+    const float* tapeA;   // [q][ngroups][d_pad][WC]
+    const float* tapeG;
+    const float* zf;      // [q][BS][m]
+    const float* zb;
+    float* dV;            // column-major d x n
+    int64_t lddv;
+};
+
+// wy_build.cu
+cudaError_t launch_build(const Plan& p, const float* V, int64_t ldv, ErrWord* err,
+                         cudaStream_t s);
+// chain_sweep.cu
+cudaError_t launch_sweep(const SweepArgs& a, int C, int WC, int num_sms, cudaStream_t s);
+int pick_cluster(int d_pad, int m, int BS, int num_sms, int* WC);
+size_t sweep_smem_bytes(int C, int WC, int BS, int d_pad);
+// dv.cu
+cudaError_t launch_dv(const DvArgs& a, cudaStream_t s);
+// sigma_ops.cu
+cudaError_t launch_scale_rows(const float* x, int64_t ldx, int n_valid, const float* scale,
+                              int rows, int m, float* y, int64_t ldy, int mode,
+                              cudaStream_t s);
+cudaError_t launch_dsigma(const float* dT2, int64_t ld2, const float* T1, int64_t ld1, int k,
+                          int m, float* dsigma, cudaStream_t s);
+cudaError_t launch_step(const float* P, int64_t ldp, const float* dP, int64_t lddp, int dim,
+                        int n, float eta, float* out, int64_t ldo, ErrWord* err, int tag,
+                        cudaStream_t s);
+cudaError_t launch_sigma_step(const float* sigma, const float* dsigma, int k, float eta,
+                              float clamp_eps, float* out, cudaStream_t s);
+cudaError_t launch_sigma_map(const float* sigma, int k, int kind, float* out, ErrWord* err,
+                             cudaStream_t s);
+cudaError_t launch_logdet(const float* sigma, int k, double* out, ErrWord* err,
+                          cudaStream_t s);
+
+}  // namespace fasthb

@@ -1,0 +1,413 @@
+"""Python mirror of the reference FastH API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference's
+header-only C++ API (/root/reference/proj/include/fasth/), with torch CUDA
+tensors in place of ``fasth::Matrix``:
+
+=====================================  ==========================================
+reference (file:line)                  here
+=====================================  ==========================================
+``fasth_forward`` fasth.hpp:40         ``fasth_forward(V, X, block_width)``
+``fasth_backward`` fasth.hpp:69        ``fasth_backward(tape, G)``
+``svd_forward`` svd_layer.hpp:106      ``svd_forward(p, X, block_width)``
+``svd_backward`` svd_layer.hpp:122     ``svd_backward(p, tape, G)``
+``svd_step`` svd_layer.hpp:158         ``svd_step(p, grads, eta)``
+``clamp_sigma`` svd_layer.hpp:196      ``clamp_sigma(p, epsilon)``
+``apply_inverse`` matops.hpp:69        ``apply_inverse(p, X, block_width)``
+``apply_exponential`` matops.hpp:98    ``apply_exponential(p, X, block_width)``
+``apply_cayley`` matops.hpp:107        ``apply_cayley(p, X, block_width)``
+``log_abs_det`` matops.hpp:57          ``log_abs_det(p)``
+=====================================  ==========================================
+
+Shapes follow the reference: a chain is an ``(n, d)`` tensor (row k = v_k,
+chain order), activations are ``(d, m)`` (rows = dimension, columns = batch).
+Activations are stored column-major on the device (each sample contiguous);
+inputs in any layout are accepted, outputs are ``(d, m)`` views of
+column-major storage.  All arithmetic runs in the sm_100a kernels of
+``lib/libfasth_b200.so``; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+
+# ---- error hierarchy (matrix.hpp:12-30) -----------------------------------
+
+
+class Error(RuntimeError):
+    """fasth::Error"""
+
+
+class DimensionError(Error):
+    """fasth::DimensionError"""
+
+
+class DegenerateVectorError(Error):
+    """fasth::DegenerateVectorError"""
+
+
+class SingularMatrixError(Error):
+    """fasth::SingularMatrixError"""
+
+
+class CudaError(Error):
+    pass
+
+
+_ERRORS = {1: DimensionError, 2: DegenerateVectorError, 3: SingularMatrixError, 4: Error,
+           5: CudaError, 6: CudaError}
+
+
+def _check(status: int):
+    if status:
+        msg = _lib.load().fasth_last_error().decode()
+        raise _ERRORS.get(status, Error)(msg)
+
+
+# ---- context -------------------------------------------------------------
+
+
+class Context:
+    """One per (device, stream).  ``stream=None`` follows torch's current
+    stream at every call.  ``deferred=True`` latches device-side errors
+    (degeneracy, singular sigma) until :meth:`check` instead of
+    synchronising inside each call."""
+
+    def __init__(self, device: int = 0, deferred: bool = False):
+        self.lib = _lib.load()
+        self.device = device
+        h = C.c_void_p()
+        with torch.cuda.device(device):
+            _check(self.lib.fasth_ctx_create(device, None, C.byref(h)))
+        self.h = h
+        self.set_deferred(deferred)
+
+    def set_deferred(self, deferred: bool):
+        _check(self.lib.fasth_ctx_set_check(self.h, 1 if deferred else 0))
+        self.deferred = deferred
+
+    def bind_stream(self, stream: torch.cuda.Stream | None = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _check(self.lib.fasth_ctx_set_stream(self.h, C.c_void_p(s.cuda_stream)))
+
+    def check(self):
+        _check(self.lib.fasth_ctx_check(self.h))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.fasth_ctx_launch_count(self.h))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.lib.fasth_ctx_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int | None = None) -> Context:
+    dev = torch.cuda.current_device() if device is None else device
+    if dev not in _default:
+        _default[dev] = Context(dev)
+    return _default[dev]
+
+
+def _ctx(ctx, t: torch.Tensor) -> Context:
+    c = ctx if ctx is not None else default_context(t.device.index)
+    c.bind_stream()
+    return c
+
+
+# ---- layout helpers --------------------------------------------------------
+
+
+def _dev_f32(t: torch.Tensor, what: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        raise Error(f"{what}: expected a torch tensor")
+    if not t.is_cuda:
+        raise Error(f"{what}: expected a CUDA tensor (no CPU path)")
+    if t.dtype != torch.float32:
+        t = t.float()
+    return t
+
+
+def _colmajor(X: torch.Tensor, what: str):
+    """(d, m) tensor -> (tensor, ld) with column-major storage."""
+    X = _dev_f32(X, what)
+    if X.dim() != 2:
+        raise DimensionError(f"{what}: expected a 2-D (d, m) tensor")
+    d, m = X.shape
+    if X.stride(0) == 1 and (m <= 1 or X.stride(1) >= max(d, 1)):
+        return X, max(X.stride(1), d, 1)
+    Xc = X.t().contiguous().t()
+    return Xc, max(d, 1)
+
+
+def _chain(V: torch.Tensor, what: str, d: int | None = None):
+    """(n, d) chain tensor -> (tensor, n, d, ld) as column-major d x n."""
+    V = _dev_f32(V, what)
+    if V.dim() != 2:
+        raise DimensionError(f"{what}: expected an (n, d) chain tensor")
+    n, dd = V.shape
+    if d is not None and n > 0 and dd != d:
+        raise DimensionError(f"{what}: vector length {dd} != dim {d}")
+    if n > 0 and not (V.stride(1) == 1 and V.stride(0) >= dd):
+        V = V.contiguous()
+    return V, n, (dd if n > 0 or d is None else d), max(V.stride(0) if n > 0 else dd, 1)
+
+
+def _new_out(d: int, m: int, like: torch.Tensor) -> torch.Tensor:
+    return torch.empty((m, d), dtype=torch.float32, device=like.device).t()
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else None
+
+
+# ---- FastH (fasth.hpp) ------------------------------------------------------
+
+
+class Tape:
+    """TapeForward (fasth.hpp:22-29): an opaque device record (compacted WY
+    blocks + per-block activations)."""
+
+    def __init__(self, ctx: Context, handle, output: torch.Tensor, d: int, n: int, m: int, b: int):
+        self.ctx, self.h = ctx, handle
+        self._output = output
+        self.d, self.n, self.m, self.block_width = d, n, m, b
+
+    def output(self) -> torch.Tensor:
+        return self._output
+
+    def block_count(self) -> int:
+        q = C.c_int()
+        _check(self.ctx.lib.fasth_tape_info(self.h, None, None, None, None, C.byref(q)))
+        return q.value
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.fasth_tape_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+@dataclass
+class BackwardResult:
+    """BackwardResult (fasth.hpp:31-34); grad_vectors is (n, d)."""
+    grad_input: torch.Tensor
+    grad_vectors: torch.Tensor
+
+
+def fasth_forward(V: torch.Tensor, X: torch.Tensor, block_width: int, *, ctx: Context | None = None,
+                  record: bool = True, out: torch.Tensor | None = None) -> Tape:
+    """fasth.hpp:40 — returns a Tape whose ``output()`` is H_1...H_n X."""
+    X, ldx = _colmajor(X, "fasth_forward: X")
+    d, m = X.shape
+    V, n, dv, ldv = _chain(V, "fasth_forward: V", d)
+    if n > 0 and dv != d:
+        raise DimensionError("fasth_forward: X row count != chain dim")
+    c = _ctx(ctx, X)
+    Y = _new_out(d, m, X) if out is None else out
+    ldy = max(Y.stride(1), d, 1)
+    h = C.c_void_p()
+    _check(c.lib.fasth_forward(c.h, _ptr(V), ldv, d, n, _ptr(X), ldx, m, int(block_width),
+                               _ptr(Y), ldy, C.byref(h) if record else None))
+    return Tape(c, h if record else None, Y, d, n, m, int(block_width))
+
+
+def fasth_backward(tape: Tape, G: torch.Tensor, *, want_vectors: bool = True) -> BackwardResult:
+    """fasth.hpp:69 — dX = U^T G and the Eq. (5) gradients of every vector."""
+    if tape.h is None:
+        raise Error("fasth_backward: tape was recorded with record=False")
+    G, ldg = _colmajor(G, "fasth_backward: grad_output")
+    if tuple(G.shape) != (tape.d, tape.m):
+        raise DimensionError("fasth_backward: grad_output shape mismatch")
+    c = tape.ctx
+    c.bind_stream()
+    dX = _new_out(tape.d, tape.m, G)
+    dV = torch.empty((tape.n, tape.d), dtype=torch.float32, device=G.device) if want_vectors else None
+    _check(c.lib.fasth_backward(c.h, tape.h, _ptr(G), ldg, _ptr(dX), max(tape.d, 1),
+                                _ptr(dV), max(tape.d, 1)))
+    return BackwardResult(dX, dV)
+
+
+def forward_backward_host(V, X, G, block_width: int, *, ctx: Context | None = None):
+    """Host-buffer drop-in for fasth_forward + fasth_backward
+    (``fasth_forward_backward_host``).  V: (n, d), X, G: (m, d) CPU float32
+    tensors (pin them for full bandwidth) — i.e. column-major d x m.
+    Returns (Y, dX, dV) as CPU tensors of the same layouts."""
+    c = ctx if ctx is not None else default_context()
+    c.bind_stream()
+    n, d = V.shape
+    m = X.shape[0]
+    Y = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
+    dX = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
+    dV = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    _check(c.lib.fasth_forward_backward_host(c.h, _ptr(V), d, n, _ptr(X), _ptr(G), m,
+                                             int(block_width), _ptr(Y), _ptr(dX), _ptr(dV)))
+    return Y, dX, dV
+
+
+# ---- SVD layer (svd_layer.hpp) ---------------------------------------------
+
+
+@dataclass
+class SvdParam:
+    """SvdParam (svd_layer.hpp:25-72): U (nu, out_dim), V (nv, in_dim),
+    sigma (min(out_dim, in_dim),)."""
+    out_dim: int
+    in_dim: int
+    U: torch.Tensor
+    V: torch.Tensor
+    sigma: torch.Tensor
+
+    def min_dim(self) -> int:
+        return min(self.out_dim, self.in_dim)
+
+    def validate(self):
+        if self.U.shape[0] and self.U.shape[1] != self.out_dim or \
+                self.V.shape[0] and self.V.shape[1] != self.in_dim:
+            raise DimensionError("SvdParam: chain dims inconsistent")
+        if self.sigma.numel() != self.min_dim():
+            raise DimensionError("SvdParam: sigma length != min(out_dim, in_dim)")
+
+    def _c(self) -> _lib.SvdParamC:
+        self.validate()
+        self.U = _dev_f32(self.U, "SvdParam.U").contiguous()
+        self.V = _dev_f32(self.V, "SvdParam.V").contiguous()
+        self.sigma = _dev_f32(self.sigma, "SvdParam.sigma").contiguous()
+        return _lib.SvdParamC(self.out_dim, self.in_dim, self.U.shape[0], self.V.shape[0],
+                              _ptr(self.U), self.out_dim, _ptr(self.V), self.in_dim,
+                              _ptr(self.sigma))
+
+
+@dataclass
+class SvdGradients:
+    """SvdGradients (svd_layer.hpp:74-79)."""
+    grad_U_vectors: torch.Tensor
+    grad_V_vectors: torch.Tensor
+    grad_sigma: torch.Tensor
+    grad_input: torch.Tensor
+
+
+class SvdTape:
+    """SvdTape (svd_layer.hpp:83-86), opaque."""
+
+    def __init__(self, ctx, handle, m):
+        self.ctx, self.h, self.m = ctx, handle, m
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.fasth_svd_tape_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def svd_forward(p: SvdParam, X: torch.Tensor, block_width: int, *, ctx: Context | None = None):
+    """svd_layer.hpp:106 — returns (Y, tape), Y = U (Sigma (V^T X))."""
+    X, ldx = _colmajor(X, "svd_forward: X")
+    if X.shape[0] != p.in_dim:
+        raise DimensionError(f"svd_forward: X has {X.shape[0]} rows, in_dim {p.in_dim}")
+    pc = p._c()
+    c = _ctx(ctx, X)
+    m = X.shape[1]
+    Y = _new_out(p.out_dim, m, X)
+    h = C.c_void_p()
+    _check(c.lib.fasth_svd_forward(c.h, C.byref(pc), _ptr(X), ldx, m, int(block_width), _ptr(Y),
+                                   max(p.out_dim, 1), C.byref(h)))
+    return Y, SvdTape(c, h, m)
+
+
+def svd_backward(p: SvdParam, tape: SvdTape, G: torch.Tensor) -> SvdGradients:
+    """svd_layer.hpp:122."""
+    G, ldg = _colmajor(G, "svd_backward: grad_output")
+    if tuple(G.shape) != (p.out_dim, tape.m):
+        raise DimensionError("svd_backward: grad_output shape mismatch")
+    pc = p._c()
+    c = tape.ctx
+    c.bind_stream()
+    dev = G.device
+    dX = _new_out(p.in_dim, tape.m, G)
+    dU = torch.empty((p.U.shape[0], p.out_dim), dtype=torch.float32, device=dev)
+    dV = torch.empty((p.V.shape[0], p.in_dim), dtype=torch.float32, device=dev)
+    ds = torch.empty(p.min_dim(), dtype=torch.float32, device=dev)
+    _check(c.lib.fasth_svd_backward(c.h, C.byref(pc), tape.h, _ptr(G), ldg, _ptr(dX),
+                                    max(p.in_dim, 1), _ptr(dU), max(p.out_dim, 1), _ptr(dV),
+                                    max(p.in_dim, 1), _ptr(ds)))
+    return SvdGradients(dU, dV, ds, dX)
+
+
+def svd_step(p: SvdParam, g: SvdGradients, eta: float, *, clamp_epsilon: float | None = None,
+             inplace: bool = False, ctx: Context | None = None) -> SvdParam:
+    """svd_layer.hpp:158 (optionally fused with clamp_sigma, :196)."""
+    pc = p._c()
+    if g.grad_U_vectors.shape != p.U.shape or g.grad_V_vectors.shape != p.V.shape or \
+            g.grad_sigma.numel() != p.sigma.numel():
+        raise DimensionError("svd_step: gradient shapes do not match parameter")
+    c = _ctx(ctx, p.sigma)
+    out = p if inplace else SvdParam(p.out_dim, p.in_dim, torch.empty_like(p.U),
+                                     torch.empty_like(p.V), torch.empty_like(p.sigma))
+    dU = g.grad_U_vectors.contiguous()
+    dV = g.grad_V_vectors.contiguous()
+    _check(c.lib.fasth_svd_step(c.h, C.byref(pc), _ptr(dU), max(p.out_dim, 1), _ptr(dV),
+                                max(p.in_dim, 1), _ptr(g.grad_sigma.contiguous()), float(eta),
+                                -1.0 if clamp_epsilon is None else float(clamp_epsilon),
+                                _ptr(out.U), max(p.out_dim, 1), _ptr(out.V), max(p.in_dim, 1),
+                                _ptr(out.sigma)))
+    return out
+
+
+def clamp_sigma(p: SvdParam, epsilon: float, *, ctx: Context | None = None) -> SvdParam:
+    """svd_layer.hpp:196."""
+    c = _ctx(ctx, p.sigma)
+    s = _dev_f32(p.sigma, "sigma").contiguous()
+    out = torch.empty_like(s)
+    _check(c.lib.fasth_clamp_sigma(c.h, _ptr(s), s.numel(), float(epsilon), _ptr(out)))
+    return SvdParam(p.out_dim, p.in_dim, p.U, p.V, out)
+
+
+def _sigma_op(fn_name, p: SvdParam, X, block_width, ctx):
+    X, ldx = _colmajor(X, fn_name)
+    pc = p._c()
+    c = _ctx(ctx, X)
+    d, m = X.shape
+    Y = _new_out(d, m, X)
+    _check(getattr(c.lib, fn_name)(c.h, C.byref(pc), _ptr(X), ldx, m, int(block_width), _ptr(Y),
+                                   max(d, 1)))
+    return Y
+
+
+def apply_inverse(p: SvdParam, X, block_width: int, *, ctx=None):
+    """matops.hpp:69 — W^{-1} X = V Sigma^{-1} U^T X."""
+    return _sigma_op("fasth_apply_inverse", p, X, block_width, ctx)
+
+
+def apply_exponential(p: SvdParam, X, block_width: int, *, ctx=None):
+    """matops.hpp:98 — e^W X for the symmetric form (empty V chain)."""
+    return _sigma_op("fasth_apply_exponential", p, X, block_width, ctx)
+
+
+def apply_cayley(p: SvdParam, X, block_width: int, *, ctx=None):
+    """matops.hpp:107 — (I - W)(I + W)^{-1} X for the symmetric form."""
+    return _sigma_op("fasth_apply_cayley", p, X, block_width, ctx)
+
+
+def log_abs_det(p: SvdParam, *, ctx=None) -> float:
+    """matops.hpp:57 — sum ln|sigma_i| (square parameters)."""
+    pc = p._c()
+    c = _ctx(ctx, p.sigma)
+    out = C.c_double()
+    _check(c.lib.fasth_log_abs_det(c.h, C.byref(pc), C.byref(out)))
+    return out.value

@@ -1,0 +1,156 @@
+"""CPU suite: pin the oracle to the reference, and check the device
+algorithm's closed forms (tests/algo_model.py) against it.
+
+* oracle/fasth_oracle.c (the C restatement) vs golden vectors produced by the
+  unmodified reference (tests/golden/make_golden.py), tol 1e-12;
+* the live reference build (oracle/_ref) vs the restatement, plus the
+  reference's own verify() suite, when the build is present;
+* reference known-answer tests (test_wy.cpp:27-45, test_dense_core.cpp:26-42);
+* finite differences (test_support.hpp:66-77) on the restatement;
+* the kernels' algebra (UT form on raw vectors, blocked dV) vs the oracle.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Port, Ref, relative_error as rel
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+G = np.load(os.path.join(HERE, "golden", "fasth_golden.npz"))
+META = json.load(open(os.path.join(HERE, "golden", "fasth_golden.json")))
+
+
+def case(name):
+    return {k.split("/", 1)[1]: G[k] for k in G.files if k.startswith(name + "/")}
+
+
+@pytest.fixture(scope="module")
+def port():
+    return Port()
+
+
+@pytest.fixture(scope="module")
+def ref():
+    try:
+        return Ref()
+    except Exception as e:  # no reference build on this machine
+        pytest.skip(f"oracle/_ref unavailable: {e}")
+
+
+@pytest.mark.parametrize("name", ["cfg1", "ragged", "n1", "b1", "bn", "m1", "oddb"])
+def test_port_fasth_vs_reference_golden(port, name):
+    g, b = case(name), META[name]["b"]
+    Y, dX, dV = port.fasth_fwd_bwd(g["V"], g["X"], g["G"], b)
+    assert rel(Y, g["Y"]) < 1e-12
+    assert rel(dX, g["dX"]) < 1e-12
+    assert rel(dV, g["dV"]) < 1e-12
+
+
+def test_port_sequential_vs_reference_golden(port):
+    g = case("cfg1")
+    Y, dX, dV = port.sequential_fwd_bwd(g["V"], g["X"], g["G"])
+    assert rel(Y, g["Y_seq"]) < 1e-12 and rel(dX, g["dX_seq"]) < 1e-12 and rel(dV, g["dV_seq"]) < 1e-12
+    # the reference's blocked and sequential paths agree (test_fasth.cpp:95-111)
+    assert rel(g["dV"], g["dV_seq"]) < 1e-10
+
+
+def test_known_answers(port):
+    g = case("kat_wy1")  # W = Y = (0.6, 0.8)
+    W, Y = port.wy_compact(g["V"])
+    assert np.allclose(W, [[0.6, 0.8]]) and np.allclose(Y, [[0.6, 0.8]])
+    assert np.allclose(W, g["W"], atol=1e-15)
+    g = case("kat_wy2")
+    W, Y = port.wy_compact(g["V"])
+    assert np.allclose(W, g["W"], atol=1e-15) and np.allclose(Y, g["Y"], atol=1e-15)
+    g = case("kat_e1")
+    assert np.allclose(port.chain_apply(g["V"], g["X"]), np.diag([-1.0, 1.0, 1.0]))
+    g = case("kat_swap")
+    assert np.allclose(port.chain_apply(g["V"], g["X"]), [[0.0], [-1.0]])
+    g = case("wy48")
+    W, Y = port.wy_compact(g["V"])
+    assert rel(W, g["W"]) < 1e-13 and rel(Y, g["Y"]) < 1e-13
+
+
+@pytest.mark.parametrize("name", ["svd8", "svd6x4", "svd4x6", "svd64"])
+def test_port_svd_vs_reference_golden(port, name):
+    g, meta = case(name), META[name]
+    Y, dX, dU, dV, ds = port.svd_fwd_bwd(g["U"], g["V"], g["sigma"], g["X"], g["G"], meta["b"],
+                                         meta["out"], meta["in"])
+    for got, key in ((Y, "Y"), (dX, "dX"), (dU, "dU"), (dV, "dV"), (ds, "dsigma")):
+        assert rel(got, g[key]) < 1e-12, key
+    Uo, Vo, so = port.svd_step(g["U"], g["V"], g["sigma"], dU, dV, ds, meta["eta"], meta["eps"])
+    assert rel(Uo, g["U_step"]) < 1e-12 and rel(Vo, g["V_step"]) < 1e-12
+    assert rel(so, g["sigma_step"]) < 1e-12
+
+
+def test_port_matops_vs_reference_golden(port):
+    g = case("inverse32")
+    assert rel(port.matop(0, g["U"], g["V"], g["sigma"], g["X"], 6), g["Y"]) < 1e-12
+    assert abs(port.log_abs_det(g["sigma"]) - g["logdet"][0]) < 1e-12
+    for name, kind in (("exp32", 1), ("cayley32", 2)):
+        g = case(name)
+        assert rel(port.matop(kind, g["U"], np.zeros((0, 32)), g["sigma"], g["X"], 6), g["Y"]) < 1e-12
+
+
+def test_port_errors(port):
+    from oracle.oracle import OracleError
+    V = np.random.default_rng(0).standard_normal((4, 4))
+    V[1] = 0
+    with pytest.raises(OracleError) as e:
+        port.fasth_fwd_bwd(V, np.ones((4, 2)), np.ones((4, 2)), 2)
+    assert e.value.kind == "DegenerateVectorError"
+    with pytest.raises(OracleError) as e:
+        port.log_abs_det(np.array([1.0, 0.0]))
+    assert e.value.kind == "SingularMatrixError"
+
+
+def test_port_finite_differences(port):
+    """test_fasth.cpp:75-93 / test_support.hpp:66-77 (central FD, h = 1e-5)."""
+    rng = np.random.default_rng(131)
+    d, n, m = 10, 10, 3
+    V, X, Gm = rng.standard_normal((n, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    _, _, dV = port.fasth_fwd_bwd(V, X, Gm, 5)
+    h = 1e-5
+    for k in range(n):
+        for c in range(d):
+            Vp, Vm = V.copy(), V.copy()
+            Vp[k, c] += h
+            Vm[k, c] -= h
+            fd = (np.sum(Gm * port.chain_apply(Vp, X)) - np.sum(Gm * port.chain_apply(Vm, X))) / (2 * h)
+            assert abs(dV[k, c] - fd) <= max(1e-8, 1e-6 * abs(fd))
+
+
+def test_ref_live_agrees_with_port(port, ref):
+    for seed, (d, n, m, b) in enumerate([(64, 64, 32, 8), (784, 784, 32, 32), (50, 33, 7, 9)]):
+        V, X, Gm = ref.gen_chain(seed, d, n, m)
+        a = ref.fasth_fwd_bwd(V, X, Gm, b)
+        c = port.fasth_fwd_bwd(V, X, Gm, b)
+        assert max(rel(x, y) for x, y in zip(a, c)) < 1e-12
+
+
+def test_ref_verify_suite(ref):
+    passed, total = ref.verify()
+    assert passed == total == 10
+
+
+def test_ref_generators_are_the_bench_workload(ref):
+    """bench.hpp:117-134: op=mul draws V, then X, then G from mt19937_64(seed + d)."""
+    V, X, Gm = ref.gen_mul(0, 64, 32)
+    g = case("cfg1")
+    assert np.array_equal(V, g["V"]) and np.array_equal(X, g["X"]) and np.array_equal(Gm, g["G"])
+
+
+# ---- the kernels' algebra, in f64, against the oracle ------------------------
+
+@pytest.mark.parametrize("d,n,m,b", [(64, 64, 32, 8), (20, 17, 4, 6), (128, 128, 8, 100),
+                                     (96, 40, 5, 7), (16, 16, 3, 1)])
+def test_device_algorithm_model_vs_oracle(port, d, n, m, b):
+    from tests.algo_model import fwd_bwd
+    rng = np.random.default_rng(d + n + m + b)
+    V, X, Gm = rng.standard_normal((n, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = port.fasth_fwd_bwd(V, X, Gm, b)
+    got = fwd_bwd(V, X, Gm, b)
+    for a, w in zip(got, want):
+        assert rel(a, w) < 1e-11
