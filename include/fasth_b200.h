@@ -71,8 +71,24 @@ fasth_status fasth_ctx_set_check(fasth_ctx ctx, int mode);
 fasth_status fasth_ctx_check(fasth_ctx ctx);
 /* Number of CUDA kernels this context has launched so far. */
 int64_t fasth_ctx_launch_count(fasth_ctx ctx);
+/* Timing mode: bracket every kernel launch with CUDA events on the context
+ * stream (for per-kernel roofline figures; off by default).  Turning it on
+ * or off clears the accumulated times. */
+fasth_status fasth_ctx_set_timing(fasth_ctx ctx, int on);
+/* Accumulated per-kernel device time as text lines "name total_ms launches".
+ * Returns the length written (truncated to buflen), -1 on bad arguments. */
+int fasth_ctx_kernel_times(fasth_ctx ctx, char* buf, int buflen);
 /* Release cached device memory held by the context's pool. */
 fasth_status fasth_ctx_trim(fasth_ctx ctx);
+
+/* Device buffers from the context's pool and stream-ordered copies, so host
+ * code (the C++ mirror, language bindings) needs no CUDA headers.
+ * fasth_copy kinds: 0 host->device, 1 device->host, 2 device->device.
+ * Copies are asynchronous on the context stream; fasth_ctx_synchronize waits. */
+fasth_status fasth_device_alloc(fasth_ctx ctx, int64_t bytes, void** out);
+fasth_status fasth_device_free(fasth_ctx ctx, void* ptr);
+fasth_status fasth_copy(fasth_ctx ctx, void* dst, const void* src, int64_t bytes, int kind);
+fasth_status fasth_ctx_synchronize(fasth_ctx ctx);
 
 /* ---- FastH ---------------------------------------------------------------
  * fasth_forward  replaces  TapeForward fasth_forward(const HouseholderChain&,

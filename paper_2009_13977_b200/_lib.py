@@ -35,6 +35,12 @@ SIGNATURES = {
     "fasth_ctx_check": (C.c_int, [VP]),
     "fasth_ctx_launch_count": (I64, [VP]),
     "fasth_ctx_trim": (C.c_int, [VP]),
+    "fasth_device_alloc": (C.c_int, [VP, I64, C.POINTER(VP)]),
+    "fasth_device_free": (C.c_int, [VP, VP]),
+    "fasth_copy": (C.c_int, [VP, VP, VP, I64, C.c_int]),
+    "fasth_ctx_synchronize": (C.c_int, [VP]),
+    "fasth_ctx_set_timing": (C.c_int, [VP, C.c_int]),
+    "fasth_ctx_kernel_times": (C.c_int, [VP, C.c_char_p, C.c_int]),
     "fasth_forward": (C.c_int, [VP, VP, I64, C.c_int, C.c_int, VP, I64, C.c_int, C.c_int, VP, I64,
                                 C.POINTER(VP)]),
     "fasth_backward": (C.c_int, [VP, VP, VP, I64, VP, I64, VP, I64]),

@@ -111,11 +111,47 @@ struct fasth_ctx_s {
         counters_len = len;
         return FASTH_OK;
     }
-    fasth_status launched(cudaError_t e, const char* what) {
+    // Launch bookkeeping: counts kernels and, in timing mode, brackets each
+    // launch with CUDA events on the context stream (bench.py's per-kernel
+    // roofline timing).
+    bool timing = false;
+    struct Timed {
+        std::string name;
+        cudaEvent_t start, stop;
+    };
+    std::vector<Timed> pending;
+    std::map<std::string, std::pair<double, int64_t>> kernel_ms;
+    template <typename F>
+    fasth_status timed(F&& launch, const char* what) {
+        cudaEvent_t a = nullptr, b = nullptr;
+        if (timing) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+            cudaEventRecord(a, stream);
+        }
+        cudaError_t e = launch();
+        if (timing) {
+            cudaEventRecord(b, stream);
+            pending.push_back({what, a, b});
+        }
         if (e != cudaSuccess)
             return fail(FASTH_ERR_CUDA, "%s launch failed: %s", what, cudaGetErrorString(e));
         ++launches;
         return FASTH_OK;
+    }
+    void collect_timing() {
+        for (auto& t : pending) {
+            float ms = 0.f;
+            if (cudaEventSynchronize(t.stop) == cudaSuccess &&
+                cudaEventElapsedTime(&ms, t.start, t.stop) == cudaSuccess) {
+                auto& acc = kernel_ms[t.name];
+                acc.first += ms;
+                acc.second += 1;
+            }
+            cudaEventDestroy(t.start);
+            cudaEventDestroy(t.stop);
+        }
+        pending.clear();
     }
     // Report latched device errors (after a stream sync) and clear them.
     fasth_status harvest() {
@@ -146,7 +182,7 @@ struct fasth_tape_s {
     fasth_ctx ctx = nullptr;
     Plan plan;
     int m = 0, b_user = 0;
-    int C = 0, WC = 0, ngroups = 0;
+    int C = 0, WC = 0, ngroups = 0, nstg = 3;
     float* tapeA = nullptr;  // activations per block
     float* zf = nullptr;
     float* tapeG = nullptr;  // gradient per block (backward scratch)
@@ -167,10 +203,12 @@ namespace {
 
 void free_plan(fasth_ctx c, Plan& p) {
     c->release(p.Vbl);
+    c->release(p.Wf);
+    c->release(p.Wb);
     c->release(p.Tt);
-    c->release(p.gram);
-    p.Vbl = p.Tt = nullptr;
-    p.gram = nullptr;
+    c->release(p.Sf);
+    c->release(p.Sb);
+    p.Vbl = p.Wf = p.Wb = p.Tt = p.Sf = p.Sb = nullptr;
 }
 
 void free_tape(fasth_tape t) {
@@ -197,25 +235,31 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int n, 
     p.d = d;
     p.n = n;
     const int b = std::min(std::max(b_user, 1), n);  // fasth.hpp:52
-    p.b = std::min(b, kMaxBS);  // wider blocks run as 64-wide sub-blocks (same product)
+    // Wider blocks run as 64-wide (32-wide when d is large, to keep the chain
+    // kernel's shared-memory stages in budget) sub-blocks: the same product.
+    p.b = std::min(b, d > 1536 ? 32 : kMaxBS);
     p.BS = next_pow2_min8(p.b);
     p.q = (n + p.b - 1) / p.b;
     p.d_pad = (d + 15) / 16 * 16;
     p.reversed = reversed;
     p.tag = tag;
-    const int cap = p.BS >= 64 ? 64 : 128;
-    int RS = std::max(1, (2 * c->num_sms + p.q - 1) / p.q);
-    RS = std::min(RS, p.d_pad / 16);
-    int rps = (p.d_pad + RS - 1) / RS;
-    rps = std::min((rps + 15) / 16 * 16, cap);
-    p.rps = rps;
-    p.RS = (p.d_pad + rps - 1) / rps;
-    TRY(c->alloc_n((size_t)p.q * p.d_pad * p.BS, &p.Vbl));
+    // Build cluster: CB CTAs per block split its rows; aim at ~one CTA per SM
+    // over all blocks, within the shared-memory budget.
+    int CB = 1;
+    while (CB < 16 && CB * p.q < c->num_sms) CB *= 2;
+    while (CB < 16 && build_smem_bytes(p.BS, p.d_pad / CB) > 220 * 1024) CB *= 2;
+    while (CB > 1 && p.d_pad / CB < 4) CB /= 2;
+    if (build_smem_bytes(p.BS, p.d_pad / CB) > 227 * 1024)
+        return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for block width %d", d, p.b);
+    p.CB = CB;
+    const size_t blk = (size_t)p.q * p.d_pad * (p.BS + 4);  // padded row pitch BS + 4
+    TRY(c->alloc_n(blk, &p.Vbl));
+    TRY(c->alloc_n(blk, &p.Wf));
+    TRY(c->alloc_n(blk, &p.Wb));
     TRY(c->alloc_n((size_t)p.q * p.BS * p.BS, &p.Tt));
-    TRY(c->alloc_n((size_t)p.q * p.RS * p.BS * p.BS, &p.gram));
-    TRY(c->ensure_counters(p.q));
-    p.counter = c->counters;
-    TRY(c->launched(launch_build(p, V, ldv, c->err_d, c->stream), "wy_build"));
+    TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sf));
+    TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sb));
+    TRY(c->timed([&] { return launch_build(p, V, ldv, c->err_d, c->stream); }, "wy_build"));
     *out = p;
     return FASTH_OK;
 }
@@ -237,6 +281,37 @@ fasth_status copy_cols(fasth_ctx c, const float* src, int64_t lds, float* dst, i
     return FASTH_OK;
 }
 
+// Debug aid (FASTH_TRACE=<prefix>): record the sweep's per-phase clock64
+// stamps and dump them to <prefix>.<what>.bin (int32 nctas, int32 q, then
+// nctas*(q+1)*8 int64).  Synchronises; never used on the measured path.
+fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int C, int WC, const char* what) {
+    const char* prefix = getenv("FASTH_TRACE");
+    if (!prefix) {
+        a.trace = nullptr;
+        return c->timed([&] { return launch_sweep(a, C, WC, c->num_sms, c->stream); }, what);
+    }
+    const int nctas = C * ((a.m + WC - 1) / WC);
+    const size_t n = (size_t)nctas * (a.q + 1) * 8;
+    long long* tr = nullptr;
+    CU(cudaMalloc(&tr, n * sizeof(long long)));
+    CU(cudaMemsetAsync(tr, 0, n * sizeof(long long), c->stream));
+    a.trace = tr;
+    fasth_status s = c->timed([&] { return launch_sweep(a, C, WC, c->num_sms, c->stream); }, what);
+    a.trace = nullptr;
+    std::vector<long long> h(n);
+    CU(cudaMemcpyAsync(h.data(), tr, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(tr);
+    std::string path = std::string(prefix) + "." + (a.forward ? "fwd" : "bwd") + ".bin";
+    if (FILE* f = fopen(path.c_str(), "wb")) {
+        int hdr[2] = {nctas, a.q};
+        fwrite(hdr, sizeof(int), 2, f);
+        fwrite(h.data(), sizeof(long long), n, f);
+        fclose(f);
+    }
+    return s;
+}
+
 // Forward sweep through a built plan (Alg. 1 step 2).
 fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx, float* Y,
                          int64_t ldy, bool record) {
@@ -247,7 +322,9 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     }
     SweepArgs a{};
     a.Vbl = p.Vbl;
-    a.Tt = p.Tt;
+    a.Wbl = p.Wf;
+    a.Sbl = p.Sf;
+    a.nstg = t->nstg;
     a.d = p.d;
     a.d_pad = p.d_pad;
     a.m = t->m;
@@ -262,7 +339,7 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     a.ldo = ldy;
     a.tape = record ? t->tapeA : nullptr;
     a.zhat = record ? t->zf : nullptr;
-    return c->launched(launch_sweep(a, t->C, t->WC, c->num_sms, c->stream), "sweep(forward)");
+    return launch_traced_sweep(c, a, t->C, t->WC, "sweep(forward)");
 }
 
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
@@ -284,7 +361,9 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     }
     SweepArgs a{};
     a.Vbl = p.Vbl;
-    a.Tt = p.Tt;
+    a.Wbl = p.Wb;
+    a.Sbl = p.Sb;
+    a.nstg = t->nstg;
     a.d = p.d;
     a.d_pad = p.d_pad;
     a.m = t->m;
@@ -299,8 +378,7 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     a.ldo = lddx;
     a.tape = want_dv ? t->tapeG : nullptr;
     a.zhat = want_dv ? t->zb : nullptr;
-    fasth_status s = c->launched(launch_sweep(a, t->C, t->WC, c->num_sms, c->stream),
-                                 "sweep(backward)");
+    fasth_status s = launch_traced_sweep(c, a, t->C, t->WC, "sweep(backward)");
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
@@ -322,7 +400,7 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     v.zb = t->zb;
     v.dV = dV;
     v.lddv = lddv;
-    return c->launched(launch_dv(v, c->stream), "dv");
+    return c->timed([&] { return launch_dv(v, c->stream); }, "dv");
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
@@ -337,7 +415,7 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
         delete t;
         return s;
     }
-    t->C = pick_cluster(t->plan.d_pad, m, t->plan.BS, c->num_sms, &t->WC);
+    t->C = pick_cluster(t->plan.d_pad, m, t->plan.BS, c->num_sms, &t->WC, &t->nstg);
     t->ngroups = (m + t->WC - 1) / t->WC;
     *out = t;
     return FASTH_OK;
@@ -363,8 +441,7 @@ fasth_status apply_chain(fasth_ctx c, const float* V, int64_t ldv, int d, int n,
                          int m, int b, float* Y, int64_t ldy) {
     if (n == 0) {
         if (scale || n_valid < d)
-            return c->launched(launch_scale_rows(X, ldx, n_valid, scale, d, m, Y, ldy, 0, c->stream),
-                               "scale_rows");
+            return c->timed([&] { return launch_scale_rows(X, ldx, n_valid, scale, d, m, Y, ldy, 0, c->stream); }, "scale_rows");
         return copy_cols(c, X, ldx, Y, ldy, d, m);
     }
     fasth_tape t = nullptr;
@@ -458,6 +535,55 @@ fasth_status fasth_ctx_check(fasth_ctx c) {
 }
 
 int64_t fasth_ctx_launch_count(fasth_ctx c) { return c ? c->launches : 0; }
+
+fasth_status fasth_device_alloc(fasth_ctx c, int64_t bytes, void** out) {
+    if (!c || !out || bytes < 0) return fail(FASTH_ERR_INVALID, "fasth_device_alloc: bad argument");
+    return c->alloc((size_t)bytes, out);
+}
+
+fasth_status fasth_device_free(fasth_ctx c, void* ptr) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    c->release(ptr);
+    return FASTH_OK;
+}
+
+fasth_status fasth_copy(fasth_ctx c, void* dst, const void* src, int64_t bytes, int kind) {
+    if (!c || bytes < 0 || kind < 0 || kind > 2) return fail(FASTH_ERR_INVALID, "fasth_copy: bad argument");
+    if (bytes == 0) return FASTH_OK;
+    const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
+                             : kind == 1 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    CU(cudaMemcpyAsync(dst, src, (size_t)bytes, k, c->stream));
+    return FASTH_OK;
+}
+
+fasth_status fasth_ctx_synchronize(fasth_ctx c) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    CU(cudaStreamSynchronize(c->stream));
+    return FASTH_OK;
+}
+
+fasth_status fasth_ctx_set_timing(fasth_ctx c, int on) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    c->collect_timing();
+    c->timing = on != 0;
+    c->kernel_ms.clear();
+    return FASTH_OK;
+}
+
+int fasth_ctx_kernel_times(fasth_ctx c, char* buf, int buflen) {
+    if (!c || !buf || buflen <= 0) return -1;
+    c->collect_timing();
+    std::string out;
+    char line[160];
+    for (auto& kv : c->kernel_ms) {
+        snprintf(line, sizeof(line), "%s %.6f %lld\n", kv.first.c_str(), kv.second.first,
+                 (long long)kv.second.second);
+        out += line;
+    }
+    snprintf(buf, buflen, "%s", out.c_str());
+    return (int)out.size();
+}
 
 fasth_status fasth_ctx_trim(fasth_ctx c) {
     if (!c) return FASTH_OK;
@@ -610,9 +736,8 @@ fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const floa
             st->u->n_valid = st->k;
             s = run_forward(c, st->u, st->T1, p->in_dim, Y, ldy, tape != nullptr);
         } else {
-            s = c->launched(launch_scale_rows(st->T1, p->in_dim, st->k, p->sigma, p->out_dim, m, Y,
-                                              ldy, 0, c->stream),
-                            "scale_rows");
+            s = c->timed([&] { return launch_scale_rows(st->T1, p->in_dim, st->k, p->sigma, p->out_dim, m, Y,
+                                              ldy, 0, c->stream); }, "scale_rows");
         }
         if (s) break;
         s = c->finish();
@@ -658,18 +783,16 @@ fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd
         if (s) break;
         // dSigma (svd_layer.hpp:131-137)
         if (dsigma) {
-            s = c->launched(launch_dsigma(dT2, p->out_dim, st->T1, p->in_dim, k, m, dsigma,
-                                          c->stream),
-                            "dsigma");
+            s = c->timed([&] { return launch_dsigma(dT2, p->out_dim, st->T1, p->in_dim, k, m, dsigma,
+                                          c->stream); }, "dsigma");
             if (s) break;
         }
         // V^T leg on dT1 = Sigma dT2 (svd_layer.hpp:139-147), Sigma fused into the load
         if (st->v) {
             s = run_backward(c, st->v, dT2, p->out_dim, k, p->sigma, dX, lddx, dV, lddv);
         } else if (dX) {
-            s = c->launched(launch_scale_rows(dT2, p->out_dim, k, p->sigma, p->in_dim, m, dX, lddx,
-                                              0, c->stream),
-                            "scale_rows");
+            s = c->timed([&] { return launch_scale_rows(dT2, p->out_dim, k, p->sigma, p->in_dim, m, dX, lddx,
+                                              0, c->stream); }, "scale_rows");
         }
         if (s) break;
     } while (0);
@@ -701,14 +824,11 @@ fasth_status fasth_svd_step(fasth_ctx c, const fasth_svd_param* p, const float* 
     TRY(check_mat("svd_step: V_out", V_out, ldov, p->in_dim, p->nv));
     const int k = std::min(p->out_dim, p->in_dim);
     if (k && (!dsigma || !sigma_out)) return fail(FASTH_ERR_INVALID, "svd_step: null sigma");
-    TRY(c->launched(launch_step(p->U, p->ldu, dU, lddu, p->out_dim, p->nu, eta, U_out, ldou,
-                                c->err_d, 0, c->stream),
-                    "step(U)"));
-    TRY(c->launched(launch_step(p->V, p->ldv, dV, lddv, p->in_dim, p->nv, eta, V_out, ldov,
-                                c->err_d, 1, c->stream),
-                    "step(V)"));
-    TRY(c->launched(launch_sigma_step(p->sigma, dsigma, k, eta, clamp_eps, sigma_out, c->stream),
-                    "sigma_step"));
+    TRY(c->timed([&] { return launch_step(p->U, p->ldu, dU, lddu, p->out_dim, p->nu, eta, U_out, ldou,
+                                c->err_d, 0, c->stream); }, "step(U)"));
+    TRY(c->timed([&] { return launch_step(p->V, p->ldv, dV, lddv, p->in_dim, p->nv, eta, V_out, ldov,
+                                c->err_d, 1, c->stream); }, "step(V)"));
+    TRY(c->timed([&] { return launch_sigma_step(p->sigma, dsigma, k, eta, clamp_eps, sigma_out, c->stream); }, "sigma_step"));
     fasth_status s = c->finish();
     if (s == FASTH_ERR_DEGENERATE)  // svd_layer.hpp:177-178 wording
         return fail(s, "svd_step: update degenerates %s vector %d", c->last_chain == 1 ? "V" : "U",
@@ -721,8 +841,7 @@ fasth_status fasth_clamp_sigma(fasth_ctx c, const float* sigma, int k, float eps
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     if (!(epsilon >= 0.f && epsilon < 1.f))
         return fail(FASTH_ERR_INVALID, "clamp_sigma: epsilon outside [0, 1)");
-    TRY(c->launched(launch_sigma_step(sigma, nullptr, k, 0.f, epsilon, sigma_out, c->stream),
-                    "clamp_sigma"));
+    TRY(c->timed([&] { return launch_sigma_step(sigma, nullptr, k, 0.f, epsilon, sigma_out, c->stream); }, "clamp_sigma"));
     return c->finish();
 }
 
@@ -744,7 +863,7 @@ fasth_status sigma_op(fasth_ctx c, const fasth_svd_param* p, const float* X, int
     fasth_status s = c->alloc_n((size_t)d * std::max(m, 1), &t);
     do {
         if (s) break;
-        s = c->launched(launch_sigma_map(p->sigma, d, kind, f, c->err_d, c->stream), "sigma_map");
+        s = c->timed([&] { return launch_sigma_map(p->sigma, d, kind, f, c->err_d, c->stream); }, "sigma_map");
         if (s) break;
         if (c->check_mode == FASTH_CHECK_SYNC) {  // reference checks before any chain work
             s = c->harvest();
@@ -787,8 +906,7 @@ fasth_status fasth_log_abs_det(fasth_ctx c, const fasth_svd_param* p, double* ou
     TRY(check_param("log_abs_det", p));
     if (p->out_dim != p->in_dim)
         return fail(FASTH_ERR_DIMENSION, "log_abs_det: requires a square parameter");
-    TRY(c->launched(launch_logdet(p->sigma, p->out_dim, c->logdet_d, c->err_d, c->stream),
-                    "logdet"));
+    TRY(c->timed([&] { return launch_logdet(p->sigma, p->out_dim, c->logdet_d, c->err_d, c->stream); }, "logdet"));
     CU(cudaMemcpyAsync(out, c->logdet_d, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     fasth_status s = c->harvest();  // the value is host-visible: always synchronise
     if (s == FASTH_ERR_SINGULAR) return fail(s, "log_abs_det: zero singular value");

@@ -44,16 +44,20 @@ struct Plan {
     int reversed = 0;
     int tag = 0;  // error-report tag (0 = U / plain chain, 1 = V)
     float* Vbl = nullptr;
-    float* Tt = nullptr;
-    double* gram = nullptr;      // [q][RS][BS][BS] partial Gram
-    unsigned* counter = nullptr; // [q], self-resetting
-    int RS = 0, rps = 0;         // row splits of the build, rows per split
+    float* Wf = nullptr;         // [q][d_pad][BS]  V T~^T  (forward partials)
+    float* Wb = nullptr;         // [q][d_pad][BS]  V T~    (backward partials)
+    float* Sf = nullptr;         // [q][BS][BS+4]   Wf_i^T V_{i+1}  (forward look-ahead)
+    float* Sb = nullptr;         // [q][BS][BS+4]   Wb_i^T V_{i-1}  (backward look-ahead)
+    float* Tt = nullptr;         // [q][BS][BS]     T~ (diagnostics / tests)
+    int CB = 8;                  // build cluster size (CTAs per block)
 };
 
 struct SweepArgs {
-    const float* Vbl;
-    const float* Tt;
+    const float* Vbl;  // update operand  (X -= 2 V Z')
+    const float* Wbl;  // partial operand (Z' = W^T X): Wf forward, Wb backward
+    const float* Sbl;  // look-ahead corrections: Sf forward, Sb backward
     int d, d_pad, m, q, BS;
+    int nstg;             // prefetch stages (3, or 2 at large d)
     int forward;          // 1: Alg 1 step 2 (blocks q-1..0, T~), 0: Alg 2 step 1 (0..q-1, T~^T)
     const float* x_in;    // column-major, rows < n_valid are read
     int64_t ldx;
@@ -63,6 +67,7 @@ struct SweepArgs {
     int64_t ldo;
     float* tape;          // optional, see header comment
     float* zhat;          // optional [q][BS][m]
+    long long* trace;     // optional phase timestamps (FASTH_TRACE): [CTA][q+1][8]
 };
 
 struct DvArgs {
@@ -80,10 +85,11 @@ struct DvArgs {
 // wy_build.cu
 cudaError_t launch_build(const Plan& p, const float* V, int64_t ldv, ErrWord* err,
                          cudaStream_t s);
+size_t build_smem_bytes(int BS, int RB);
 // chain_sweep.cu
 cudaError_t launch_sweep(const SweepArgs& a, int C, int WC, int num_sms, cudaStream_t s);
-int pick_cluster(int d_pad, int m, int BS, int num_sms, int* WC);
-size_t sweep_smem_bytes(int C, int WC, int BS, int d_pad);
+int pick_cluster(int d_pad, int m, int BS, int num_sms, int* WC, int* nstg);
+size_t sweep_smem_bytes(int C, int WC, int BS, int d_pad, int nstg);
 // dv.cu
 cudaError_t launch_dv(const DvArgs& a, cudaStream_t s);
 // sigma_ops.cu

@@ -97,6 +97,19 @@ class Context:
     def check(self):
         _check(self.lib.fasth_ctx_check(self.h))
 
+    def set_timing(self, on: bool):
+        _check(self.lib.fasth_ctx_set_timing(self.h, 1 if on else 0))
+
+    def kernel_times(self) -> dict:
+        """{kernel: (total_ms, launches)} accumulated in timing mode."""
+        buf = C.create_string_buffer(1 << 16)
+        self.lib.fasth_ctx_kernel_times(self.h, buf, len(buf))
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, ms, cnt = line.rsplit(" ", 2)
+            out[name] = (float(ms), int(cnt))
+        return out
+
     @property
     def launch_count(self) -> int:
         return int(self.lib.fasth_ctx_launch_count(self.h))
