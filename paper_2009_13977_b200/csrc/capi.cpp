@@ -222,40 +222,41 @@ void free_tape(fasth_tape t) {
     delete t;
 }
 
-int next_pow2_min8(int x) {
-    int p = 8;
+int next_pow2_min16(int x) {
+    int p = 16;
     while (p < x) p <<= 1;
     return p;
 }
 
-// Build the compacted chain (Alg. 1 step 1) on the device.
-fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int b_user,
-                        int reversed, int tag, Plan* out) {
+// Internal block width: the reference's b clamped to [1, n] (fasth.hpp:52);
+// wider blocks run as 64-wide (32-wide when d is large, to keep the chain
+// kernel's shared-memory stages in budget) sub-blocks: the same product.
+int internal_b(int d, int n, int b_user) {
+    const int b = std::min(std::max(b_user, 1), n);
+    return std::min(b, d > 1536 ? 32 : kMaxBS);
+}
+
+// Build the compacted chain (Alg. 1 step 1) on the device, in the row
+// padding d_pad the chain geometry asks for.
+fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_pad, int cb, int n,
+                        int b_user, int reversed, int tag, Plan* out) {
     Plan p;
     p.d = d;
     p.n = n;
-    const int b = std::min(std::max(b_user, 1), n);  // fasth.hpp:52
-    // Wider blocks run as 64-wide (32-wide when d is large, to keep the chain
-    // kernel's shared-memory stages in budget) sub-blocks: the same product.
-    p.b = std::min(b, d > 1536 ? 32 : kMaxBS);
-    p.BS = next_pow2_min8(p.b);
+    p.b = internal_b(d, n, b_user);
+    p.BS = next_pow2_min16(p.b);
     p.q = (n + p.b - 1) / p.b;
-    p.d_pad = (d + 15) / 16 * 16;
+    p.d_pad = d_pad;
     p.reversed = reversed;
     p.tag = tag;
-    // Build cluster: CB CTAs per block split its rows; aim at ~one CTA per SM
-    // over all blocks, within the shared-memory budget.
-    int CB = 1;
-    while (CB < 16 && CB * p.q < c->num_sms) CB *= 2;
-    while (CB < 16 && build_smem_bytes(p.BS, p.d_pad / CB) > 220 * 1024) CB *= 2;
-    while (CB > 1 && p.d_pad / CB < 4) CB /= 2;
-    if (build_smem_bytes(p.BS, p.d_pad / CB) > 227 * 1024)
+    // Build cluster: the chain kernel's cluster size, so each build CTA owns
+    // the same 16-row-multiple slab the chain CTAs do.
+    p.CB = cb;
+    if (build_smem_bytes(p.BS, p.d_pad / p.CB) > 227 * 1024)
         return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for block width %d", d, p.b);
-    p.CB = CB;
-    const size_t blk = (size_t)p.q * p.d_pad * (p.BS + 4);  // padded row pitch BS + 4
-    TRY(c->alloc_n(blk, &p.Vbl));
-    TRY(c->alloc_n(blk, &p.Wf));
-    TRY(c->alloc_n(blk, &p.Wb));
+    TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldv(p.BS), &p.Vbl));
+    TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wf));
+    TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wb));
     TRY(c->alloc_n((size_t)p.q * p.BS * p.BS, &p.Tt));
     TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sf));
     TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sb));
@@ -284,19 +285,19 @@ fasth_status copy_cols(fasth_ctx c, const float* src, int64_t lds, float* dst, i
 // Debug aid (FASTH_TRACE=<prefix>): record the sweep's per-phase clock64
 // stamps and dump them to <prefix>.<what>.bin (int32 nctas, int32 q, then
 // nctas*(q+1)*8 int64).  Synchronises; never used on the measured path.
-fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int C, int WC, const char* what) {
+fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int WC, const char* what) {
     const char* prefix = getenv("FASTH_TRACE");
     if (!prefix) {
         a.trace = nullptr;
-        return c->timed([&] { return launch_sweep(a, C, WC, c->num_sms, c->stream); }, what);
+        return c->timed([&] { return launch_sweep(a, WC, c->stream); }, what);
     }
-    const int nctas = C * ((a.m + WC - 1) / WC);
+    const int nctas = a.C * ((a.m + WC - 1) / WC);
     const size_t n = (size_t)nctas * (a.q + 1) * 8;
     long long* tr = nullptr;
     CU(cudaMalloc(&tr, n * sizeof(long long)));
     CU(cudaMemsetAsync(tr, 0, n * sizeof(long long), c->stream));
     a.trace = tr;
-    fasth_status s = c->timed([&] { return launch_sweep(a, C, WC, c->num_sms, c->stream); }, what);
+    fasth_status s = c->timed([&] { return launch_sweep(a, WC, c->stream); }, what);
     a.trace = nullptr;
     std::vector<long long> h(n);
     CU(cudaMemcpyAsync(h.data(), tr, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
@@ -325,6 +326,7 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     a.Wbl = p.Wf;
     a.Sbl = p.Sf;
     a.nstg = t->nstg;
+    a.C = t->C;
     a.d = p.d;
     a.d_pad = p.d_pad;
     a.m = t->m;
@@ -339,7 +341,7 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     a.ldo = ldy;
     a.tape = record ? t->tapeA : nullptr;
     a.zhat = record ? t->zf : nullptr;
-    return launch_traced_sweep(c, a, t->C, t->WC, "sweep(forward)");
+    return launch_traced_sweep(c, a, t->WC, "sweep(forward)");
 }
 
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
@@ -364,6 +366,7 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     a.Wbl = p.Wb;
     a.Sbl = p.Sb;
     a.nstg = t->nstg;
+    a.C = t->C;
     a.d = p.d;
     a.d_pad = p.d_pad;
     a.m = t->m;
@@ -378,7 +381,7 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     a.ldo = lddx;
     a.tape = want_dv ? t->tapeG : nullptr;
     a.zhat = want_dv ? t->zb : nullptr;
-    fasth_status s = launch_traced_sweep(c, a, t->C, t->WC, "sweep(backward)");
+    fasth_status s = launch_traced_sweep(c, a, t->WC, "sweep(backward)");
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
@@ -410,13 +413,16 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     t->m = m;
     t->b_user = b;
     t->n_valid = d;
-    fasth_status s = build_plan(c, V, ldv, d, n, b, reversed, tag, &t->plan);
+    const SweepGeom G = pick_geometry(d, m, next_pow2_min16(internal_b(d, n, b)), c->num_sms);
+    t->C = G.C;
+    t->WC = G.WC;
+    t->nstg = G.nstg;
+    t->ngroups = (m + t->WC - 1) / t->WC;
+    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, &t->plan);
     if (s != FASTH_OK) {
         delete t;
         return s;
     }
-    t->C = pick_cluster(t->plan.d_pad, m, t->plan.BS, c->num_sms, &t->WC, &t->nstg);
-    t->ngroups = (m + t->WC - 1) / t->WC;
     *out = t;
     return FASTH_OK;
 }

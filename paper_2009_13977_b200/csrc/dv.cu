@@ -13,13 +13,14 @@
 //
 // where A = activations[i] (block output), G = dA[i] (its gradient) and
 // Z'f / Z'b are the reductions the forward / backward sweeps already
-// produced for the block (no extra pass over d).  Grid (row tiles, q): all
-// blocks and row tiles in parallel.  Batch columns are processed in chunks
-// of MC so any m works; dV goes straight into the caller's column-major
-// d x n buffer in chain order (un-reversed for the V^T leg,
-// svd_layer.hpp:150-151) with coalesced column writes.
+// produced for the block (no extra pass over d).  Both products run on the
+// tensor cores (mma.sync m16n8k8, 3xTF32).  Grid (row tiles, q): all blocks
+// and row tiles in parallel; batch columns in chunks of MC so any m works;
+// dV goes straight into the caller's column-major d x n buffer in chain
+// order (un-reversed for the V^T leg, svd_layer.hpp:150-151), coalesced.
 #include "device_prims.cuh"
 #include "fasth_internal.h"
+#include "mma_tf32.cuh"
 
 namespace fasthb {
 namespace {
@@ -28,49 +29,61 @@ constexpr int RT = 64;  // rows per CTA
 
 template <int BS>
 struct DvShape {
-    static constexpr int MC = BS >= 64 ? 32 : 64;       // batch columns per chunk
-    static constexpr int KA = 2 * MC;                    // A|G columns per chunk
-    static constexpr int LDA = KA + 4;                   // smem pitch of the A operand
-    static constexpr int LDZ = BS + 1;                   // smem pitch of Z'^T chunks
-    static constexpr int JT = BS >= 16 ? BS / 16 : 1;    // output columns per thread
-    static constexpr int RTH = RT * BS / (kThreads * JT);  // output rows per thread (4)
+    static constexpr int MC = 64;         // batch columns per chunk
+    static constexpr int KA = 2 * MC;     // A|G columns per chunk
+    static constexpr int LDA = KA + 4;    // A-operand pitch (== 4 mod 32: conflict-free)
+    static constexpr int LDZ = BS + 8;    // B-operand pitch (== 8 mod 32)
+    static constexpr int LDV = BS + 4;    // V rows (== Vbl pitch)
+    static constexpr int LDC = RT + 1;    // transposed output staging
+    static constexpr int TILES = (RT / 16) * (BS / 8);
+    static constexpr int TPW = (TILES + 7) / 8;  // tiles per warp (8 warps)
 };
 
 template <int BS>
 __global__ void __launch_bounds__(kThreads) dv_kernel(DvArgs a) {
     using S = DvShape<BS>;
-    constexpr int MC = S::MC, KA = S::KA, LDA = S::LDA, LDZ = S::LDZ, JT = S::JT, RTH = S::RTH;
+    constexpr int MC = S::MC, KA = S::KA, LDA = S::LDA, LDZ = S::LDZ, LDV = S::LDV, LDC = S::LDC;
+    constexpr int TPW = S::TPW;
     extern __shared__ __align__(16) float sm[];
-    float* Aop = sm;                         // [RT][LDA]    A | G rows of this chunk
-    float* Bop = Aop + RT * LDA;             // [KA][LDZ]    Z'b^T ; Z'f^T
-    float* Vr = Bop + KA * LDZ;              // [RT][BS+1]   V rows
-    float* Kp = Vr + RT * (BS + 1);          // [BS][LDZ]    2 K'
-    float* Ct = Kp + BS * LDZ;               // [BS][RT+1]   output, transposed
+    float* Aop = sm;                      // [RT][LDA]   A | G rows of this chunk
+    float* Bop = Aop + RT * LDA;          // [KA][LDZ]   Z'b^T ; Z'f^T
+    float* Vr = Bop + KA * LDZ;           // [RT][LDV]   V rows
+    float* Kp = Vr + RT * LDV;            // [BS][LDZ]   2 K' (Q first)
+    float* Ct = Kp + BS * LDZ;            // [BS][LDC]   output, transposed
 
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
     const int i = blockIdx.y;
     const int r0 = blockIdx.x * RT;
     const int m = a.m, WC = a.WC;
     const float* zf = a.zf + (size_t)i * BS * m;
     const float* zb = a.zb + (size_t)i * BS * m;
 
-    // thread tile: rows rt*RTH .. +RTH-1, columns jt*JT .. +JT-1
-    const int jt = tid % (BS / JT), rt = tid / (BS / JT);
-    float acc[RTH][JT];
+    // V rows for the final K-slice (needed only after the chunks)
+    const float* vb = a.Vbl + ((size_t)i * a.d_pad + r0) * LDV;
+    for (int idx = tid; idx < RT * LDV / 4; idx += kThreads) {
+        const bool ok = r0 + idx / (LDV / 4) < a.d_pad;
+        dev::cp_async16(Vr + idx * 4, ok ? vb + idx * 4 : a.Vbl, ok);
+    }
+
+    dev::Frag4 acc[TPW][2];  // [tile][main, correction]
 #pragma unroll
-    for (int u = 0; u < RTH; ++u)
+    for (int u = 0; u < TPW; ++u)
 #pragma unroll
-        for (int v = 0; v < JT; ++v) acc[u][v] = 0.f;
-    constexpr int KPT = (BS * BS + kThreads - 1) / kThreads;
-    float kacc[KPT];
+        for (int v = 0; v < 4; ++v) acc[u][0].v[v] = acc[u][1].v[v] = 0.f;
+    // Q tile of this warp (BS/16 x BS/8 tiles of 16x8; BS<=64 -> <= 32 tiles, 8 warps)
+    constexpr int QT = (BS / 16) * (BS / 8);
+    constexpr int QPW = (QT + 7) / 8;
+    dev::Frag4 qacc[QPW][2];
 #pragma unroll
-    for (int u = 0; u < KPT; ++u) kacc[u] = 0.f;
+    for (int u = 0; u < QPW; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) qacc[u][0].v[v] = qacc[u][1].v[v] = 0.f;
 
     for (int lc = 0; lc < m; lc += MC) {
         const int mc = min(MC, m - lc);
         __syncthreads();
-        // all of this chunk's loads in flight at once (cp.async):
-        // Z'b^T, Z'f^T: coalesced along l, conflict-free transposed store
+        // all of this chunk's loads in flight at once (cp.async)
         for (int idx = tid; idx < BS * MC; idx += kThreads) {
             const int j = idx / MC, l = idx - j * MC;
             const bool ok = l < mc;
@@ -78,8 +91,8 @@ __global__ void __launch_bounds__(kThreads) dv_kernel(DvArgs a) {
             dev::cp_async4(Bop + l * LDZ + j, zb + off, ok);
             dev::cp_async4(Bop + (MC + l) * LDZ + j, zf + off, ok);
         }
-        // A | G rows from the tapes ([q][ngroups][d_pad][WC], WC % 4 == 0).
-        // Columns of the last group beyond m hold zeros (the sweeps load
+        // A | G rows from the tapes ([q][ngroups][d_pad][WC], WC % 4 == 0);
+        // columns of the last group beyond m hold zeros (the sweeps load
         // zeros there), so whole float4s are safe to take.
         for (int idx = tid; idx < RT * (MC / 4); idx += kThreads) {
             const int r = idx / (MC / 4), l4 = (idx - r * (MC / 4)) * 4;
@@ -87,8 +100,8 @@ __global__ void __launch_bounds__(kThreads) dv_kernel(DvArgs a) {
             size_t off = 0;
             if (ok) {
                 const int gl = lc + l4;
-                const int g = gl / WC, c = gl - g * WC;
-                off = (((size_t)i * a.ngroups + g) * a.d_pad + r0 + r) * WC + c;
+                const int gg = gl / WC, c = gl - gg * WC;
+                off = (((size_t)i * a.ngroups + gg) * a.d_pad + r0 + r) * WC + c;
             }
             dev::cp_async16(Aop + r * LDA + l4, a.tapeA + off, ok);
             dev::cp_async16(Aop + r * LDA + MC + l4, a.tapeG + off, ok);
@@ -96,78 +109,100 @@ __global__ void __launch_bounds__(kThreads) dv_kernel(DvArgs a) {
         dev::cp_async_commit();
         dev::cp_async_wait_all();
         __syncthreads();
-        // K' partial: Q[k][j] - Q[j][k] over this chunk, k < j
+        // Q += Z'f Z'b^T over this chunk: A[k][l] = Bop[MC + l][k], B[l][j] = Bop[l][j]
 #pragma unroll
-        for (int u = 0; u < KPT; ++u) {
-            const int idx = tid + u * kThreads;
-            if (idx < BS * BS) {
-                const int k = idx / BS, j = idx - k * BS;
-                if (k < j) {
-                    float s = kacc[u];
-                    for (int l = 0; l < mc; ++l)
-                        s += Bop[(MC + l) * LDZ + k] * Bop[l * LDZ + j] -
-                             Bop[(MC + l) * LDZ + j] * Bop[l * LDZ + k];
-                    kacc[u] = s;
+        for (int u = 0; u < QPW; ++u) {
+            const int qt = warp + u * 8;
+            if (qt < QT) {
+                const int m0 = (qt / (BS / 8)) * 16, n0 = (qt % (BS / 8)) * 8;
+                for (int k0 = 0; k0 < MC; k0 += 8) {
+                    const float* fa = Bop + (MC + k0 + tq) * LDZ + m0 + g;
+                    const float av[4] = {fa[0], fa[8], fa[4 * LDZ], fa[4 * LDZ + 8]};
+                    const float bv[2] = {Bop[(k0 + tq) * LDZ + n0 + g], Bop[(k0 + tq + 4) * LDZ + n0 + g]};
+                    dev::mma3(qacc[u][0], qacc[u][1], av, bv);
                 }
             }
         }
         // [A | G] [Z'b^T ; Z'f^T]
-#pragma unroll 4
-        for (int kk = 0; kk < KA; ++kk) {
-            float bv[JT];
 #pragma unroll
-            for (int v = 0; v < JT; ++v) bv[v] = Bop[kk * LDZ + jt * JT + v];
-#pragma unroll
-            for (int u = 0; u < RTH; ++u) {
-                const float av = Aop[(rt * RTH + u) * LDA + kk];
-#pragma unroll
-                for (int v = 0; v < JT; ++v) acc[u][v] = fmaf(av, bv[v], acc[u][v]);
+        for (int u = 0; u < TPW; ++u) {
+            const int tile = warp + u * 8;
+            if (tile < S::TILES) {
+                const int rr = (tile / (BS / 8)) * 16, n0 = (tile % (BS / 8)) * 8;
+                for (int k0 = 0; k0 < KA; k0 += 8) {
+                    const float* ar = Aop + (rr + g) * LDA + k0 + tq;
+                    const float av[4] = {ar[0], ar[8 * LDA], ar[4], ar[8 * LDA + 4]};
+                    const float bv[2] = {Bop[(k0 + tq) * LDZ + n0 + g], Bop[(k0 + tq + 4) * LDZ + n0 + g]};
+                    dev::mma3(acc[u][0], acc[u][1], av, bv);
+                }
             }
         }
     }
-    // + V (2 K')
+    // K' = striu(Q - Q^T), times 2, into Kp[k][j]
+    __syncthreads();
 #pragma unroll
-    for (int u = 0; u < KPT; ++u) {
-        const int idx = tid + u * kThreads;
-        if (idx < BS * BS) {
-            const int k = idx / BS, j = idx - k * BS;
-            Kp[k * LDZ + j] = 2.f * kacc[u];
+    for (int u = 0; u < QPW; ++u) {
+        const int qt = warp + u * 8;
+        if (qt < QT) {
+            const int m0 = (qt / (BS / 8)) * 16, n0 = (qt % (BS / 8)) * 8;
+            float* q0 = Kp + (m0 + g) * LDZ + n0 + 2 * tq;
+            q0[0] = qacc[u][0].v[0] + qacc[u][1].v[0];
+            q0[1] = qacc[u][0].v[1] + qacc[u][1].v[1];
+            q0[8 * LDZ] = qacc[u][0].v[2] + qacc[u][1].v[2];
+            q0[8 * LDZ + 1] = qacc[u][0].v[3] + qacc[u][1].v[3];
         }
-    }
-    constexpr int LDB = BS + 4;
-    const float* vb = a.Vbl + ((size_t)i * a.d_pad + r0) * LDB;
-    for (int idx = tid; idx < RT * BS; idx += kThreads) {
-        const int r = idx / BS, c = idx - r * BS;
-        const bool ok = r0 + r < a.d_pad;
-        dev::cp_async4(Vr + r * (BS + 1) + c, ok ? vb + (size_t)r * LDB + c : a.Vbl, ok);
     }
     dev::cp_async_commit();
-    dev::cp_async_wait_all();
+    dev::cp_async_wait_all();  // V rows
     __syncthreads();
-#pragma unroll 4
-    for (int k = 0; k < BS; ++k) {
-        float bv[JT];
+    // in place: Kp[k][j] = 2 (Q[k][j] - Q[j][k]) for k < j, else 0.  Each
+    // thread reads both mirror entries before the barrier, then writes.
+    float kv[(BS * BS + kThreads - 1) / kThreads];
 #pragma unroll
-        for (int v = 0; v < JT; ++v) bv[v] = Kp[k * LDZ + jt * JT + v];
+    for (int u = 0; u < (BS * BS + kThreads - 1) / kThreads; ++u) {
+        const int idx = tid + u * kThreads;
+        float v = 0.f;
+        if (idx < BS * BS) {
+            const int k = idx / BS, j = idx - k * BS;
+            if (k < j) v = 2.f * (Kp[k * LDZ + j] - Kp[j * LDZ + k]);
+        }
+        kv[u] = v;
+    }
+    __syncthreads();
 #pragma unroll
-        for (int u = 0; u < RTH; ++u) {
-            const float vv = Vr[(rt * RTH + u) * (BS + 1) + k];
+    for (int u = 0; u < (BS * BS + kThreads - 1) / kThreads; ++u) {
+        const int idx = tid + u * kThreads;
+        if (idx < BS * BS) Kp[(idx / BS) * LDZ + idx % BS] = kv[u];
+    }
+    __syncthreads();
+    // + V (2 K')
 #pragma unroll
-            for (int v = 0; v < JT; ++v) acc[u][v] = fmaf(vv, bv[v], acc[u][v]);
+    for (int u = 0; u < TPW; ++u) {
+        const int tile = warp + u * 8;
+        if (tile < S::TILES) {
+            const int rr = (tile / (BS / 8)) * 16, n0 = (tile % (BS / 8)) * 8;
+#pragma unroll
+            for (int k0 = 0; k0 < BS; k0 += 8) {
+                const float* vr = Vr + (rr + g) * LDV + k0 + tq;
+                const float av[4] = {vr[0], vr[8 * LDV], vr[4], vr[8 * LDV + 4]};
+                const float bv[2] = {Kp[(k0 + tq) * LDZ + n0 + g], Kp[(k0 + tq + 4) * LDZ + n0 + g]};
+                dev::mma3(acc[u][0], acc[u][1], av, bv);
+            }
+            // stage -2 * result transposed: Ct[j][r]
+            const int j = n0 + 2 * tq, r = rr + g;
+            Ct[j * LDC + r] = -2.f * (acc[u][0].v[0] + acc[u][1].v[0]);
+            Ct[(j + 1) * LDC + r] = -2.f * (acc[u][0].v[1] + acc[u][1].v[1]);
+            Ct[j * LDC + r + 8] = -2.f * (acc[u][0].v[2] + acc[u][1].v[2]);
+            Ct[(j + 1) * LDC + r + 8] = -2.f * (acc[u][0].v[3] + acc[u][1].v[3]);
         }
     }
-    // stage transposed, then coalesced column writes
-#pragma unroll
-    for (int u = 0; u < RTH; ++u)
-#pragma unroll
-        for (int v = 0; v < JT; ++v) Ct[(jt * JT + v) * (RT + 1) + rt * RTH + u] = -2.f * acc[u][v];
     __syncthreads();
     for (int idx = tid; idx < BS * RT; idx += kThreads) {
         const int j = idx / RT, r = idx - j * RT;
         const int kc = i * a.b + j;
         if (j < a.b && kc < a.n && r0 + r < a.d) {
             const int col = a.reversed ? a.n - 1 - kc : kc;
-            a.dV[(int64_t)col * a.lddv + r0 + r] = Ct[j * (RT + 1) + r];
+            a.dV[(int64_t)col * a.lddv + r0 + r] = Ct[j * LDC + r];
         }
     }
 }
@@ -175,8 +210,8 @@ __global__ void __launch_bounds__(kThreads) dv_kernel(DvArgs a) {
 template <int BS>
 size_t dv_smem() {
     using S = DvShape<BS>;
-    return sizeof(float) * ((size_t)RT * S::LDA + (size_t)S::KA * S::LDZ + (size_t)RT * (BS + 1) +
-                            (size_t)BS * S::LDZ + (size_t)BS * (RT + 1));
+    return sizeof(float) * ((size_t)RT * S::LDA + (size_t)S::KA * S::LDZ + (size_t)RT * S::LDV +
+                            (size_t)BS * S::LDZ + (size_t)BS * S::LDC);
 }
 
 template <int BS>
@@ -198,7 +233,6 @@ cudaError_t launch_dv_t(const DvArgs& a, cudaStream_t s) {
 
 cudaError_t launch_dv(const DvArgs& a, cudaStream_t s) {
     switch (a.BS) {
-        case 8: return launch_dv_t<8>(a, s);
         case 16: return launch_dv_t<16>(a, s);
         case 32: return launch_dv_t<32>(a, s);
         case 64: return launch_dv_t<64>(a, s);

@@ -43,9 +43,9 @@ struct Plan {
     int q = 0, BS = 0, d_pad = 0;
     int reversed = 0;
     int tag = 0;  // error-report tag (0 = U / plain chain, 1 = V)
-    float* Vbl = nullptr;
-    float* Wf = nullptr;         // [q][d_pad][BS]  V T~^T  (forward partials)
-    float* Wb = nullptr;         // [q][d_pad][BS]  V T~    (backward partials)
+    float* Vbl = nullptr;        // [q][d_pad][BS+4]
+    float* Wf = nullptr;         // [q][d_pad][BS+8]  V T~^T  (forward partials)
+    float* Wb = nullptr;         // [q][d_pad][BS+8]  V T~    (backward partials)
     float* Sf = nullptr;         // [q][BS][BS+4]   Wf_i^T V_{i+1}  (forward look-ahead)
     float* Sb = nullptr;         // [q][BS][BS+4]   Wb_i^T V_{i-1}  (backward look-ahead)
     float* Tt = nullptr;         // [q][BS][BS]     T~ (diagnostics / tests)
@@ -57,6 +57,7 @@ struct SweepArgs {
     const float* Wbl;  // partial operand (Z' = W^T X): Wf forward, Wb backward
     const float* Sbl;  // look-ahead corrections: Sf forward, Sb backward
     int d, d_pad, m, q, BS;
+    int C;                // CTAs per cluster (rows split; d_pad / C is a multiple of 16)
     int nstg;             // prefetch stages (3, or 2 at large d)
     int forward;          // 1: Alg 1 step 2 (blocks q-1..0, T~), 0: Alg 2 step 1 (0..q-1, T~^T)
     const float* x_in;    // column-major, rows < n_valid are read
@@ -87,9 +88,14 @@ cudaError_t launch_build(const Plan& p, const float* V, int64_t ldv, ErrWord* er
                          cudaStream_t s);
 size_t build_smem_bytes(int BS, int RB);
 // chain_sweep.cu
-cudaError_t launch_sweep(const SweepArgs& a, int C, int WC, int num_sms, cudaStream_t s);
-int pick_cluster(int d_pad, int m, int BS, int num_sms, int* WC, int* nstg);
+struct SweepGeom {
+    int C = 1, RC = 16, d_pad = 16, WC = 8, nstg = 3;
+};
+cudaError_t launch_sweep(const SweepArgs& a, int WC, cudaStream_t s);
+SweepGeom pick_geometry(int d, int m, int BS, int num_sms);
 size_t sweep_smem_bytes(int C, int WC, int BS, int d_pad, int nstg);
+int sweep_ldw(int BS);  // row pitch of Wf / Wb blocks
+int sweep_ldv(int BS);  // row pitch of Vbl blocks and Sf / Sb
 // dv.cu
 cudaError_t launch_dv(const DvArgs& a, cudaStream_t s);
 // sigma_ops.cu

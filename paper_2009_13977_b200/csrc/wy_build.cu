@@ -10,23 +10,25 @@
 // fp32 reflection stays exactly a reflection).
 //
 // ONE launch builds all q blocks: one thread-block cluster of CB CTAs per
-// block, the CTAs splitting the block's rows.  Each CTA
-//   1. stages its rows of the block's vectors (coalesced column reads) and
-//      writes them into the blocked row-major layout the chain kernels
-//      stream with bulk copies (Vbl, row pitch BS + 4);
-//   2. accumulates its rows' partial Gram V^T V in f64 (exact products);
-//   3. cluster reduce-scatter/all-gather of the Gram over DSMEM (fixed order:
+// block (CB = the chain kernel's cluster size, so every CTA owns RB rows, a
+// multiple of 16).  Each CTA
+//   1. stages its rows of the block's vectors with cp.async and writes them
+//      in the blocked row-major layout the chain kernels stream (Vbl);
+//   2. accumulates its rows' partial Gram V^T V on the FP64 tensor cores
+//      (mma.sync m8n8k4 f64: exact fp32 products, f64 sums);
+//   3. cluster all-reduce of the Gram over DSMEM (fixed order:
 //      deterministic), degeneracy check against householder.hpp:15, :28;
 //   4. inverts the b x b triangle (f64, recursive 2x2 blocking with 8x8
 //      leaves) redundantly — cheaper than another round trip;
-//   5. writes its rows of Wf = V T~^T and Wb = V T~ (the chain kernels'
-//      partial-product operands, so T~ never sits on their critical path);
+//   5. writes its rows of Wf = V T~^T and Wb = V T~ (3xTF32 mma.sync), the
+//      chain kernels' partial-product operands;
 //   6. forms the look-ahead corrections of the pipelined chain,
 //         Sf_i = Wf_i^T V_{i+1}   (forward step after block i+1)
 //         Sb_i = Wb_i^T V_{i-1}   (backward step after block i-1)
-//      as a second cluster reduction (chain_sweep.cu explains their use).
+//      (3xTF32 mma.sync, second cluster reduction; chain_sweep.cu).
 #include "device_prims.cuh"
 #include "fasth_internal.h"
+#include "mma_tf32.cuh"
 
 namespace fasthb {
 namespace {
@@ -37,7 +39,7 @@ __device__ __forceinline__ int src_col(int k, int n, int reversed) {
 
 __device__ __forceinline__ double ld_dsmem_f64(uint32_t addr) {
     double v;
-    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr) : "memory");
+    asm("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void st_dsmem_f64(uint32_t addr, double v) {
@@ -45,7 +47,7 @@ __device__ __forceinline__ void st_dsmem_f64(uint32_t addr, double v) {
 }
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
     float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
@@ -53,7 +55,8 @@ __device__ __forceinline__ void st_dsmem_f32(uint32_t addr, float v) {
 }
 
 // Sum `n` values of `part` over the CB CTAs of the cluster into `out` of every
-// CTA (CTA r reduces the slice r*n/CB.. in fixed rank order, then pushes it).
+// CTA: CTA r reduces the slice r*n/CB.. in fixed rank order (all its remote
+// loads in flight together), then pushes it to every CTA.
 template <typename T>
 __device__ void cluster_allreduce(const T* part, T* out, int n, int CB, uint32_t rank) {
     dev::cluster_sync();
@@ -61,12 +64,19 @@ __device__ void cluster_allreduce(const T* part, T* out, int n, int CB, uint32_t
     const int lo = (int)rank * per, hi = min(n, lo + per);
     const uint32_t pa = dev::smem_u32(part), oa = dev::smem_u32(out);
     for (int e = lo + (int)threadIdx.x; e < hi; e += kThreads) {
-        T s = 0;
-        for (int c = 0; c < CB; ++c) {
-            const uint32_t ra = dev::mapa(pa + e * (uint32_t)sizeof(T), c);
-            if constexpr (sizeof(T) == 8) s += ld_dsmem_f64(ra);
-            else s += ld_dsmem_f32(ra);
+        T v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            v[c] = 0;
+            if (c < CB) {
+                const uint32_t ra = dev::mapa(pa + e * (uint32_t)sizeof(T), c);
+                if constexpr (sizeof(T) == 8) v[c] = ld_dsmem_f64(ra);
+                else v[c] = ld_dsmem_f32(ra);
+            }
         }
+        T s = 0;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) s += v[c];
         for (int c = 0; c < CB; ++c) {
             const uint32_t ra = dev::mapa(oa + e * (uint32_t)sizeof(T), c);
             if constexpr (sizeof(T) == 8) st_dsmem_f64(ra, s);
@@ -78,10 +88,10 @@ __device__ void cluster_allreduce(const T* part, T* out, int n, int CB, uint32_t
 
 // T~ = M^{-1}, M = diag(g) + 2 striu(G) (upper triangular), in f64, by
 // recursive 2x2 blocking: leaves of 8 solved by back-substitution (one lane
-// per column), then T_AB = -T_AA M_AB T_BB level by level.  G, T, tmp have
-// pitch BS + 1.
+// per column), then T_AB = -T_AA (2 G_AB) T_BB level by level.  G, T, tmp
+// have pitch BS + 1; rinv[r] = 1 / g_rr.
 template <int BS>
-__device__ void invert_upper(const double* G, double* T, double* tmp, int w) {
+__device__ void invert_upper(const double* G, const double* rinv, double* T, double* tmp, int w) {
     constexpr int LD = BS + 1;
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
@@ -99,7 +109,7 @@ __device__ void invert_upper(const double* G, double* T, double* tmp, int w) {
 #pragma unroll
                 for (int k = r + 1; k < 8; ++k)
                     if (k <= lane) acc = fma(G[gr * LD + leaf * 8 + k], col[k], acc);
-                const double inv = 1.0 / G[gr * LD + gr];
+                const double inv = rinv[gr];
                 col[r] = (r == lane) ? inv : (r < lane ? -2.0 * acc * inv : 0.0);
             }
 #pragma unroll
@@ -130,40 +140,35 @@ __device__ void invert_upper(const double* G, double* T, double* tmp, int w) {
     }
 }
 
-// Shared memory, with regions reused across phases:
-//   RA: partial Gram Gp (phase 1) -> Gram with pitch LD, Gld (phase 2) ->
-//       partial S, Sp (phase 3)
-//   RB_: reduced Gram G (phase 1) -> inversion scratch tmp (phase 2) ->
-//        reduced S, So (phase 3)
+// Shared memory.  Regions reused across phases:
+//   ra: partial Gram Gp (f64) -> Gram with pitch LD, Gld -> partial S, Sp
+//   rb: reduced Gram G (f64) -> inversion scratch tmp -> reduced S, So
 template <int BS>
 struct BuildSmem {
-    static constexpr int LD = BS + 1;
-    static constexpr size_t kRegion = (size_t)BS * LD * 8;  // >= BS*BS*8 and 2*BS*BS*4
-    size_t vs, ws, nb, vd, gp, g, gld, t, tmp, tf, tft, sp, so, total;
+    static constexpr int LD = BS + 1;   // f64 inversion pitch
+    static constexpr int LDV = BS + 4;  // V rows (== Vbl pitch)
+    static constexpr int LDN = BS + 8;  // W / neighbour rows (== Wf/Wb pitch), T~ (f32)
+    static constexpr size_t kRegion = (size_t)BS * LD * 8;
+    size_t ra, rb, t, rinv, tf, vs, ws, nb, total;
     __host__ __device__ explicit BuildSmem(int RB) {
         size_t o = 0;
-        vd = o;  o += (size_t)RB * (BS + 2) * 8;  // f64 copy of the rows (Gram)
-        gp = gld = sp = o;
-        o += kRegion;
-        g = tmp = so = o;
-        o += kRegion;
-        t = o;   o += kRegion;                // T~ (f64)
-        tf = o;  o += (size_t)BS * BS * 4;
-        tft = o; o += (size_t)BS * BS * 4;
-        vs = o;  o += (size_t)RB * LD * 4;    // V_i rows
-        ws = o;  o += (size_t)RB * LD * 4;    // W rows (Wf, then Wb)
-        nb = o;  o += (size_t)RB * LD * 4;    // neighbour block rows
+        ra = o;   o += kRegion;
+        rb = o;   o += kRegion;
+        t = o;    o += kRegion;
+        rinv = o; o += (size_t)BS * 8;
+        tf = o;   o += (size_t)BS * LDN * 4;
+        vs = o;   o += (size_t)RB * LDV * 4;
+        ws = o;   o += (size_t)RB * LDN * 4;
+        nb = o;   o += (size_t)RB * LDN * 4;
         total = o;
     }
 };
 
-// Stage rows [row0, row0+RB) of block `blk` (zero outside the chain) into
-// dst[r][j] with cp.async: all loads of the CTA in flight at once (coalesced
-// along rows of the column-major V).  Caller commits and waits.
-template <int BS>
+// rows [row0, row0+RB) of block `blk` (zero outside the chain) -> dst[r][j],
+// pitch LDP, with cp.async (all loads in flight); caller commits and waits.
+template <int BS, int LDP>
 __device__ void load_rows_async(float* dst, const float* __restrict__ V, int64_t ldv, const Plan& p,
                                 int blk, int row0, int RB) {
-    constexpr int LD = BS + 1;
     const int k0 = blk * p.b;
     const int w = (blk >= 0 && blk < p.q) ? min(p.b, p.n - k0) : 0;
     for (int idx = threadIdx.x; idx < RB * BS; idx += kThreads) {
@@ -171,123 +176,132 @@ __device__ void load_rows_async(float* dst, const float* __restrict__ V, int64_t
         const int gr = row0 + r;
         const bool ok = j < w && gr < p.d;
         const float* src = ok ? V + (int64_t)src_col(k0 + j, p.n, p.reversed) * ldv + gr : V;
-        dev::cp_async4(dst + r * LD + j, src, ok);
+        dev::cp_async4(dst + r * LDP + j, src, ok);
     }
 }
 
-// S = W^T N over this CTA's rows (BS x BS, K = RB), into Sp.
+// rows (pitch LDP in smem and in global) -> global, float4 at a time
+template <int LDP>
+__device__ void store_rows(float* dst, const float* src, int RB) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    for (int idx = threadIdx.x; idx < RB * LDP / 4; idx += kThreads) d4[idx] = s4[idx];
+}
+
+// W[RB x BS] = Vs[RB x BS] * B, B[k][j] = Tf[k][j] (tr = 0: W = V T~) or
+// Tf[j][k] (tr = 1: W = V T~^T); 3xTF32 tensor cores, 16x8 tiles per warp.
 template <int BS>
-__device__ void partial_wtn(const float* W, const float* N, float* Sp, int RB) {
-    constexpr int LD = BS + 1;
-    for (int idx = threadIdx.x; idx < BS * BS; idx += kThreads) {
-        const int j = idx / BS, k = idx - j * BS;
-        float s0 = 0.f, s1 = 0.f;
-        int r = 0;
-        for (; r + 1 < RB; r += 2) {
-            s0 = fmaf(W[r * LD + j], N[r * LD + k], s0);
-            s1 = fmaf(W[(r + 1) * LD + j], N[(r + 1) * LD + k], s1);
+__device__ void w_rows_mma(const float* Vs, const float* Tf, float* Ws, int RB, int tr) {
+    constexpr int LDV = BS + 4, LDN = BS + 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+    const int ntiles = (RB / 16) * (BS / 8);
+    for (int u = warp; u < ntiles; u += kThreads / 32) {
+        const int r0 = (u / (BS / 8)) * 16, n0 = (u % (BS / 8)) * 8;
+        dev::Frag4 m = {{0.f, 0.f, 0.f, 0.f}}, c = m;
+#pragma unroll
+        for (int k0 = 0; k0 < BS; k0 += 8) {
+            const float* v0 = Vs + (r0 + g) * LDV + k0 + tq;
+            const float av[4] = {v0[0], v0[8 * LDV], v0[4], v0[8 * LDV + 4]};
+            float bv[2];
+            if (tr) {
+                bv[0] = Tf[(n0 + g) * LDN + k0 + tq];
+                bv[1] = Tf[(n0 + g) * LDN + k0 + tq + 4];
+            } else {
+                bv[0] = Tf[(k0 + tq) * LDN + n0 + g];
+                bv[1] = Tf[(k0 + tq + 4) * LDN + n0 + g];
+            }
+            dev::mma3(m, c, av, bv);
         }
-        if (r < RB) s0 = fmaf(W[r * LD + j], N[r * LD + k], s0);
-        Sp[idx] = s0 + s1;
+        float* w0 = Ws + (r0 + g) * LDN + n0 + 2 * tq;
+        w0[0] = m.v[0] + c.v[0];
+        w0[1] = m.v[1] + c.v[1];
+        w0[8 * LDN] = m.v[2] + c.v[2];
+        w0[8 * LDN + 1] = m.v[3] + c.v[3];
     }
 }
 
-// W rows = V rows * M  (M = T~^T for Wf, T~ for Wb; row-major BS x BS).
+// Sp[BS x BS] = Ws^T Nb over this CTA's RB rows; 3xTF32 tensor cores.
 template <int BS>
-__device__ void w_rows(const float* Vs, const float* M, float* Ws, int RB) {
-    constexpr int LD = BS + 1;
-    for (int idx = threadIdx.x; idx < RB * BS; idx += kThreads) {
-        const int r = idx / BS, j = idx - r * BS;
-        float s0 = 0.f, s1 = 0.f;
-#pragma unroll 8
-        for (int k = 0; k < BS; k += 2) {
-            s0 = fmaf(Vs[r * LD + k], M[k * BS + j], s0);
-            s1 = fmaf(Vs[r * LD + k + 1], M[(k + 1) * BS + j], s1);
+__device__ void wtn_mma(const float* Ws, const float* Nb, float* Sp, int RB) {
+    constexpr int LDN = BS + 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
+    constexpr int ntiles = (BS / 16) * (BS / 8);
+    for (int u = warp; u < ntiles; u += kThreads / 32) {
+        const int m0 = (u / (BS / 8)) * 16, n0 = (u % (BS / 8)) * 8;
+        dev::Frag4 m = {{0.f, 0.f, 0.f, 0.f}}, c = m;
+        for (int k0 = 0; k0 < RB; k0 += 8) {
+            const float* w0 = Ws + (k0 + tq) * LDN + m0 + g;
+            const float av[4] = {w0[0], w0[8], w0[4 * LDN], w0[4 * LDN + 8]};
+            const float bv[2] = {Nb[(k0 + tq) * LDN + n0 + g], Nb[(k0 + tq + 4) * LDN + n0 + g]};
+            dev::mma3(m, c, av, bv);
         }
-        Ws[r * LD + j] = s0 + s1;
-    }
-}
-
-template <int BS>
-__device__ void store_rows(float* dst, const float* src, int row0, int RB, int d_pad) {
-    constexpr int LD = BS + 1, LDB = BS + 4;
-    for (int idx = threadIdx.x; idx < RB * LDB; idx += kThreads) {
-        const int r = idx / LDB, j = idx - r * LDB;
-        if (row0 + r < d_pad) dst[(size_t)(row0 + r) * LDB + j] = j < BS ? src[r * LD + j] : 0.f;
+        float* s0 = Sp + (m0 + g) * BS + n0 + 2 * tq;
+        s0[0] = m.v[0] + c.v[0];
+        s0[1] = m.v[1] + c.v[1];
+        s0[8 * BS] = m.v[2] + c.v[2];
+        s0[8 * BS + 1] = m.v[3] + c.v[3];
     }
 }
 
 template <int BS>
 __global__ void __launch_bounds__(kThreads, 1) build_kernel(Plan p, const float* __restrict__ V,
                                                              int64_t ldv, ErrWord* err) {
-    constexpr int LD = BS + 1;
+    using L_ = BuildSmem<BS>;
+    constexpr int LD = L_::LD, LDV = L_::LDV, LDN = L_::LDN;
     extern __shared__ __align__(16) unsigned char smem[];
     const int CB = p.CB;
     const int RB = p.d_pad / CB;
-    const BuildSmem<BS> L(RB);
-    double* Gp = reinterpret_cast<double*>(smem + L.gp);
-    double* G = reinterpret_cast<double*>(smem + L.g);
-    double* Gld = reinterpret_cast<double*>(smem + L.gld);
+    const L_ L(RB);
+    double* Gp = reinterpret_cast<double*>(smem + L.ra);
+    double* Gld = Gp;
+    float* Sp = reinterpret_cast<float*>(smem + L.ra);
+    double* G = reinterpret_cast<double*>(smem + L.rb);
+    double* tmp = G;
+    float* So = reinterpret_cast<float*>(smem + L.rb);
     double* T = reinterpret_cast<double*>(smem + L.t);
-    double* tmp = reinterpret_cast<double*>(smem + L.tmp);
-    float* Sp = reinterpret_cast<float*>(smem + L.sp);
-    float* So = reinterpret_cast<float*>(smem + L.so);
+    double* rinv = reinterpret_cast<double*>(smem + L.rinv);
     float* Tf = reinterpret_cast<float*>(smem + L.tf);
-    float* TfT = reinterpret_cast<float*>(smem + L.tft);
     float* Vs = reinterpret_cast<float*>(smem + L.vs);
     float* Ws = reinterpret_cast<float*>(smem + L.ws);
     float* Nb = reinterpret_cast<float*>(smem + L.nb);
 
     const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
     const uint32_t rank = dev::cluster_ctarank();
     const int i = (int)dev::cluster_id_x();
     const int row0 = (int)rank * RB;
     const int w = min(p.b, p.n - i * p.b);
-    const size_t boff = (size_t)i * p.d_pad * (BS + 4);
+    const size_t voff = ((size_t)i * p.d_pad + row0) * LDV;
+    const size_t woff = ((size_t)i * p.d_pad + row0) * LDN;
 
     // 1. this block's rows, and the next block's (for Sf), all in flight
-    load_rows_async<BS>(Vs, V, ldv, p, i, row0, RB);
-    load_rows_async<BS>(Nb, V, ldv, p, i + 1, row0, RB);
+    load_rows_async<BS, LDV>(Vs, V, ldv, p, i, row0, RB);
+    load_rows_async<BS, LDN>(Nb, V, ldv, p, i + 1, row0, RB);
     dev::cp_async_commit();
     dev::cp_async_wait_all();
     __syncthreads();
-    store_rows<BS>(p.Vbl + boff, Vs, row0, RB, p.d_pad);
-    // 2. partial Gram (upper incl. diagonal), f64: convert the rows once, then
-    //    2x2 register tiles (exact fp32 products, f64 accumulation)
-    constexpr int LDD = BS + 2;
-    double* Vd = reinterpret_cast<double*>(smem + L.vd);
-    for (int idx = tid; idx < RB * BS; idx += kThreads) {
-        const int r = idx / BS, j = idx - r * BS;
-        Vd[r * LDD + j] = (double)Vs[r * LD + j];
-    }
-    __syncthreads();
-    constexpr int NT2 = BS / 2;
-    for (int tile = tid; tile < NT2 * NT2; tile += kThreads) {
-        const int tj = tile / NT2, tk = tile - tj * NT2;
-        double a00 = 0, a01 = 0, a10 = 0, a11 = 0;
-        if (tj <= tk) {
+    store_rows<LDV>(p.Vbl + voff, Vs, RB);
+    // 2. partial Gram on the FP64 tensor cores (8x8 tiles, upper triangle)
+    for (int u = warp; u < (BS / 8) * (BS / 8); u += kThreads / 32) {
+        const int mi = u / (BS / 8), ni = u % (BS / 8);
+        double d0 = 0.0, d1 = 0.0;
+        if (mi <= ni) {
+            const float* va = Vs + tq * LDV + mi * 8 + g;
+            const float* vb = Vs + tq * LDV + ni * 8 + g;
 #pragma unroll 4
-            for (int r = 0; r < RB; ++r) {
-                const double2 x = *reinterpret_cast<const double2*>(Vd + r * LDD + 2 * tj);
-                const double2 y = *reinterpret_cast<const double2*>(Vd + r * LDD + 2 * tk);
-                a00 = fma(x.x, y.x, a00);
-                a01 = fma(x.x, y.y, a01);
-                a10 = fma(x.y, y.x, a10);
-                a11 = fma(x.y, y.y, a11);
-            }
+            for (int k0 = 0; k0 < RB; k0 += 4)
+                dev::dmma(d0, d1, (double)va[k0 * LDV], (double)vb[k0 * LDV]);
         }
-        const int j = 2 * tj, k = 2 * tk;
-        Gp[j * BS + k] = a00;
-        Gp[j * BS + k + 1] = a01;
-        Gp[(j + 1) * BS + k] = a10;
-        Gp[(j + 1) * BS + k + 1] = a11;
+        Gp[(mi * 8 + g) * BS + ni * 8 + 2 * tq] = d0;
+        Gp[(mi * 8 + g) * BS + ni * 8 + 2 * tq + 1] = d1;
     }
     // 3. cluster all-reduce of the Gram
     cluster_allreduce<double>(Gp, G, BS * BS, CB, rank);
-    if (rank == 0 && tid < w) {
-        const double g = G[tid * BS + tid];
-        if (!(g > 1e-30) || !isfinite(g)) {
-            atomicOr(&err->flags, isfinite(g) ? kErrDegenerate : kErrNonFinite);
+    if (tid < BS) {
+        const double gd = G[tid * BS + tid];
+        rinv[tid] = tid < w ? 1.0 / gd : 0.0;
+        if (rank == 0 && tid < w && (!(gd > 1e-30) || !isfinite(gd))) {
+            atomicOr(&err->flags, isfinite(gd) ? kErrDegenerate : kErrNonFinite);
             atomicMin(&err->index, src_col(i * p.b + tid, p.n, p.reversed));
             err->chain = p.tag;
         }
@@ -298,37 +312,36 @@ __global__ void __launch_bounds__(kThreads, 1) build_kernel(Plan p, const float*
         Gld[idx] = (j < w && k < w) ? G[j * BS + k] : 0.0;
     }
     __syncthreads();
-    invert_upper<BS>(Gld, T, tmp, w);
+    invert_upper<BS>(Gld, rinv, T, tmp, w);
     for (int idx = tid; idx < BS * BS; idx += kThreads) {
         const int r = idx / BS, c = idx - r * BS;
-        const float v = (float)T[r * LD + c];
-        Tf[idx] = v;          // T~[r][c]
-        TfT[c * BS + r] = v;  // T~^T
+        Tf[r * LDN + c] = (float)T[r * LD + c];
     }
     __syncthreads();
     if (rank == 0)
-        for (int idx = tid; idx < BS * BS; idx += kThreads) p.Tt[(size_t)i * BS * BS + idx] = Tf[idx];
+        for (int idx = tid; idx < BS * BS; idx += kThreads)
+            p.Tt[(size_t)i * BS * BS + idx] = Tf[(idx / BS) * LDN + idx % BS];
     // 5/6. Wf = V T~^T ; Sf_i = Wf^T V_{i+1}
-    w_rows<BS>(Vs, TfT, Ws, RB);
+    w_rows_mma<BS>(Vs, Tf, Ws, RB, 1);
     __syncthreads();
-    store_rows<BS>(p.Wf + boff, Ws, row0, RB, p.d_pad);
-    partial_wtn<BS>(Ws, Nb, Sp, RB);
+    store_rows<LDN>(p.Wf + woff, Ws, RB);
+    wtn_mma<BS>(Ws, Nb, Sp, RB);
     __syncthreads();
     // Wb = V T~ ; Sb_i = Wb^T V_{i-1}  (previous block's rows load meanwhile)
-    load_rows_async<BS>(Nb, V, ldv, p, i - 1, row0, RB);
+    load_rows_async<BS, LDN>(Nb, V, ldv, p, i - 1, row0, RB);
     dev::cp_async_commit();
-    w_rows<BS>(Vs, Tf, Ws, RB);
+    w_rows_mma<BS>(Vs, Tf, Ws, RB, 0);
     dev::cp_async_wait_all();
     __syncthreads();
-    store_rows<BS>(p.Wb + boff, Ws, row0, RB, p.d_pad);
-    partial_wtn<BS>(Ws, Nb, Sp + BS * BS, RB);
+    store_rows<LDN>(p.Wb + woff, Ws, RB);
+    wtn_mma<BS>(Ws, Nb, Sp + BS * BS, RB);
     cluster_allreduce<float>(Sp, So, 2 * BS * BS, CB, rank);
-    if (rank == 0)  // row pitch BS + 4: conflict-free row reads in the sweeps
-        for (int idx = tid; idx < BS * (BS + 4); idx += kThreads) {
-            const int j = idx / (BS + 4), k = idx - j * (BS + 4);
+    if (rank == 0)  // row pitch BS + 4 (the chain kernel's S pitch)
+        for (int idx = tid; idx < BS * LDV; idx += kThreads) {
+            const int j = idx / LDV, k = idx - j * LDV;
             const bool in = k < BS;
-            p.Sf[(size_t)i * BS * (BS + 4) + idx] = in ? So[j * BS + k] : 0.f;
-            p.Sb[(size_t)i * BS * (BS + 4) + idx] = in ? So[BS * BS + j * BS + k] : 0.f;
+            p.Sf[(size_t)i * BS * LDV + idx] = in ? So[j * BS + k] : 0.f;
+            p.Sb[(size_t)i * BS * LDV + idx] = in ? So[BS * BS + j * BS + k] : 0.f;
         }
 }
 
@@ -364,7 +377,6 @@ cudaError_t launch_build_t(const Plan& p, const float* V, int64_t ldv, ErrWord* 
 
 size_t build_smem_bytes(int BS, int RB) {
     switch (BS) {
-        case 8: return BuildSmem<8>(RB).total;
         case 16: return BuildSmem<16>(RB).total;
         case 32: return BuildSmem<32>(RB).total;
         default: return BuildSmem<64>(RB).total;
@@ -373,8 +385,8 @@ size_t build_smem_bytes(int BS, int RB) {
 
 cudaError_t launch_build(const Plan& p, const float* V, int64_t ldv, ErrWord* err,
                          cudaStream_t s) {
+    if (p.CB < 1 || p.CB > 16 || p.d_pad % p.CB || (p.d_pad / p.CB) % 16) return cudaErrorInvalidValue;
     switch (p.BS) {
-        case 8: return launch_build_t<8>(p, V, ldv, err, s);
         case 16: return launch_build_t<16>(p, V, ldv, err, s);
         case 32: return launch_build_t<32>(p, V, ldv, err, s);
         case 64: return launch_build_t<64>(p, V, ldv, err, s);
