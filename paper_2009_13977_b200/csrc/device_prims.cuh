@@ -26,6 +26,12 @@ __device__ __forceinline__ uint32_t cluster_id_x() {
     return r;
 }
 
+// Named barrier among `nthreads` threads (a subset of the CTA's warps).
+template <int ID>
+__device__ __forceinline__ void named_bar_sync(int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"n"(ID), "r"(nthreads) : "memory");
+}
+
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");

@@ -1,6 +1,8 @@
-"""Summarise FASTH_TRACE sweep dumps: mean cycles per phase per step.
-phases (chain_sweep.cu marks): 0 top, 1 after load wait, 2 after partial+push,
-3 after exchange wait, 4 after reduce (B), 5 after update (C), 6 end of step."""
+"""Summarise FASTH_TRACE sweep dumps: cycles per phase per step (chain_sweep.cu
+slots: 0 top, 1 A after load wait, 2 A done, 3 B after exchange wait,
+4 B done, 5 after barrier 1, 6 C done, 7 after barrier 2).  Slots 0-2,5-7
+are stamped by thread 0 (an A warp), 3-4 by the first B warp: all on the same
+SM clock."""
 import sys
 import numpy as np
 
@@ -8,22 +10,17 @@ import numpy as np
 def report(path):
     raw = open(path, "rb").read()
     nctas, q = np.frombuffer(raw[:8], dtype=np.int32)
-    tr = np.frombuffer(raw[8:], dtype=np.int64).reshape(nctas, q + 1, 8)
-    names = ["tape/top->loadwait", "partial+push", "exch wait", "reduce B", "update C", "tape+refill"]
+    tr = np.frombuffer(raw[8:], dtype=np.int64).reshape(nctas, q + 1, 8).astype(np.float64)
+    s = tr[:, :q, :]
     print(f"{path}: {nctas} CTAs, q={q}")
-    tot = tr[:, q - 1, 6] - tr[:, q, 1]
-    print(f"  prologue (L0) cycles: mean {np.mean(tr[:, q, 1] - tr[:, q, 0]):.0f}; steps total mean {np.mean(tot):.0f} "
-          f"-> {np.mean(tot) / q:.0f} cycles/step")
-    steps = tr[:, :q, :]
-    d = {}
-    d[names[0]] = steps[:, :-1, 1] - steps[:, :-1, 0]
-    d[names[1]] = steps[:, :-1, 2] - steps[:, :-1, 1]
-    d[names[2]] = steps[:, :, 3] - steps[:, :, 2]
-    d[names[3]] = steps[:, :, 4] - steps[:, :, 3]
-    d[names[4]] = steps[:, :, 5] - steps[:, :, 4]
-    d[names[5]] = steps[:, :, 6] - steps[:, :, 5]
-    for k, v in d.items():
-        print(f"  {k:22s} mean {v.mean():8.0f}  p50 {np.median(v):8.0f}  max {v.max():8.0f}")
+    print(f"  cycles/step (top to top): {np.mean(np.diff(s[:, :, 0], axis=1)):.0f}")
+    rows = [("A load wait", 1, 0, slice(0, q - 1)), ("A partial+push", 2, 1, slice(0, q - 1)),
+            ("B exch wait (from top)", 3, 0, slice(1, q)), ("B reduce+corr", 4, 3, slice(1, q)),
+            ("barrier1 (from A done)", 5, 2, slice(0, q - 1)), ("barrier1 (from B done)", 5, 4, slice(1, q)),
+            ("C update", 6, 5, slice(0, q)), ("barrier2+refill", 7, 6, slice(0, q))]
+    for name, k1, k0, sl in rows:
+        v = s[:, sl, k1] - s[:, sl, k0]
+        print(f"  {name:26s} mean {v.mean():7.0f}  p50 {np.median(v):7.0f}  max {v.max():7.0f}")
 
 
 for p in sys.argv[1:]:
