@@ -284,7 +284,7 @@ fasth_status copy_cols(fasth_ctx c, const float* src, int64_t lds, float* dst, i
 
 // Debug aid (FASTH_TRACE=<prefix>): record the sweep's per-phase clock64
 // stamps and dump them to <prefix>.<what>.bin (int32 nctas, int32 q, then
-// nctas*(q+1)*8 int64).  Synchronises; never used on the measured path.
+// nctas*(q+1)*16 int64).  Synchronises; never used on the measured path.
 fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int WC, const char* what) {
     const char* prefix = getenv("FASTH_TRACE");
     if (!prefix) {
@@ -292,7 +292,7 @@ fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int WC, const char* 
         return c->timed([&] { return launch_sweep(a, WC, c->stream); }, what);
     }
     const int nctas = a.C * ((a.m + WC - 1) / WC);
-    const size_t n = (size_t)nctas * (a.q + 1) * 8;
+    const size_t n = (size_t)nctas * (a.q + 1) * 16;
     long long* tr = nullptr;
     CU(cudaMalloc(&tr, n * sizeof(long long)));
     CU(cudaMemsetAsync(tr, 0, n * sizeof(long long), c->stream));

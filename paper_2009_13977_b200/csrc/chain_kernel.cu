@@ -43,7 +43,7 @@ namespace fasthb {
 namespace {
 
 constexpr int NSLOT = 4;  // all-to-all receive slots (see the WAR argument below)
-constexpr int NT = 256;   // threads per CTA
+constexpr int NT = 512;   // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int WC = 8;     // columns per cluster (one MMA N tile)
 
@@ -214,39 +214,40 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(SweepArgs a) {
             const float bv[2] = {Xs[(k0 + tq) * WC + g], Xs[(k0 + tq + 4) * WC + g]};
             dev::mma3(m0a, c0a, av, bv);
         }
+        if (a.trace && threadIdx.x == 0 && t > 0) a.trace[((size_t)blockIdx.x * (q + 1) + t - 1) * 16 + 8] = clock64();
         float4 v = make_float4((m0a.v[0] + m1a.v[0]) + (c0a.v[0] + c1a.v[0]),
                                (m0a.v[1] + m1a.v[1]) + (c0a.v[1] + c1a.v[1]),
                                (m0a.v[2] + m1a.v[2]) + (c0a.v[2] + c1a.v[2]),
                                (m0a.v[3] + m1a.v[3]) + (c0a.v[3] + c1a.v[3]));
         if (KS > 1) {
-            if (kc > 0) reinterpret_cast<float4*>(red)[(kc * MT + mt) * 32 + lane] = v;
+            // every chunk warp of this M tile forms the same sum (fixed
+            // order) and pushes it to its share of the destinations
+            reinterpret_cast<float4*>(red)[(kc * MT + mt) * 32 + lane] = v;
             dev::named_bar_sync<1>(NA * 32);
-            if (kc > 0) return;
+            v = reinterpret_cast<const float4*>(red)[mt * 32 + lane];
 #pragma unroll
-            for (int c = 1; c < KS; ++c) {  // fixed order
+            for (int c = 1; c < KS; ++c) {
                 const float4 p = reinterpret_cast<const float4*>(red)[(c * MT + mt) * 32 + lane];
                 v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
             }
         }
+        if (a.trace && threadIdx.x == 0 && t > 0) a.trace[((size_t)blockIdx.x * (q + 1) + t - 1) * 16 + 9] = clock64();
         const int slot = t % NSLOT;
-        // entries (m0+g, 2tq..2tq+1) and (m0+g+8, ...) of this CTA's partial
-        const uint32_t o0 = (uint32_t)(((slot * C + (int)rank) * ZN + (m0 + g) * WC + 2 * tq) * 4);
-        const uint32_t o8 = o0 + 8 * WC * 4;
+        // this lane's 4 fragment entries, contiguous in the receive slot
+        // ([slot][source CTA][M tile][lane][4]): one 16-byte push per peer
+        const uint32_t off = (uint32_t)((((slot * C + (int)rank) * MT + mt) * 32 + lane) * 16);
         const uint32_t bar = exb_local + slot * 8;
-        for (int dst = 0; dst < C; ++dst) {
-            const uint32_t rb = dev::mapa(bar, dst);
-            dev::st_async_f32x2(dev::mapa(zr_local + o0, dst), v.x, v.y, rb);
-            dev::st_async_f32x2(dev::mapa(zr_local + o8, dst), v.z, v.w, rb);
-        }
+        for (int dst = kc; dst < C; dst += KS)
+            dev::st_async_f32x4(dev::mapa(zr_local + off, dst), v.x, v.y, v.z, v.w, dev::mapa(bar, dst));
     };
 
     // debug phase trace (FASTH_TRACE): clock64 per phase.  Slots: 0 top,
     // 1 A start, 2 A done, 3 B after the exchange wait, 4 B done (slots 1-2
     // by thread 0 of warp 0, 3-4 by lane 0 of the first B warp), 5 after
     // barrier 1, 6 C done, 7 after barrier 2.
-    long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 8 : nullptr;
+    long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
     auto mark_by = [&](int who, int t, int k) {
-        if (trc && tid == who) trc[(size_t)t * 8 + k] = clock64();
+        if (trc && tid == who) trc[(size_t)t * 16 + k] = clock64();
     };
     auto mark = [&](int t, int k) { mark_by(0, t, k); };
     mark(q, 0);
@@ -296,12 +297,11 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(SweepArgs a) {
             // WAR safety of the slot: a peer pushes L_{t+4} into it only after
             // it has Z_{t+2}, which needs our L_{t+2}, pushed after this read.
             if (lane == 0 && warp == NA) dev::mbar_arrive_expect_tx(&ex_bar[slot], ex_bytes);
-            const float* zr = Zr + (size_t)slot * C * ZN + (m0 + g) * WC + 2 * tq;
+            const float* zr = Zr + (size_t)slot * C * ZN + ((warp - NA) * 32 + lane) * 4;
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-            for (int c = 0; c < C; ++c) {
-                const float2 p0 = *reinterpret_cast<const float2*>(zr + c * ZN);
-                const float2 p8 = *reinterpret_cast<const float2*>(zr + c * ZN + 8 * WC);
-                s0 += p0.x, s1 += p0.y, s2 += p8.x, s3 += p8.y;
+            for (int c = 0; c < C; ++c) {  // fixed order over the source CTAs
+                const float4 p = *reinterpret_cast<const float4*>(zr + c * ZN);
+                s0 += p.x, s1 += p.y, s2 += p.z, s3 += p.w;
             }
             const float z[4] = {s0 + (cm.v[0] + cc.v[0]), s1 + (cm.v[1] + cc.v[1]),
                                 s2 + (cm.v[2] + cc.v[2]), s3 + (cm.v[3] + cc.v[3])};
@@ -323,6 +323,45 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(SweepArgs a) {
         {
             const float* Vt = Vs + (size_t)st * RC * LDV;
             const float* Zc = Zb + (t & 1) * ZN;
+            if (TPW == 1 && 2 * RT <= NW) {
+                // two warps per row tile, each half of K; the upper half's
+                // product meets the resident tile through shared memory
+                if (warp < 2 * RT) {
+                    const int kh = warp < RT ? 0 : 1, rt = warp - kh * RT;
+                    const int r0 = rt * 16;
+                    float* t0 = tape_blk ? tape_blk + (r0 + g) * WC + 2 * tq : nullptr;
+                    if (kh == 0 && !a.forward && t0) {  // dA[i] = X^(t)
+                        *reinterpret_cast<float2*>(t0) = make_float2(xr[0][0], xr[0][1]);
+                        *reinterpret_cast<float2*>(t0 + 8 * WC) = make_float2(xr[0][2], xr[0][3]);
+                    }
+                    dev::Frag4 m = {{0.f, 0.f, 0.f, 0.f}}, cc = m;
+                    if (kh == 0) m = {{xr[0][0], xr[0][1], xr[0][2], xr[0][3]}};
+#pragma unroll
+                    for (int k0 = kh * (BS / 2); k0 < (kh + 1) * (BS / 2); k0 += 8) {
+                        const float* v0 = Vt + (r0 + g) * LDV + k0 + tq;
+                        const float av[4] = {v0[0], v0[8 * LDV], v0[4], v0[8 * LDV + 4]};
+                        const float bv[2] = {-2.f * Zc[(k0 + tq) * WC + g], -2.f * Zc[(k0 + tq + 4) * WC + g]};
+                        dev::mma3(m, cc, av, bv);
+                    }
+                    float4* hand = reinterpret_cast<float4*>(red) + rt * 32 + lane;
+                    if (kh == 1) *hand = make_float4(m.v[0] + cc.v[0], m.v[1] + cc.v[1], m.v[2] + cc.v[2], m.v[3] + cc.v[3]);
+                    dev::named_bar_sync<2>(2 * RT * 32);
+                    if (kh == 0) {
+                        const float4 p = *hand;
+                        xr[0][0] = (m.v[0] + cc.v[0]) + p.x;
+                        xr[0][1] = (m.v[1] + cc.v[1]) + p.y;
+                        xr[0][2] = (m.v[2] + cc.v[2]) + p.z;
+                        xr[0][3] = (m.v[3] + cc.v[3]) + p.w;
+                        float* x0 = Xs + (r0 + g) * WC + 2 * tq;
+                        *reinterpret_cast<float2*>(x0) = make_float2(xr[0][0], xr[0][1]);
+                        *reinterpret_cast<float2*>(x0 + 8 * WC) = make_float2(xr[0][2], xr[0][3]);
+                        if (a.forward && t0) {  // A_i = activations[i]
+                            *reinterpret_cast<float2*>(t0) = make_float2(xr[0][0], xr[0][1]);
+                            *reinterpret_cast<float2*>(t0 + 8 * WC) = make_float2(xr[0][2], xr[0][3]);
+                        }
+                    }
+                }
+            } else
 #pragma unroll
             for (int u = 0; u < TPW; ++u) {
                 const int rt = warp + u * NW;
