@@ -72,9 +72,11 @@ fasth_status fasth_ctx_check(fasth_ctx ctx);
 /* Number of CUDA kernels this context has launched so far. */
 int64_t fasth_ctx_launch_count(fasth_ctx ctx);
 /* Timing mode: bracket every kernel launch with CUDA events on the context
- * stream (for per-kernel roofline figures; off by default).  Turning it on
- * or off clears the accumulated times. */
-fasth_status fasth_ctx_set_timing(fasth_ctx ctx, int on);
+ * stream (for per-kernel roofline figures; off by default).  mode 1: events
+ * per launch, read and freed by fasth_ctx_kernel_times; mode 2: the events
+ * are kept (capture a CUDA graph in this mode, replay it, read the times
+ * after each replay: no host gaps).  Changing the mode clears the times. */
+fasth_status fasth_ctx_set_timing(fasth_ctx ctx, int mode);
 /* Accumulated per-kernel device time as text lines "name total_ms launches".
  * Returns the length written (truncated to buflen), -1 on bad arguments. */
 int fasth_ctx_kernel_times(fasth_ctx ctx, char* buf, int buflen);
@@ -109,6 +111,17 @@ fasth_status fasth_backward(fasth_ctx ctx, fasth_tape tape, const float* G, int6
 fasth_status fasth_tape_destroy(fasth_tape tape);
 /* Shape of a tape: any pointer may be NULL. q = number of WY blocks. */
 fasth_status fasth_tape_info(fasth_tape tape, int* d, int* n, int* m, int* block_width, int* q);
+
+/* The reference's call pair fasth_forward + fasth_backward (fasth.hpp:40, :69)
+ * as one call, for callers that hold the output gradient G when they start —
+ * the reference benchmark's op=mul step (bench.hpp:140-150: forward, then
+ * backward with a pre-drawn G).  Same results as the two calls; the forward
+ * and backward sweeps are independent once the WY blocks exist, so they run
+ * concurrently in one launch.  Y, dX: d x m; dV: d x n (may be NULL). */
+fasth_status fasth_forward_backward(fasth_ctx ctx, const float* V, int64_t ldv, int d, int n,
+                                    const float* X, int64_t ldx, const float* G, int64_t ldg,
+                                    int m, int block_width, float* Y, int64_t ldy, float* dX,
+                                    int64_t lddx, float* dV, int64_t lddv);
 
 /* Host-buffer form of the reference's call pair fasth_forward + fasth_backward
  * (fasth.hpp:40, :69): all pointers are HOST memory (pinned for full copy

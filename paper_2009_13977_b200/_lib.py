@@ -46,6 +46,8 @@ SIGNATURES = {
     "fasth_backward": (C.c_int, [VP, VP, VP, I64, VP, I64, VP, I64]),
     "fasth_tape_destroy": (C.c_int, [VP]),
     "fasth_tape_info": (C.c_int, [VP] + [C.POINTER(C.c_int)] * 5),
+    "fasth_forward_backward": (C.c_int, [VP, VP, I64, C.c_int, C.c_int, VP, I64, VP, I64, C.c_int,
+                                         C.c_int, VP, I64, VP, I64, VP, I64]),
     "fasth_forward_backward_host": (C.c_int, [VP, VP, C.c_int, C.c_int, VP, VP, C.c_int, C.c_int,
                                               VP, VP, VP]),
     "fasth_svd_forward": (C.c_int, [VP, C.POINTER(SvdParamC), VP, I64, C.c_int, C.c_int, VP, I64,

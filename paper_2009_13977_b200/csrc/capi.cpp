@@ -114,7 +114,7 @@ struct fasth_ctx_s {
     // Launch bookkeeping: counts kernels and, in timing mode, brackets each
     // launch with CUDA events on the context stream (bench.py's per-kernel
     // roofline timing).
-    bool timing = false;
+    int timing = 0;  // 0 off, 1 per launch, 2 persistent events (graph capture)
     struct Timed {
         std::string name;
         cudaEvent_t start, stop;
@@ -124,14 +124,19 @@ struct fasth_ctx_s {
     template <typename F>
     fasth_status timed(F&& launch, const char* what) {
         cudaEvent_t a = nullptr, b = nullptr;
+        // under stream capture only an "external" record becomes an event
+        // node that is timestamped at every replay
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (timing) cudaStreamIsCapturing(stream, &cap);
+        const unsigned rflags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
         if (timing) {
             cudaEventCreate(&a);
             cudaEventCreate(&b);
-            cudaEventRecord(a, stream);
+            cudaEventRecordWithFlags(a, stream, rflags);
         }
         cudaError_t e = launch();
         if (timing) {
-            cudaEventRecord(b, stream);
+            cudaEventRecordWithFlags(b, stream, rflags);
             pending.push_back({what, a, b});
         }
         if (e != cudaSuccess)
@@ -148,6 +153,17 @@ struct fasth_ctx_s {
                 acc.first += ms;
                 acc.second += 1;
             }
+            if (timing != 2) {
+                cudaEventDestroy(t.start);
+                cudaEventDestroy(t.stop);
+            }
+        }
+        if (timing != 2) pending.clear();
+    }
+    // mode 2 keeps the events (they are nodes of a captured graph that is
+    // replayed): each collect reads the last replay; release when done
+    void release_timing_events() {
+        for (auto& t : pending) {
             cudaEventDestroy(t.start);
             cudaEventDestroy(t.stop);
         }
@@ -183,6 +199,7 @@ struct fasth_tape_s {
     Plan plan;
     int m = 0, b_user = 0;
     int C = 0, WC = 0, ngroups = 0, nstg = 3;
+    int v2nstg = 0;  // > 0: packed stages + chain_v2.cu sweep (else chain_kernel.cu)
     float* tapeA = nullptr;  // activations per block
     float* zf = nullptr;
     float* tapeG = nullptr;  // gradient per block (backward scratch)
@@ -208,7 +225,9 @@ void free_plan(fasth_ctx c, Plan& p) {
     c->release(p.Tt);
     c->release(p.Sf);
     c->release(p.Sb);
-    p.Vbl = p.Wf = p.Wb = p.Tt = p.Sf = p.Sb = nullptr;
+    c->release(p.Pf);
+    c->release(p.Pb);
+    p.Vbl = p.Wf = p.Wb = p.Tt = p.Sf = p.Sb = p.Pf = p.Pb = nullptr;
 }
 
 void free_tape(fasth_tape t) {
@@ -239,7 +258,7 @@ int internal_b(int d, int n, int b_user) {
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row
 // padding d_pad the chain geometry asks for.
 fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_pad, int cb, int n,
-                        int b_user, int reversed, int tag, Plan* out) {
+                        int b_user, int reversed, int tag, bool packed, Plan* out) {
     Plan p;
     p.d = d;
     p.n = n;
@@ -255,12 +274,43 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
     if (build_smem_bytes(p.BS, p.d_pad / p.CB) > 227 * 1024)
         return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for block width %d", d, p.b);
     TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldv(p.BS), &p.Vbl));
-    TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wf));
-    TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wb));
     TRY(c->alloc_n((size_t)p.q * p.BS * p.BS, &p.Tt));
-    TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sf));
-    TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sb));
-    TRY(c->timed([&] { return launch_build(p, V, ldv, c->err_d, c->stream); }, "wy_build"));
+    if (packed) {
+        const size_t sf = stage_floats(p.d_pad / p.CB, p.BS);
+        TRY(c->alloc_n((size_t)p.q * p.CB * sf, &p.Pf));
+        TRY(c->alloc_n((size_t)p.q * p.CB * sf, &p.Pb));
+    } else {
+        TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wf));
+        TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wb));
+        TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sf));
+        TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sb));
+    }
+    if (packed && !getenv("FASTH_BUILD_V1") && build2_smem_bytes(p.BS, p.d_pad / p.CB) <= 227 * 1024) {
+        const char* prefix = getenv("FASTH_TRACE");
+        const size_t ntr = (size_t)p.q * p.CB * 8;
+        if (prefix) {
+            CU(cudaMalloc(&p.trace, ntr * sizeof(long long)));
+            CU(cudaMemsetAsync(p.trace, 0, ntr * sizeof(long long), c->stream));
+        }
+        fasth_status bs = c->timed([&] { return launch_build2(p, V, ldv, c->err_d, c->stream); }, "wy_build");
+        if (prefix) {
+            std::vector<long long> h(ntr);
+            CU(cudaMemcpyAsync(h.data(), p.trace, ntr * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaStreamSynchronize(c->stream));
+            cudaFree(p.trace);
+            p.trace = nullptr;
+            std::string path = std::string(prefix) + ".build.bin";
+            if (FILE* f = fopen(path.c_str(), "wb")) {
+                int hdr[2] = {p.q * p.CB, 8};
+                fwrite(hdr, sizeof(int), 2, f);
+                fwrite(h.data(), sizeof(long long), ntr, f);
+                fclose(f);
+            }
+        }
+        TRY(bs);
+    } else {
+        TRY(c->timed([&] { return launch_build(p, V, ldv, c->err_d, c->stream); }, "wy_build"));
+    }
     *out = p;
     return FASTH_OK;
 }
@@ -313,6 +363,80 @@ fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int WC, const char* 
     return s;
 }
 
+fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what) {
+    const char* prefix = getenv("FASTH_TRACE");
+    if (!prefix) {
+        a.trace = nullptr;
+        return c->timed([&] { return launch_sweep2(a, c->stream); }, what);
+    }
+    const int nctas = a.C * a.ngroups * a.ndir;
+    const size_t n = (size_t)nctas * (a.q + 1) * 16;
+    long long* tr = nullptr;
+    CU(cudaMalloc(&tr, n * sizeof(long long)));
+    CU(cudaMemsetAsync(tr, 0, n * sizeof(long long), c->stream));
+    a.trace = tr;
+    fasth_status s = c->timed([&] { return launch_sweep2(a, c->stream); }, what);
+    a.trace = nullptr;
+    std::vector<long long> h(n);
+    CU(cudaMemcpyAsync(h.data(), tr, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    cudaFree(tr);
+    std::string path = std::string(prefix) + "." + what + ".v2.bin";
+    if (FILE* f = fopen(path.c_str(), "wb")) {
+        int hdr[2] = {nctas, a.q};
+        fwrite(hdr, sizeof(int), 2, f);
+        fwrite(h.data(), sizeof(long long), n, f);
+        fclose(f);
+    }
+    return s;
+}
+
+SweepV2Args v2_args(fasth_tape t) {
+    const Plan& p = t->plan;
+    SweepV2Args a{};
+    a.ndir = 1;
+    a.d = p.d;
+    a.d_pad = p.d_pad;
+    a.m = t->m;
+    a.q = p.q;
+    a.BS = p.BS;
+    a.C = t->C;
+    a.nstg = t->v2nstg;
+    a.ngroups = t->ngroups;
+    return a;
+}
+
+SweepDirV2 v2_forward_dir(fasth_tape t, const float* X, int64_t ldx, float* Y, int64_t ldy, bool record) {
+    SweepDirV2 d{};
+    d.stage = t->plan.Pf;
+    d.x_in = X;
+    d.ldx = ldx;
+    d.n_valid = t->n_valid;
+    d.scale = t->scale;
+    d.x_out = Y;
+    d.ldo = ldy;
+    d.tape = record ? t->tapeA : nullptr;
+    d.zhat = record ? t->zf : nullptr;
+    d.forward = 1;
+    return d;
+}
+
+SweepDirV2 v2_backward_dir(fasth_tape t, const float* G, int64_t ldg, int g_valid, const float* g_scale,
+                           float* dx, int64_t lddx, bool want_dv) {
+    SweepDirV2 d{};
+    d.stage = t->plan.Pb;
+    d.x_in = G;
+    d.ldx = ldg;
+    d.n_valid = g_valid;
+    d.scale = g_scale;
+    d.x_out = dx;
+    d.ldo = lddx;
+    d.tape = want_dv ? t->tapeG : nullptr;
+    d.zhat = want_dv ? t->zb : nullptr;
+    d.forward = 0;
+    return d;
+}
+
 // Forward sweep through a built plan (Alg. 1 step 2).
 fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx, float* Y,
                          int64_t ldy, bool record) {
@@ -320,6 +444,11 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     if (record) {
         if (!t->tapeA) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeA));
         if (!t->zf) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zf));
+    }
+    if (t->v2nstg) {
+        SweepV2Args a = v2_args(t);
+        a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, record);
+        return launch_traced_sweep2(c, a, "sweep(forward)");
     }
     SweepArgs a{};
     a.Vbl = p.Vbl;
@@ -344,6 +473,8 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     return launch_traced_sweep(c, a, t->WC, "sweep(forward)");
 }
 
+fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv);
+
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
 fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, int g_valid,
                           const float* g_scale, float* dX, int64_t lddx, float* dV,
@@ -361,6 +492,12 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
         TRY(c->alloc_n((size_t)p.d * std::max(t->m, 1), &dx));
         lddx = p.d;
     }
+    fasth_status s;
+    if (t->v2nstg) {
+        SweepV2Args a = v2_args(t);
+        a.dir[0] = v2_backward_dir(t, G, ldg, g_valid, g_scale, dx, lddx, want_dv);
+        s = launch_traced_sweep2(c, a, "sweep(backward)");
+    } else {
     SweepArgs a{};
     a.Vbl = p.Vbl;
     a.Wbl = p.Wb;
@@ -381,10 +518,16 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     a.ldo = lddx;
     a.tape = want_dv ? t->tapeG : nullptr;
     a.zhat = want_dv ? t->zb : nullptr;
-    fasth_status s = launch_traced_sweep(c, a, t->WC, "sweep(backward)");
+    s = launch_traced_sweep(c, a, t->WC, "sweep(backward)");
+    }
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
+    return run_dv(c, t, dV, lddv);
+}
+
+fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv) {
+    const Plan& p = t->plan;
     DvArgs v{};
     v.Vbl = p.Vbl;
     v.d = p.d;
@@ -403,7 +546,41 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     v.zb = t->zb;
     v.dV = dV;
     v.lddv = lddv;
-    return c->timed([&] { return launch_dv(v, c->stream); }, "dv");
+    if (getenv("FASTH_DV_V1")) return c->timed([&] { return launch_dv(v, c->stream); }, "dv");
+    return c->timed([&] { return launch_dv2(v, c->stream); }, "dv");
+}
+
+// Both sweeps of one chain (X forward, G backward) and the gradients: one
+// sweep launch carrying both directions when the v2 kernel applies.
+fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx, float* Y,
+                                  int64_t ldy, const float* G, int64_t ldg, float* dX, int64_t lddx,
+                                  float* dV, int64_t lddv) {
+    const Plan& p = t->plan;
+    if (!t->v2nstg) {
+        TRY(run_forward(c, t, X, ldx, Y, ldy, true));
+        return run_backward(c, t, G, ldg, p.d, nullptr, dX, lddx, dV, lddv);
+    }
+    const bool want_dv = dV != nullptr;
+    if (!t->tapeA) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeA));
+    if (!t->zf) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zf));
+    if (want_dv) {
+        if (!t->tapeG) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeG));
+        if (!t->zb) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zb));
+    }
+    float* dx = dX;
+    if (!dx) {
+        TRY(c->alloc_n((size_t)p.d * std::max(t->m, 1), &dx));
+        lddx = p.d;
+    }
+    SweepV2Args a = v2_args(t);
+    a.ndir = 2;
+    a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, want_dv);
+    a.dir[1] = v2_backward_dir(t, G, ldg, p.d, nullptr, dx, lddx, want_dv);
+    fasth_status s = launch_traced_sweep2(c, a, "sweep(fwd+bwd)");
+    if (dx != dX) c->release(dx);
+    TRY(s);
+    if (!want_dv) return FASTH_OK;
+    return run_dv(c, t, dV, lddv);
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
@@ -413,12 +590,14 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     t->m = m;
     t->b_user = b;
     t->n_valid = d;
-    const SweepGeom G = pick_geometry(d, m, next_pow2_min16(internal_b(d, n, b)), c->num_sms);
+    const int BS = next_pow2_min16(internal_b(d, n, b));
+    const SweepGeom G = pick_geometry(d, m, BS, c->num_sms);
     t->C = G.C;
     t->WC = G.WC;
     t->nstg = G.nstg;
     t->ngroups = (m + t->WC - 1) / t->WC;
-    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, &t->plan);
+    t->v2nstg = getenv("FASTH_SWEEP_V1") ? 0 : sweep2_nstg(G.C, BS, G.d_pad);
+    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, t->v2nstg > 0, &t->plan);
     if (s != FASTH_OK) {
         delete t;
         return s;
@@ -569,10 +748,13 @@ fasth_status fasth_ctx_synchronize(fasth_ctx c) {
     return FASTH_OK;
 }
 
-fasth_status fasth_ctx_set_timing(fasth_ctx c, int on) {
-    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
-    c->collect_timing();
-    c->timing = on != 0;
+fasth_status fasth_ctx_set_timing(fasth_ctx c, int mode) {
+    if (!c || mode < 0 || mode > 2) return fail(FASTH_ERR_INVALID, "fasth_ctx_set_timing: bad argument");
+    if (c->timing == 2)
+        c->release_timing_events();
+    else
+        c->collect_timing();
+    c->timing = mode;
     c->kernel_ms.clear();
     return FASTH_OK;
 }
@@ -669,6 +851,34 @@ fasth_status fasth_tape_info(fasth_tape t, int* d, int* n, int* m, int* block_wi
     return FASTH_OK;
 }
 
+fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, int d, int n,
+                                    const float* X, int64_t ldx, const float* G, int64_t ldg,
+                                    int m, int block_width, float* Y, int64_t ldy, float* dX,
+                                    int64_t lddx, float* dV, int64_t lddv) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (d < 1) return fail(FASTH_ERR_DIMENSION, "fasth_forward: chain dim must be >= 1");
+    if (n < 0 || m < 0) return fail(FASTH_ERR_DIMENSION, "fasth_forward: negative shape");
+    TRY(check_mat("fasth_forward: V", V, ldv, d, n));
+    TRY(check_mat("fasth_forward: X", X, ldx, d, m));
+    TRY(check_mat("fasth_forward: Y", Y, ldy, d, m));
+    TRY(check_mat("fasth_backward: G", G, ldg, d, m));
+    if (dX) TRY(check_mat("fasth_backward: dX", dX, lddx, d, m));
+    if (dV) TRY(check_mat("fasth_backward: dV", dV, lddv, d, n));
+    if (n == 0 || m == 0) {  // the two-call path handles the degenerate shapes
+        fasth_tape t = nullptr;
+        TRY(fasth_forward(c, V, ldv, d, n, X, ldx, m, block_width, Y, ldy, &t));
+        fasth_status s = fasth_backward(c, t, G, ldg, dX, lddx, dV, lddv);
+        free_tape(t);
+        return s;
+    }
+    fasth_tape t = nullptr;
+    TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t));
+    fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);
+    free_tape(t);  // pool reuse is stream ordered
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
 fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int n,
                                          const float* X, const float* G, int m, int block_width,
                                          float* Y, float* dX, float* dV) {
@@ -690,9 +900,8 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
         if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
         if (nx) CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
         if (nx) CU(cudaMemcpyAsync(g, G, nx * 4, cudaMemcpyHostToDevice, c->stream));
-        s = fasth_forward(c, v, d, d, n, x, d, m, block_width, y, d, &t);
-        if (s != FASTH_OK) break;
-        s = fasth_backward(c, t, g, d, dx, d, n ? dv : nullptr, d);
+        s = fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d,
+                                   n ? dv : nullptr, d);
         if (s != FASTH_OK) break;
         if (nx) CU(cudaMemcpyAsync(Y, y, nx * 4, cudaMemcpyDeviceToHost, c->stream));
         if (nx) CU(cudaMemcpyAsync(dX, dx, nx * 4, cudaMemcpyDeviceToHost, c->stream));

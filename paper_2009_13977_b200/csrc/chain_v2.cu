@@ -1,0 +1,530 @@
+// Sequential block chain, v2: north_star subsystem (3) (forward sweep,
+// Alg. 1 step 2, fasth.hpp:58-59 / wy_apply wy.hpp:104-133) and the sweep of
+// subsystem (4) (backward step 1, fasth.hpp:82-86 / wy_apply_transpose
+// wy.hpp:137-146) — optionally BOTH in one launch (fasth_forward_backward:
+// the two sweeps are independent once the WY blocks exist).
+//
+// Same algebra as chain_kernel.cu (look-ahead pipelined UT-form steps),
+//     Z_t     = sum_c L_t^c - 2 S_t Z_{t-1},      L_t = W_t^T X^(t-1) (per CTA rows)
+//     X^(t+1) = X^(t) - 2 V_t Z_t
+// re-laid out for instruction count, which is what bounds a 25-step chain on
+// 7-CTA clusters (ncu: HMMA was 2.7% of the v1 kernel's instructions):
+//   * one bulk copy per step per CTA: the build kernel writes each CTA's
+//     W | V | S rows of a step contiguously, columns permuted into mma.sync
+//     fragment order (fasth_internal.h), so every A-operand fragment is one
+//     or two 16-byte shared loads with compile-time offsets;
+//   * the 3xTF32 split is 3 ops per streamed operand (hi = rn_tf32(x) by two
+//     integer ops, lo = x - hi exact), done while the previous phase's
+//     tensor-core work is in flight (the update's V fragments are split in
+//     phase 1, before Z exists);
+//   * the B operands (X for the partial, -2Z for the update and the
+//     look-ahead correction) are written pre-split, in B-fragment order, by
+//     the warps that produce them — no conversions on the consumer side;
+//   * "row warps" own 16-row tiles of X in registers (tensor-core C
+//     fragments) and do both the partial (A) and the update (C) on them; two
+//     B warps form Z; one producer warp only issues the stage copies;
+//   * shared addresses are computed once; ring indices are counters.
+// Per step (two CTA barriers):
+//   phase 1   row warps: L_{t+1} partial from X^(t) and W_{t+1}, combined over
+//             the row warps in fixed order, pushed to every CTA of the
+//             cluster (st.async + remote mbarrier complete_tx)
+//             B warps:   Z_t = sum_c L_t^c (fixed order) + (-2 S_t Z_{t-1})
+//   phase 2   row warps: X^(t+1) = X^(t) + V_t (-2 Z_t) in their accumulators
+#include "device_prims.cuh"
+#include "fasth_internal.h"
+
+namespace fasthb {
+namespace {
+
+constexpr int WCV = 8;     // batch columns per cluster (one MMA N tile)
+constexpr int NSLOTV = 4;  // exchange receive slots (WAR argument in chain_kernel.cu)
+constexpr int MAXNR = 8;   // row warps
+
+// 3xTF32 split with round-to-nearest hi: hi = rn_tf32(x), lo = x - hi (exact
+// in fp32, either sign, so the tensor core's truncation of lo is unbiased).
+__device__ __forceinline__ uint32_t hi_rn(float x) { return (__float_as_uint(x) + 0x1000u) & 0xffffe000u; }
+__device__ __forceinline__ float lo_rn(float x) { return x - __uint_as_float(hi_rn(x)); }
+
+__device__ __forceinline__ void hmma(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                     uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// A fragment (m16n8k8 .tf32: a0 (g,tq) a1 (g+8,tq) a2 (g,tq+4) a3 (g+8,tq+4)), split
+struct AFrag {
+    uint32_t h[4], l[4];
+};
+__device__ __forceinline__ AFrag make_a(float a0, float a1, float a2, float a3) {
+    AFrag f;
+    const float v[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f.h[i] = hi_rn(v[i]);
+        f.l[i] = __float_as_uint(v[i] - __uint_as_float(f.h[i]));
+    }
+    return f;
+}
+
+// m += ah bh ; c1 += ah bl ; c2 += al bh   (3xTF32, three independent chains)
+__device__ __forceinline__ void mma3s(float (&m)[4], float (&c1)[4], float (&c2)[4], const AFrag& a,
+                                      float bh0, float bh1, float bl0, float bl1) {
+    const uint32_t B0 = __float_as_uint(bh0), B1 = __float_as_uint(bh1);
+    hmma(m, a.h[0], a.h[1], a.h[2], a.h[3], B0, B1);
+    hmma(c1, a.h[0], a.h[1], a.h[2], a.h[3], __float_as_uint(bl0), __float_as_uint(bl1));
+    hmma(c2, a.l[0], a.l[1], a.l[2], a.l[3], B0, B1);
+}
+
+template <int N>
+__device__ __forceinline__ void lds_vec(float (&r)[N], const float* p) {
+    static_assert(N % 2 == 0, "vec");
+    if constexpr (N % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < N; i += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(p + i);
+            r[i] = v.x, r[i + 1] = v.y, r[i + 2] = v.z, r[i + 3] = v.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+            const float2 v = *reinterpret_cast<const float2*>(p + i);
+            r[i] = v.x, r[i + 1] = v.y;
+        }
+    }
+}
+
+// C fragment of a 16x8 tile (rows g, g+8; cols 2tq, 2tq+1) -> B-fragment
+// order of its transposed use as a K=16 x N=8 operand: consumer lane
+// 4c + (rho & 3), slot 2*(rho >> 3) + ((rho >> 2) & 1); hi = raw, lo split.
+__device__ __forceinline__ void scatter_cb(float* hi, float* lo, const float (&v)[4], int g, int tq,
+                                           float s) {
+#pragma unroll
+    for (int e2 = 0; e2 < 2; ++e2)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 2 * tq + e;
+            const int o = (4 * c + (g & 3)) * 4 + 2 * e2 + (g >> 2);
+            const float x = s * v[e2 * 2 + e];
+            const uint32_t h = hi_rn(x);
+            hi[o] = __uint_as_float(h);
+            lo[o] = x - __uint_as_float(h);
+        }
+}
+
+__device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_u32(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_u32(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void push4(uint32_t raddr, const float (&v)[4], uint32_t rbar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(rbar)
+        : "memory");
+}
+
+struct V2Smem {
+    size_t stg, zr, xn, zn, red, bars, total;
+};
+
+__host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg) {
+    const int RC = d_pad / C, RT = RC / 16, MT = BS / 16, KB = BS / 8;
+    const int NR = RT < MAXNR ? RT : MAXNR;
+    V2Smem L;
+    size_t o = 0;  // in floats
+    L.stg = o;
+    o += (size_t)nstg * stage_floats(RC, BS);
+    L.zr = o;
+    o += (size_t)NSLOTV * C * MT * 128;
+    L.xn = o;
+    o += (size_t)RT * 256;
+    L.zn = o;
+    o += (size_t)2 * KB * 128;
+    L.red = o;
+    o += (size_t)NR * MT * 128;
+    o = (o + 3) & ~size_t(3);
+    L.bars = o;
+    o += 2 * (nstg + NSLOTV);
+    L.total = o * 4;
+    return L;
+}
+
+template <int BS, int TPW>
+__global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(SweepV2Args a) {
+    constexpr int MT = BS / 16, KB = BS / 8;
+    constexpr int LDW = stage_ldw(BS), LDV = stage_ldv(BS);
+    constexpr int WOFF = 0;
+    extern __shared__ __align__(128) float sm[];
+
+    const int C = a.C, q = a.q, NSTG = a.nstg;
+    const int RC = a.d_pad / C, RT = RC / 16;
+    const int NR = RT < MAXNR ? RT : MAXNR;
+    const V2Smem L = v2_layout(C, BS, a.d_pad, NSTG);
+    const int SF = (int)stage_floats(RC, BS);
+    const int VOFF = RC * LDW, SOFF = RC * (LDW + LDV);
+    float* stg = sm + L.stg;
+    float* Zr = sm + L.zr;
+    float* Xn = sm + L.xn;
+    float* Zn = sm + L.zn;
+    float* red = sm + L.red;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+    const uint32_t rank = dev::cluster_ctarank();
+    const int cid = (int)dev::cluster_id_x();
+    const int dirn = cid / a.ngroups, group = cid - dirn * a.ngroups;
+    const SweepDirV2 D = a.dir[dirn];
+    const int row0 = (int)rank * RC, col0 = group * WCV;
+    const uint32_t bar_u32 = dev::smem_u32(bars);  // ld_bar[s] = +8 s, ex_bar[s] = +8 (NSTG + s)
+    const uint32_t exb_u32 = bar_u32 + 8u * NSTG;
+    const uint32_t stage_bytes = (uint32_t)SF * 4u;
+    const uint32_t ex_bytes = (uint32_t)C * MT * 512u;
+    const int PW = NR + MT;  // producer warp
+    long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
+
+    auto block_of = [&](int t) { return D.forward ? q - 1 - t : t; };
+    auto gstage = [&](int t) { return D.stage + ((size_t)t * C + rank) * SF; };
+
+    if (tid == 0) {
+        for (int s = 0; s < NSTG + NSLOTV; ++s) dev::mbar_init(&bars[s], 1);
+        dev::fence_mbar_init();
+        for (int s = 0; s < NSLOTV; ++s) mbar_expect_u32(exb_u32 + 8u * s, ex_bytes);
+    }
+    __syncthreads();
+    if (warp == PW && lane == 0) {
+        const uint32_t stg_u32 = dev::smem_u32(stg);
+        for (int t = 0; t < NSTG && t < q; ++t) {
+            mbar_expect_u32(bar_u32 + 8u * t, stage_bytes);
+            bulk_u32(stg_u32 + (uint32_t)t * stage_bytes, gstage(t), stage_bytes, bar_u32 + 8u * t);
+        }
+    }
+
+    // row warps: X^(0) tiles into registers and B-fragment order
+    float x[TPW][4];
+    if (warp < NR) {
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            const int rt = warp + u * NR;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x[u][e] = 0.f;
+            if (rt < RT) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int gr = row0 + rt * 16 + g + 8 * (e >> 1), gc = col0 + 2 * tq + (e & 1);
+                    if (gr < D.n_valid && gc < a.m) {
+                        float v = D.x_in[(int64_t)gc * D.ldx + gr];
+                        if (D.scale) v *= D.scale[gr];
+                        x[u][e] = v;
+                    }
+                }
+                scatter_cb(Xn + rt * 256, Xn + rt * 256 + 128, x[u], g, tq, 1.f);
+            }
+        }
+    }
+    // peers' barriers armed before anyone pushes; Xn visible
+    dev::cluster_sync();
+
+    const uint32_t zr_u32 = dev::smem_u32(Zr);
+    const int NCOMB = MT < NR ? MT : NR;  // row warps that combine + push the partial
+    const size_t tape_step = (size_t)a.ngroups * a.d_pad * WCV;
+    float* const tape0 = D.tape ? D.tape + ((size_t)group * a.d_pad + row0) * WCV : nullptr;
+
+    // ---- phase-1 work of the row warps: L partial for step s (stage ss) from X^(cur)
+    auto partial_push = [&](int s, int ss) {
+        const float* Ws = stg + ss * SF;
+        float pm[MT][4], p1[MT][4], p2[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) pm[mt][e] = p1[mt][e] = p2[mt][e] = 0.f;
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            const int rt = warp + u * NR;
+            if (rt < RT) {
+                float xh[4], xl[4];
+                lds_vec<4>(xh, Xn + rt * 256 + lane * 4);
+                lds_vec<4>(xl, Xn + rt * 256 + 128 + lane * 4);
+                float w0[2][2 * MT], w1[2][2 * MT];
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks) {
+                    const int R = rt * 16 + ks * 8 + tq;
+                    lds_vec<2 * MT>(w0[ks], Ws + R * LDW + g * 2 * MT);
+                    lds_vec<2 * MT>(w1[ks], Ws + (R + 4) * LDW + g * 2 * MT);
+                }
+#pragma unroll
+                for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const AFrag af = make_a(w0[ks][2 * mt], w0[ks][2 * mt + 1], w1[ks][2 * mt], w1[ks][2 * mt + 1]);
+                        mma3s(pm[mt], p1[mt], p2[mt], af, xh[2 * ks], xh[2 * ks + 1], xl[2 * ks], xl[2 * ks + 1]);
+                    }
+            }
+        }
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+            *reinterpret_cast<float4*>(red + (warp * MT + mt) * 128 + lane * 4) =
+                make_float4(pm[mt][0] + (p1[mt][0] + p2[mt][0]), pm[mt][1] + (p1[mt][1] + p2[mt][1]),
+                            pm[mt][2] + (p1[mt][2] + p2[mt][2]), pm[mt][3] + (p1[mt][3] + p2[mt][3]));
+        if (trc && tid == 0) trc[(size_t)(s > 0 ? s - 1 : q) * 16 + 1] = clock64();
+        if (warp < NCOMB) {
+            dev::named_bar_sync<1>(NR * 32);
+            // one float4 of the CTA's partial per thread, summed in fixed order
+            // over the row warps, pushed to every CTA of the cluster
+            const int slot = s % NSLOTV;
+            const uint32_t rbar_l = exb_u32 + 8u * slot;
+            for (int k = tid; k < MT * 32; k += NCOMB * 32) {
+                float sum[4];
+                lds_vec<4>(sum, red + k * 4);
+                for (int w = 1; w < NR; ++w) {
+                    float p[4];
+                    lds_vec<4>(p, red + w * MT * 128 + k * 4);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) sum[e] += p[e];
+                }
+                const uint32_t off = zr_u32 + (uint32_t)(((slot * C + (int)rank) * MT * 128 + k * 4) * 4);
+                for (int dst = 0; dst < C; ++dst)
+                    push4(dev::mapa(off, dst), sum, dev::mapa(rbar_l, dst));
+            }
+        } else {
+            asm volatile("bar.arrive 1, %0;" ::"r"(NR * 32) : "memory");
+        }
+    };
+
+    if (warp < NR && q > 0) {  // prologue: Z_0's partials from X^(0)
+        mbar_wait_u32(bar_u32, 0);
+        partial_push(0, 0);
+    }
+    __syncthreads();  // the combine scratch is reused by step 0's partial
+
+    int st = 0, ph = 0;  // stage ring position of step t
+    for (int t = 0; t < q; ++t) {
+        const int i = block_of(t);
+        if (trc && tid == 0) trc[(size_t)t * 16 + 0] = clock64();
+        // ---------------- phase 1 ----------------
+        AFrag va[TPW][KB];  // row warps: step t's update operands, split ahead of Z_t
+        if (warp < NR) {
+            if (t + 1 < q) {
+                const int st1 = st + 1 == NSTG ? 0 : st + 1;
+                const int ph1 = st + 1 == NSTG ? ph ^ 1 : ph;
+                mbar_wait_u32(bar_u32 + 8u * st1, (uint32_t)ph1);
+                partial_push(t + 1, st1);
+            }
+            const float* Vs = stg + st * SF + VOFF;
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const int rt = warp + u * NR;
+                if (rt < RT) {
+                    float v0[2 * KB], v1[2 * KB];
+                    lds_vec<2 * KB>(v0, Vs + (rt * 16 + g) * LDV + tq * 2 * KB);
+                    lds_vec<2 * KB>(v1, Vs + (rt * 16 + g + 8) * LDV + tq * 2 * KB);
+#pragma unroll
+                    for (int ks = 0; ks < KB; ++ks)
+                        va[u][ks] = make_a(v0[2 * ks], v1[2 * ks], v0[2 * ks + 1], v1[2 * ks + 1]);
+                }
+            }
+            if (trc && tid == 0) trc[(size_t)t * 16 + 2] = clock64();
+        } else if (warp < NR + MT) {
+            const int mt = warp - NR;
+            float cm[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f};
+            mbar_wait_u32(bar_u32 + 8u * st, (uint32_t)ph);
+            if (t > 0) {  // -2 S_t Z_{t-1}: Zn holds -2 Z_{t-1}, pre-split
+                const float* Ss = stg + st * SF + SOFF;
+                float s0[2 * KB], s1[2 * KB];
+                lds_vec<2 * KB>(s0, Ss + (mt * 16 + g) * LDV + tq * 2 * KB);
+                lds_vec<2 * KB>(s1, Ss + (mt * 16 + g + 8) * LDV + tq * 2 * KB);
+                const float* zp = Zn + ((t - 1) & 1) * (KB * 128);
+#pragma unroll
+                for (int h2 = 0; h2 < KB / 2; ++h2) {
+                    float zh[4], zl[4];
+                    lds_vec<4>(zh, zp + h2 * 128 + lane * 4);
+                    lds_vec<4>(zl, zp + (KB / 2) * 128 + h2 * 128 + lane * 4);
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const int ks = 2 * h2 + kk;
+                        const AFrag af = make_a(s0[2 * ks], s1[2 * ks], s0[2 * ks + 1], s1[2 * ks + 1]);
+                        mma3s(cm, c1, c2, af, zh[2 * kk], zh[2 * kk + 1], zl[2 * kk], zl[2 * kk + 1]);
+                    }
+                }
+            }
+            const int slot = t % NSLOTV;
+            mbar_wait_u32(exb_u32 + 8u * slot, (uint32_t)((t / NSLOTV) & 1));
+            if (trc && lane == 0 && mt == 0) trc[(size_t)t * 16 + 3] = clock64();
+            if (lane == 0 && mt == 0) mbar_expect_u32(exb_u32 + 8u * slot, ex_bytes);
+            float z[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) z[e] = cm[e] + (c1[e] + c2[e]);
+            const float* zr = Zr + ((size_t)slot * C * MT + mt) * 128 + lane * 4;
+            float zs[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int c = 0; c < C; ++c) {  // fixed order over the source CTAs
+                float p[4];
+                lds_vec<4>(p, zr + c * MT * 128);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) zs[e] += p[e];
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) z[e] += zs[e];
+            float* zc = Zn + (t & 1) * (KB * 128) + mt * 128;
+            scatter_cb(zc, zc + (KB / 2) * 128, z, g, tq, -2.f);
+            if (D.zhat && rank == 0) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = mt * 16 + g + 8 * (e >> 1), l = col0 + 2 * tq + (e & 1);
+                    if (l < a.m) D.zhat[((size_t)i * BS + j) * a.m + l] = z[e];
+                }
+            }
+            if (trc && lane == 0 && mt == 0) trc[(size_t)t * 16 + 4] = clock64();
+        } else if (warp == PW && lane == 0) {
+            // refill the stage step t-1 used (all its readers passed the last barrier)
+            const int tn = t - 1 + NSTG;
+            if (t > 0 && tn < q) {
+                const int sp = st == 0 ? NSTG - 1 : st - 1;
+                mbar_expect_u32(bar_u32 + 8u * sp, stage_bytes);
+                bulk_u32(dev::smem_u32(stg) + (uint32_t)sp * stage_bytes, gstage(tn), stage_bytes,
+                         bar_u32 + 8u * sp);
+            }
+        }
+        __syncthreads();
+        if (trc && tid == 0) trc[(size_t)t * 16 + 5] = clock64();
+        // ---------------- phase 2: X^(t+1) = X^(t) + V_t (-2 Z_t) ----------------
+        if (warp < NR) {
+            const float* zc = Zn + (t & 1) * (KB * 128);
+            float zh[KB / 2][4], zl[KB / 2][4];
+#pragma unroll
+            for (int h2 = 0; h2 < KB / 2; ++h2) {
+                lds_vec<4>(zh[h2], zc + h2 * 128 + lane * 4);
+                lds_vec<4>(zl[h2], zc + (KB / 2) * 128 + h2 * 128 + lane * 4);
+            }
+            float* tblk = tape0 ? tape0 + (size_t)i * tape_step : nullptr;
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const int rt = warp + u * NR;
+                if (rt < RT) {
+                    float* tp = tblk ? tblk + (rt * 16 + g) * WCV + 2 * tq : nullptr;
+                    if (tp && !D.forward) {  // dA[i] = X^(t), the gradient at the block output
+                        *reinterpret_cast<float2*>(tp) = make_float2(x[u][0], x[u][1]);
+                        *reinterpret_cast<float2*>(tp + 8 * WCV) = make_float2(x[u][2], x[u][3]);
+                    }
+                    float c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                    for (int ks = 0; ks < KB; ++ks)
+                        mma3s(x[u], c1, c2, va[u][ks], zh[ks >> 1][2 * (ks & 1)], zh[ks >> 1][2 * (ks & 1) + 1],
+                              zl[ks >> 1][2 * (ks & 1)], zl[ks >> 1][2 * (ks & 1) + 1]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) x[u][e] += c1[e] + c2[e];
+                    if (tp && D.forward) {  // A_i = activations[i]
+                        *reinterpret_cast<float2*>(tp) = make_float2(x[u][0], x[u][1]);
+                        *reinterpret_cast<float2*>(tp + 8 * WCV) = make_float2(x[u][2], x[u][3]);
+                    }
+                    if (t + 2 < q) scatter_cb(Xn + rt * 256, Xn + rt * 256 + 128, x[u], g, tq, 1.f);
+                }
+            }
+            __syncwarp();
+            if (trc && tid == 0) trc[(size_t)t * 16 + 6] = clock64();
+        }
+        __syncthreads();
+        if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64();
+        if (++st == NSTG) st = 0, ph ^= 1;
+    }
+
+    if (warp < NR) {
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            const int rt = warp + u * NR;
+            if (rt < RT) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int gr = row0 + rt * 16 + g + 8 * (e >> 1), gc = col0 + 2 * tq + (e & 1);
+                    if (gr < a.d && gc < a.m) D.x_out[(int64_t)gc * D.ldo + gr] = x[u][e];
+                }
+            }
+        }
+    }
+    // no CTA may exit while a peer could still push into it
+    dev::cluster_sync();
+}
+
+template <int BS, int TPW>
+cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
+    const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg);
+    auto kern = sweep2_kernel<BS, TPW>;
+    static size_t configured = 0;
+    if (L.total > configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        configured = L.total;
+    }
+    const int RT = a.d_pad / a.C / 16;
+    const int NR = RT < MAXNR ? RT : MAXNR;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(a.C * a.ngroups * a.ndir, 1, 1);
+    cfg.blockDim = dim3((NR + BS / 16 + 1) * 32, 1, 1);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int TPW>
+cudaError_t launch_bs(const SweepV2Args& a, cudaStream_t s) {
+    switch (a.BS) {
+        case 16: return launch_t<16, TPW>(a, s);
+        case 32: return launch_t<32, TPW>(a, s);
+        case 64: return launch_t<64, TPW>(a, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace
+
+size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg) { return v2_layout(C, BS, d_pad, nstg).total; }
+
+int sweep2_nstg(int C, int BS, int d_pad) {
+    if (C < 1 || C > 16 || d_pad % C) return 0;
+    const int RC = d_pad / C;
+    if (RC % 16 || RC / 16 > 2 * MAXNR) return 0;
+    if (BS != 16 && BS != 32 && BS != 64) return 0;
+    int best = 0;
+    for (int n = 2; n <= 4; ++n)
+        if (sweep2_smem_bytes(C, BS, d_pad, n) <= 227 * 1024) best = n;
+    return best;
+}
+
+cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s) {
+    if (a.ndir < 1 || a.ndir > 2 || a.ngroups < 1 || a.q < 1) return cudaErrorInvalidValue;
+    const int nst = sweep2_nstg(a.C, a.BS, a.d_pad);
+    if (nst == 0 || a.nstg < 2 || a.nstg > nst) return cudaErrorInvalidConfiguration;
+    const int RT = a.d_pad / a.C / 16;
+    if (RT <= MAXNR) return launch_bs<1>(a, s);
+    return launch_bs<2>(a, s);
+}
+
+}  // namespace fasthb

@@ -49,7 +49,54 @@ struct Plan {
     float* Sf = nullptr;         // [q][BS][BS+4]   Wf_i^T V_{i+1}  (forward look-ahead)
     float* Sb = nullptr;         // [q][BS][BS+4]   Wb_i^T V_{i-1}  (backward look-ahead)
     float* Tt = nullptr;         // [q][BS][BS]     T~ (diagnostics / tests)
+    float* Pf = nullptr;         // packed forward stages  [q][CB][stage_floats] (step order)
+    float* Pb = nullptr;         // packed backward stages [q][CB][stage_floats]
     int CB = 8;                  // build cluster size (CTAs per block)
+    long long* trace = nullptr;  // optional build phase stamps (FASTH_TRACE)
+};
+
+// ---- packed chain stages (chain_v2.cu) ------------------------------------
+// Everything CTA r of a chain cluster needs for one step t of a sweep, one
+// contiguous run so that ONE bulk copy lands it:
+//   [ W rows (RC x LDW) | V rows (RC x LDV) | S (BS x LDV) ]
+// of block i(t) (forward: i = q-1-t, Wf / Sf; backward: i = t, Wb / Sb), rows
+// [r*RC, (r+1)*RC).  Columns are permuted into mma.sync fragment order so a
+// lane's operands are contiguous 16-byte vectors:
+//   W: pos = g*2MT + mt*2 + h  for column c = 16 mt + 8 h + g   (A operand of W^T X)
+//   V, S: pos = tq*2KB + ks*2 + h  for column c = 8 ks + 4 h + tq (A operand of V Z, S Z)
+// with MT = BS/16, KB = BS/8.  Pitches: LDW = BS+8 (== 8 mod 32), LDV = BS+4.
+__host__ __device__ constexpr int stage_ldw(int BS) { return BS + 8; }
+__host__ __device__ constexpr int stage_ldv(int BS) { return BS + 4; }
+__host__ __device__ constexpr size_t stage_floats(int RC, int BS) {
+    return (size_t)RC * stage_ldw(BS) + (size_t)RC * stage_ldv(BS) + (size_t)BS * stage_ldv(BS);
+}
+__host__ __device__ inline int perm_w_bs(int c, int BS) {
+    const int MT = BS / 16;
+    return (c & 7) * 2 * MT + (c >> 4) * 2 + ((c >> 3) & 1);
+}
+__host__ __device__ inline int perm_v_bs(int c, int BS) {
+    const int KB = BS / 8;
+    return (c & 3) * 2 * KB + (c >> 3) * 2 + ((c >> 2) & 1);
+}
+
+struct SweepDirV2 {
+    const float* stage;   // [q][C][stage_floats] packed, step order
+    const float* x_in;    // column-major, rows < n_valid are read
+    int64_t ldx;
+    int n_valid;
+    const float* scale;   // optional per-row scale applied on load (Sigma)
+    float* x_out;         // column-major d x m
+    int64_t ldo;
+    float* tape;          // optional [q][ngroups][d_pad][WC] (same as SweepArgs)
+    float* zhat;          // optional [q][BS][m]
+    int forward;
+};
+
+struct SweepV2Args {
+    SweepDirV2 dir[2];    // cluster c runs dir[c / ngroups] on column group c % ngroups
+    int ndir;             // 1, or 2 (forward and backward sweeps in one launch)
+    int d, d_pad, m, q, BS, C, nstg, ngroups;
+    long long* trace;     // optional phase timestamps [CTA][q+1][16]
 };
 
 struct SweepArgs {
@@ -87,6 +134,9 @@ struct DvArgs {
 cudaError_t launch_build(const Plan& p, const float* V, int64_t ldv, ErrWord* err,
                          cudaStream_t s);
 size_t build_smem_bytes(int BS, int RB);
+// wy_build2.cu (packed stages for chain_v2.cu)
+cudaError_t launch_build2(const Plan& p, const float* V, int64_t ldv, ErrWord* err, cudaStream_t s);
+size_t build2_smem_bytes(int BS, int RB);
 // chain_sweep.cu
 struct SweepGeom {
     int C = 1, RC = 16, d_pad = 16, WC = 8, nstg = 3;
@@ -96,8 +146,14 @@ SweepGeom pick_geometry(int d, int m, int BS, int num_sms);
 size_t sweep_smem_bytes(int C, int WC, int BS, int d_pad, int nstg);
 int sweep_ldw(int BS);  // row pitch of Wf / Wb blocks
 int sweep_ldv(int BS);  // row pitch of Vbl blocks and Sf / Sb
+// chain_v2.cu
+int sweep2_nstg(int C, int BS, int d_pad);  // 0 = geometry not supported by the v2 kernel
+size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg);
+cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
 // dv.cu
 cudaError_t launch_dv(const DvArgs& a, cudaStream_t s);
+// dv2.cu (tapes with WC == 8)
+cudaError_t launch_dv2(const DvArgs& a, cudaStream_t s);
 // sigma_ops.cu
 cudaError_t launch_scale_rows(const float* x, int64_t ldx, int n_valid, const float* scale,
                               int rows, int m, float* y, int64_t ldy, int mode,

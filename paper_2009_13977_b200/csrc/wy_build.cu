@@ -243,6 +243,19 @@ __device__ void wtn_mma(const float* Ws, const float* Nb, float* Sp, int RB) {
     }
 }
 
+// This CTA's rows of W (pitch LDN) and V (pitch LDV) -> its packed chain
+// stage (fasth_internal.h): columns permuted into mma fragment order.
+template <int BS>
+__device__ void store_packed_wv(float* dst, const float* Ws, const float* Vs, int RB) {
+    constexpr int LDN = BS + 8, LDVs = BS + 4;
+    constexpr int LDW = stage_ldw(BS), LDV = stage_ldv(BS);
+    for (int idx = threadIdx.x; idx < RB * BS; idx += kThreads) {
+        const int r = idx / BS, c = idx - r * BS;
+        dst[r * LDW + perm_w_bs(c, BS)] = Ws[r * LDN + c];
+        dst[RB * LDW + r * LDV + perm_v_bs(c, BS)] = Vs[r * LDVs + c];
+    }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(kThreads, 1) build_kernel(Plan p, const float* __restrict__ V,
                                                              int64_t ldv, ErrWord* err) {
@@ -324,7 +337,11 @@ __global__ void __launch_bounds__(kThreads, 1) build_kernel(Plan p, const float*
     // 5/6. Wf = V T~^T ; Sf_i = Wf^T V_{i+1}
     w_rows_mma<BS>(Vs, Tf, Ws, RB, 1);
     __syncthreads();
-    store_rows<LDN>(p.Wf + woff, Ws, RB);
+    if (p.Wf) store_rows<LDN>(p.Wf + woff, Ws, RB);
+    const size_t SF = stage_floats(RB, BS);
+    float* pf = p.Pf ? p.Pf + ((size_t)(p.q - 1 - i) * CB + rank) * SF : nullptr;
+    float* pb = p.Pb ? p.Pb + ((size_t)i * CB + rank) * SF : nullptr;
+    if (pf) store_packed_wv<BS>(pf, Ws, Vs, RB);
     wtn_mma<BS>(Ws, Nb, Sp, RB);
     __syncthreads();
     // Wb = V T~ ; Sb_i = Wb^T V_{i-1}  (previous block's rows load meanwhile)
@@ -333,10 +350,19 @@ __global__ void __launch_bounds__(kThreads, 1) build_kernel(Plan p, const float*
     w_rows_mma<BS>(Vs, Tf, Ws, RB, 0);
     dev::cp_async_wait_all();
     __syncthreads();
-    store_rows<LDN>(p.Wb + woff, Ws, RB);
+    if (p.Wb) store_rows<LDN>(p.Wb + woff, Ws, RB);
+    if (pb) store_packed_wv<BS>(pb, Ws, Vs, RB);
     wtn_mma<BS>(Ws, Nb, Sp + BS * BS, RB);
     cluster_allreduce<float>(Sp, So, 2 * BS * BS, CB, rank);
-    if (rank == 0)  // row pitch BS + 4 (the chain kernel's S pitch)
+    if (pf) {  // every CTA's stage carries the block's look-ahead correction
+        const int soff = RB * (stage_ldw(BS) + LDV);
+        for (int idx = tid; idx < BS * BS; idx += kThreads) {
+            const int j = idx / BS, k = idx - j * BS;
+            pf[soff + j * LDV + perm_v_bs(k, BS)] = So[idx];
+            pb[soff + j * LDV + perm_v_bs(k, BS)] = So[BS * BS + idx];
+        }
+    }
+    if (rank == 0 && p.Sf)  // row pitch BS + 4 (the chain kernel's S pitch)
         for (int idx = tid; idx < BS * LDV; idx += kThreads) {
             const int j = idx / LDV, k = idx - j * LDV;
             const bool in = k < BS;

@@ -97,8 +97,11 @@ class Context:
     def check(self):
         _check(self.lib.fasth_ctx_check(self.h))
 
-    def set_timing(self, on: bool):
-        _check(self.lib.fasth_ctx_set_timing(self.h, 1 if on else 0))
+    def set_timing(self, on, graph: bool = False):
+        """Per-kernel CUDA-event timing.  graph=True keeps the events alive so
+        a CUDA graph captured while timing is on can be replayed and read with
+        kernel_times() after every replay (no host gaps in the figures)."""
+        _check(self.lib.fasth_ctx_set_timing(self.h, (2 if graph else 1) if on else 0))
 
     def kernel_times(self) -> dict:
         """{kernel: (total_ms, launches)} accumulated in timing mode."""
@@ -252,6 +255,31 @@ def fasth_backward(tape: Tape, G: torch.Tensor, *, want_vectors: bool = True) ->
     _check(c.lib.fasth_backward(c.h, tape.h, _ptr(G), ldg, _ptr(dX), max(tape.d, 1),
                                 _ptr(dV), max(tape.d, 1)))
     return BackwardResult(dX, dV)
+
+
+def fasth_forward_backward(V: torch.Tensor, X: torch.Tensor, G: torch.Tensor, block_width: int, *,
+                           ctx: Context | None = None, want_vectors: bool = True, out=None):
+    """fasth.hpp:40 + :69 as one call (``fasth_forward_backward``), for a
+    caller that already holds grad_output G (the reference benchmark's
+    op=mul step, bench.hpp:140-150).  Returns (Y, BackwardResult)."""
+    X, ldx = _colmajor(X, "fasth_forward: X")
+    G, ldg = _colmajor(G, "fasth_backward: grad_output")
+    d, m = X.shape
+    if tuple(G.shape) != (d, m):
+        raise DimensionError("fasth_backward: grad_output shape mismatch")
+    V, n, dv, ldv = _chain(V, "fasth_forward: V", d)
+    if n > 0 and dv != d:
+        raise DimensionError("fasth_forward: X row count != chain dim")
+    c = _ctx(ctx, X)
+    if out is None:
+        Y, dX = _new_out(d, m, X), _new_out(d, m, X)
+        dV = torch.empty((n, d), dtype=torch.float32, device=X.device) if want_vectors else None
+    else:
+        Y, dX, dV = out
+    _check(c.lib.fasth_forward_backward(c.h, _ptr(V), ldv, d, n, _ptr(X), ldx, _ptr(G), ldg, m,
+                                        int(block_width), _ptr(Y), max(d, 1), _ptr(dX), max(d, 1),
+                                        _ptr(dV), max(d, 1)))
+    return Y, BackwardResult(dX, dV)
 
 
 def forward_backward_host(V, X, G, block_width: int, *, ctx: Context | None = None):

@@ -1,28 +1,58 @@
-"""Summarise FASTH_TRACE sweep dumps: cycles per phase per step (chain_sweep.cu
-slots: 0 top, 1 A after load wait, 2 A done, 3 B after exchange wait,
-4 B done, 5 after barrier 1, 6 C done, 7 after barrier 2).  Slots 0-2,5-7
-are stamped by thread 0 (an A warp), 3-4 by the first B warp: all on the same
-SM clock."""
+"""Summarise FASTH_TRACE sweep dumps: cycles per phase per step.
+
+v1 (chain_kernel.cu, *.fwd.bin / *.bwd.bin) slots: 0 top, 1 A after load
+wait, 2 A done, 3 B after exchange wait, 4 B done, 5 after barrier 1, 6 C
+done, 7 after barrier 2, 8 A mma loop done, 9 A chunk combine done.
+v2 (chain_v2.cu, *.v2.bin) slots: 0 top, 1 partial MMAs done (before the
+combine barrier), 2 row warps' phase 1 done (pushed), 3 B after exchange
+wait, 4 B done, 5 after barrier 1, 6 update done, 7 after barrier 2.
+Slots 0-2, 5-7 are stamped by thread 0 (row warp 0), 3-4 by the first B
+warp: the same SM clock.  Note BAR.SYNC defers its block to the next
+dependent instruction, so a stamp right after a barrier is its issue time."""
 import sys
+
 import numpy as np
 
 
+def report_build(path):
+    raw = open(path, "rb").read()
+    n, k = np.frombuffer(raw[:8], dtype=np.int32)
+    tr = np.frombuffer(raw[8:], dtype=np.int64).reshape(n, k).astype(np.float64)
+    names = ["load V rows", "Gram band", "cluster reduce", "degeneracy+mask", "T~ + B operands", "W rows", "stores"]
+    print(f"{path}: {n} CTAs; build phases (cycles, mean / max over CTAs); total mean {np.mean(tr[:, 7] - tr[:, 0]):.0f}")
+    for j, nm in enumerate(names):
+        v = tr[:, j + 1] - tr[:, j]
+        print(f"  {nm:22s} mean {v.mean():7.0f}  max {v.max():7.0f}")
+    t0 = tr[:, 0].min()
+    print(f"  CTA start spread: {tr[:, 0].max() - t0:.0f} cycles (same-SM clocks only comparable)")
+
+
 def report(path):
+    if path.endswith(".build.bin"):
+        return report_build(path)
     raw = open(path, "rb").read()
     nctas, q = np.frombuffer(raw[:8], dtype=np.int32)
     tr = np.frombuffer(raw[8:], dtype=np.int64).reshape(nctas, q + 1, 16).astype(np.float64)
     s = tr[:, :q, :]
     print(f"{path}: {nctas} CTAs, q={q}")
-    print(f"  cycles/step (top to top): {np.mean(np.diff(s[:, :, 0], axis=1)):.0f}")
-    rows = [("A load wait", 1, 0, slice(0, q - 1)), ("A partial+push", 2, 1, slice(0, q - 1)),
-            ("B exch wait (from top)", 3, 0, slice(1, q)), ("B reduce+corr", 4, 3, slice(1, q)),
-            ("barrier1 (from A done)", 5, 2, slice(0, q - 1)), ("barrier1 (from B done)", 5, 4, slice(1, q)),
-            ("C update", 6, 5, slice(0, q)), ("barrier2+refill", 7, 6, slice(0, q)),
-            ("  A: mma loop", 8, 1, slice(0, q - 1)), ("  A: chunk combine", 9, 8, slice(0, q - 1)),
-            ("  A: push", 2, 9, slice(0, q - 1))]
+    print(f"  cycles/step (top to top): {np.mean(np.diff(s[:, :, 0], axis=1)):.0f}"
+          f"   whole sweep (top 0 -> after last barrier): {np.mean(s[:, q - 1, 7] - s[:, 0, 0]):.0f}")
+    if path.endswith(".v2.bin"):
+        rows = [("row: partial MMAs", 1, 0, slice(0, q - 1)), ("row: combine+push", 2, 1, slice(0, q - 1)),
+                ("B: exch wait (from top)", 3, 0, slice(0, q)), ("B: reduce+scatter", 4, 3, slice(0, q)),
+                ("barrier1 (from row done)", 5, 2, slice(0, q)), ("barrier1 (from B done)", 5, 4, slice(0, q)),
+                ("update", 6, 5, slice(0, q)), ("barrier2", 7, 6, slice(0, q))]
+    else:
+        rows = [("A load wait", 1, 0, slice(0, q - 1)), ("A partial+push", 2, 1, slice(0, q - 1)),
+                ("B exch wait (from top)", 3, 0, slice(1, q)), ("B reduce+corr", 4, 3, slice(1, q)),
+                ("barrier1 (from A done)", 5, 2, slice(0, q - 1)), ("barrier1 (from B done)", 5, 4, slice(1, q)),
+                ("C update", 6, 5, slice(0, q)), ("barrier2+refill", 7, 6, slice(0, q)),
+                ("  A: mma loop", 8, 1, slice(0, q - 1)), ("  A: chunk combine", 9, 8, slice(0, q - 1)),
+                ("  A: push", 2, 9, slice(0, q - 1))]
     for name, k1, k0, sl in rows:
         v = s[:, sl, k1] - s[:, sl, k0]
-        print(f"  {name:26s} mean {v.mean():7.0f}  p50 {np.median(v):7.0f}  max {v.max():7.0f}")
+        if v.size:
+            print(f"  {name:26s} mean {v.mean():7.0f}  p50 {np.median(v):7.0f}  max {v.max():7.0f}")
 
 
 for p in sys.argv[1:]:

@@ -57,10 +57,76 @@ def rel(a, b):
     return relative_error(host(a) if not isinstance(a, np.ndarray) else a, b)
 
 
-def run_chain(fb, V, X, G, b):
+def run_chain(fb, V, X, G, b, fused=False):
+    if fused:  # fasth_forward_backward: both sweeps in one launch
+        Y, back = fb.fasth_forward_backward(dev(V), dev(X), dev(G), b)
+        return Y, back.grad_input, back.grad_vectors
     tape = fb.fasth_forward(dev(V), dev(X), b)
     back = fb.fasth_backward(tape, dev(G))
     return tape.output(), back.grad_input, back.grad_vectors
+
+
+@pytest.mark.parametrize("case", ["cfg1", "ragged", "n1", "b1", "bn", "m1", "oddb"])
+def test_fused_forward_backward_matches_reference_golden(fb, golden, case):
+    g = {k.split("/", 1)[1]: golden[k] for k in golden.files if k.startswith(case + "/")}
+    import json
+    meta = json.load(open(os.path.join(HERE, "golden", "fasth_golden.json")))[case]
+    Y, dX, dV = run_chain(fb, g["V"], g["X"], g["G"], meta["b"], fused=True)
+    errs = (rel(Y, g["Y"]), rel(dX, g["dX"]), rel(dV, g["dV"]))
+    assert max(errs) <= TOL, errs
+
+
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (64, 8, 32), (2048, 32, 32), (200, 17, 33), (96, 8, 100)])
+def test_fused_equals_two_calls_bitwise(fb, d, b, m):
+    """Same kernels, same per-column arithmetic: the one-launch fwd+bwd must
+    reproduce the fasth_forward + fasth_backward pair bit for bit."""
+    rng = np.random.default_rng(d + b + m)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    a = run_chain(fb, V, X, G, b)
+    f = run_chain(fb, V, X, G, b, fused=True)
+    for u, w in zip(a, f):
+        assert np.array_equal(host(u), host(w))
+
+
+@pytest.mark.parametrize("env", ["FASTH_BUILD_V1", "FASTH_DV_V1"])
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (200, 17, 33), (64, 8, 100)])
+def test_build2_dv2_match_first_kernels(fb, oracle, env, d, b, m):
+    """wy_build2.cu / dv2.cu against the first WY builder / gradient kernel
+    (selected by FASTH_BUILD_V1 / FASTH_DV_V1): both within tolerance of the
+    oracle and of each other."""
+    port, _ = oracle
+    rng = np.random.default_rng(3 * d + b + m)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = port.fasth_fwd_bwd(V, X, G, b)
+    os.environ[env] = "1"
+    try:
+        old = run_chain(fb, V, X, G, b, fused=True)
+    finally:
+        del os.environ[env]
+    new = run_chain(fb, V, X, G, b, fused=True)
+    for a1, a2, w in zip(old, new, want):
+        assert rel(a1, w) <= TOL and rel(a2, w) <= TOL
+        assert rel(a2, host(a1)) <= 2e-5
+
+
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (256, 64, 32), (128, 16, 8), (2048, 32, 16)])
+def test_chain_v2_matches_v1_kernel(fb, oracle, d, b, m):
+    """The packed-stage chain kernel (chain_v2.cu) against the first chain
+    kernel (chain_kernel.cu, FASTH_SWEEP_V1=1): both within tolerance of the
+    oracle and of each other."""
+    port, _ = oracle
+    rng = np.random.default_rng(7 * d + b)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = port.fasth_fwd_bwd(V, X, G, b)
+    os.environ["FASTH_SWEEP_V1"] = "1"
+    try:
+        v1 = run_chain(fb, V, X, G, b)
+    finally:
+        del os.environ["FASTH_SWEEP_V1"]
+    v2 = run_chain(fb, V, X, G, b)
+    for a1, a2, w in zip(v1, v2, want):
+        assert rel(a1, w) <= TOL and rel(a2, w) <= TOL
+        assert rel(a2, host(a1)) <= 2e-5
 
 
 @pytest.mark.parametrize("case", ["cfg1", "ragged", "n1", "b1", "bn", "m1", "oddb"])
