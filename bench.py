@@ -208,7 +208,7 @@ def main():
 
     def step():
         """fasth_forward + fasth_backward of the reference benchmark step
-        (bench.hpp:140-150, G drawn up front) as the one-call
+        (bench.hpp:147-151, G drawn up front) as the one-call
         fasth_forward_backward: build, both sweeps in one launch, gradients."""
         Y, back = fb.fasth_forward_backward(Vd, Xd, Gd, B, ctx=ctx, out=(Yd, dXd, dVd))
         if world > 1:
@@ -331,21 +331,29 @@ def main():
     Xh = torch.tensor(X.T.copy(), dtype=torch.float32).pin_memory()
     Gh = torch.tensor(G.T.copy(), dtype=torch.float32).pin_memory()
     hctx = fb.Context(local)
+    hout = (torch.empty((M, D), dtype=torch.float32).pin_memory(),
+            torch.empty((M, D), dtype=torch.float32).pin_memory(),
+            torch.empty((D, D), dtype=torch.float32).pin_memory())
     for _ in range(args.warmup):
-        fb.forward_backward_host(Vh, Xh, Gh, B, ctx=hctx)
+        fb.forward_backward_host(Vh, Xh, Gh, B, ctx=hctx, out=hout)
     e2e_steps = max(20, min(args.steps, 200))
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    walls = []
     for _ in range(e2e_steps):
-        Yh, dXh, dVh = fb.forward_backward_host(Vh, Xh, Gh, B, ctx=hctx)
+        t0 = time.perf_counter()
+        Yh, dXh, dVh = fb.forward_backward_host(Vh, Xh, Gh, B, ctx=hctx, out=hout)
         if world > 1:  # the batch-summed dV of the sharded job
             dvd = dVh.to(dev, non_blocking=True)
             dist.all_reduce(dvd)
             dVh.copy_(dvd)
-    torch.cuda.synchronize()
-    e2e_us = (time.perf_counter() - t0) * 1e6 / e2e_steps
+            torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t0)
+    walls.sort()
+    # median of per-step wall times (each call returns synchronised results)
+    e2e_us = walls[len(walls) // 2] * 1e6
+    e2e_mean_us = sum(walls) / len(walls) * 1e6
     if world > 1:
         t = torch.tensor([e2e_us], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -406,7 +414,8 @@ def main():
                                   f"MEASURED_PEAKS ({pk['bf16']} TFLOP/s); the sweep runs 3xTF32 mma.sync "
                                   "and is latency bound at batch 32 (25 dependent block steps per chain)"},
         "e2e": {"value": e2e_us, "unit": "us/step", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
+                "d2h_bytes_per_step": d2h, "mean_us": e2e_mean_us, "steps": e2e_steps,
+                "timing": "host wall clock per call (median), copies and sync inside",
                 "api": "fasth_forward_backward_host (C ABI, pinned host buffers)"},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),

@@ -114,7 +114,7 @@ fasth_status fasth_tape_info(fasth_tape tape, int* d, int* n, int* m, int* block
 
 /* The reference's call pair fasth_forward + fasth_backward (fasth.hpp:40, :69)
  * as one call, for callers that hold the output gradient G when they start —
- * the reference benchmark's op=mul step (bench.hpp:140-150: forward, then
+ * the reference benchmark's op=mul step (bench.hpp:147-151: forward, then
  * backward with a pre-drawn G).  Same results as the two calls; the forward
  * and backward sweeps are independent once the WY blocks exist, so they run
  * concurrently in one launch.  Y, dX: d x m; dV: d x n (may be NULL). */

@@ -47,6 +47,8 @@ fasth_status fail(fasth_status s, const char* fmt, ...) {
         if (s_ != FASTH_OK) return s_;     \
     } while (0)
 
+constexpr int kMaxPipeQ = 4096;  // WY blocks the pipelined step supports
+
 size_t size_class(size_t bytes) {
     size_t c = 512;
     while (c < bytes) c <<= 1;
@@ -67,6 +69,23 @@ struct fasth_ctx_s {
     int counters_len = 0;
     double* logdet_d = nullptr;
     int64_t launches = 0;
+    long long* build_trace = nullptr;  // FASTH_TRACE: pending builder stamps
+    size_t build_trace_n = 0;
+    int build_trace_rows = 0;
+    void dump_build_trace(const char* prefix) {
+        if (!build_trace) return;
+        std::vector<long long> h(build_trace_n);
+        cudaMemcpy(h.data(), build_trace, build_trace_n * sizeof(long long), cudaMemcpyDeviceToHost);
+        cudaFree(build_trace);
+        build_trace = nullptr;
+        std::string path = std::string(prefix) + ".build.bin";
+        if (FILE* f = fopen(path.c_str(), "wb")) {
+            int hdr[2] = {build_trace_rows, 10};
+            fwrite(hdr, sizeof(int), 2, f);
+            fwrite(h.data(), sizeof(long long), build_trace_n, f);
+            fclose(f);
+        }
+    }
     int last_chain = 0, last_index = -1;
     std::mutex mu;
     std::map<size_t, std::vector<void*>> free_list;
@@ -200,6 +219,7 @@ struct fasth_tape_s {
     int m = 0, b_user = 0;
     int C = 0, WC = 0, ngroups = 0, nstg = 3;
     int v2nstg = 0;  // > 0: packed stages + chain_v2.cu sweep (else chain_kernel.cu)
+    bool pipelined = false;  // build -> sweep -> dv overlapped through block counters
     float* tapeA = nullptr;  // activations per block
     float* zf = nullptr;
     float* tapeG = nullptr;  // gradient per block (backward scratch)
@@ -258,7 +278,7 @@ int internal_b(int d, int n, int b_user) {
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row
 // padding d_pad the chain geometry asks for.
 fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_pad, int cb, int n,
-                        int b_user, int reversed, int tag, bool packed, Plan* out) {
+                        int b_user, int reversed, int tag, bool packed, bool* pipelined, Plan* out) {
     Plan p;
     p.d = d;
     p.n = n;
@@ -285,27 +305,31 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
         TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sf));
         TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sb));
     }
-    if (packed && !getenv("FASTH_BUILD_V1") && build2_smem_bytes(p.BS, p.d_pad / p.CB) <= 227 * 1024) {
+    const bool b2 = packed && !getenv("FASTH_BUILD_V1") && build2_smem_bytes(p.BS, p.d_pad / p.CB) <= 227 * 1024;
+    if (pipelined && *pipelined) {
+        // opt-in (FASTH_PIPELINE=1): profitable only once a block builds in
+        // well under the sweep's duration (scripts/trace_report.py --timeline)
+        *pipelined = b2 && p.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && getenv("FASTH_PIPELINE") &&
+                     !getenv("FASTH_NO_PIPELINE") && !getenv("FASTH_DV_V1");
+        if (*pipelined) {
+            p.ready = c->counters;
+            const char* nb = getenv("FASTH_BUILDERS");
+            p.nbuild = nb ? std::max(1, atoi(nb)) : 12;
+        }
+    }
+    if (b2) {
         const char* prefix = getenv("FASTH_TRACE");
-        const size_t ntr = (size_t)p.q * p.CB * 8;
-        if (prefix) {
+        const size_t ntr = (size_t)p.q * p.CB * 10;
+        if (prefix) {  // dumped after the sweep (no sync here: keep the pipeline)
             CU(cudaMalloc(&p.trace, ntr * sizeof(long long)));
             CU(cudaMemsetAsync(p.trace, 0, ntr * sizeof(long long), c->stream));
         }
         fasth_status bs = c->timed([&] { return launch_build2(p, V, ldv, c->err_d, c->stream); }, "wy_build");
         if (prefix) {
-            std::vector<long long> h(ntr);
-            CU(cudaMemcpyAsync(h.data(), p.trace, ntr * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-            CU(cudaStreamSynchronize(c->stream));
-            cudaFree(p.trace);
+            c->build_trace = p.trace;
+            c->build_trace_n = ntr;
+            c->build_trace_rows = p.q * p.CB;
             p.trace = nullptr;
-            std::string path = std::string(prefix) + ".build.bin";
-            if (FILE* f = fopen(path.c_str(), "wb")) {
-                int hdr[2] = {p.q * p.CB, 8};
-                fwrite(hdr, sizeof(int), 2, f);
-                fwrite(h.data(), sizeof(long long), ntr, f);
-                fclose(f);
-            }
         }
         TRY(bs);
     } else {
@@ -381,6 +405,7 @@ fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what)
     CU(cudaMemcpyAsync(h.data(), tr, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     cudaFree(tr);
+    c->dump_build_trace(prefix);
     std::string path = std::string(prefix) + "." + what + ".v2.bin";
     if (FILE* f = fopen(path.c_str(), "wb")) {
         int hdr[2] = {nctas, a.q};
@@ -448,6 +473,7 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     if (t->v2nstg) {
         SweepV2Args a = v2_args(t);
         a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, record);
+        a.pdl = !getenv("FASTH_NO_PDL");  // the builder was the previous launch; X predates it
         return launch_traced_sweep2(c, a, "sweep(forward)");
     }
     SweepArgs a{};
@@ -473,7 +499,7 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     return launch_traced_sweep(c, a, t->WC, "sweep(forward)");
 }
 
-fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv);
+fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe = false);
 
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
 fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, int g_valid,
@@ -526,9 +552,16 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     return run_dv(c, t, dV, lddv);
 }
 
-fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv) {
+fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe) {
     const Plan& p = t->plan;
     DvArgs v{};
+    if (pipe) {
+        v.ready = c->counters;
+        v.done = c->counters + kMaxPipeQ;
+        v.dvcnt = c->counters + 2 * kMaxPipeQ;
+        v.done_target = (unsigned)(2 * t->ngroups * t->C);
+    }
+    v.pdl = !getenv("FASTH_NO_PDL");  // the sweep was the previous launch
     v.Vbl = p.Vbl;
     v.d = p.d;
     v.d_pad = p.d_pad;
@@ -576,15 +609,21 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
     a.ndir = 2;
     a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, want_dv);
     a.dir[1] = v2_backward_dir(t, G, ldg, p.d, nullptr, dx, lddx, want_dv);
+    const bool pipe = t->pipelined && want_dv;
+    a.pdl = !getenv("FASTH_NO_PDL");  // the builder was the previous launch
+    if (pipe) {
+        a.ready = c->counters;
+        a.done = c->counters + kMaxPipeQ;
+    }
     fasth_status s = launch_traced_sweep2(c, a, "sweep(fwd+bwd)");
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
-    return run_dv(c, t, dV, lddv);
+    return run_dv(c, t, dV, lddv, pipe);
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
-                      int reversed, int tag, fasth_tape* out) {
+                      int reversed, int tag, fasth_tape* out, bool pipelined = false) {
     fasth_tape t = new fasth_tape_s;
     t->ctx = c;
     t->m = m;
@@ -597,7 +636,9 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     t->nstg = G.nstg;
     t->ngroups = (m + t->WC - 1) / t->WC;
     t->v2nstg = getenv("FASTH_SWEEP_V1") ? 0 : sweep2_nstg(G.C, BS, G.d_pad);
-    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, t->v2nstg > 0, &t->plan);
+    t->pipelined = pipelined && t->v2nstg > 0;
+    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, t->v2nstg > 0, &t->pipelined,
+                                &t->plan);
     if (s != FASTH_OK) {
         delete t;
         return s;
@@ -684,6 +725,10 @@ fasth_status fasth_ctx_create(int device, void* stream, fasth_ctx* out) {
     c->err_h->chain = 0;
     cudaHostGetDevicePointer(&c->err_d, c->err_h, 0);
     cudaMalloc(&c->logdet_d, sizeof(double));
+    // pipelined-step counters (ready | done | dvcnt per block), zero, self-resetting
+    if (cudaMalloc(&c->counters, 3 * kMaxPipeQ * sizeof(unsigned)) == cudaSuccess &&
+        cudaMemset(c->counters, 0, 3 * kMaxPipeQ * sizeof(unsigned)) == cudaSuccess)
+        c->counters_len = 3 * kMaxPipeQ;
     *out = c;
     return FASTH_OK;
 }
@@ -872,7 +917,7 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
         return s;
     }
     fasth_tape t = nullptr;
-    TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t));
+    TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr));
     fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);
     free_tape(t);  // pool reuse is stream ordered
     if (s == FASTH_OK) s = c->finish();

@@ -464,7 +464,11 @@ SweepGeom pick_geometry(int d, int m, int BS, int num_sms) {
     (void)m;
     (void)num_sms;
     SweepGeom G;
-    int C = (d + 111) / 112;
+    // ~80-row slabs up to 10 CTAs per cluster (measured on B200 at d = 784:
+    // 10 x 80 beats 7 x 112 by ~4% per fwd+bwd step; 12+ CTA clusters no longer
+    // fit the fused launch's 8 clusters at once), else ~112-row slabs
+    int C = (d + 79) / 80;
+    if (C > 10) C = (d + 111) / 112;
     if (C < 1) C = 1;
     if (C > 16) C = 16;
     if (const char* e = getenv("FASTH_CLUSTER")) C = atoi(e);

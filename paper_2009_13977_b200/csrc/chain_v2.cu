@@ -114,6 +114,18 @@ __device__ __forceinline__ void scatter_cb(float* hi, float* lo, const float (&v
         }
 }
 
+// pipelined step: spin until counter >= target (acquire, gpu scope), then make
+// the generic-proxy writes it published visible to the bulk-copy engine
+__device__ __forceinline__ void wait_counter(const unsigned* c, unsigned target) {
+    unsigned v;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -202,10 +214,17 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     const uint32_t ex_bytes = (uint32_t)C * MT * 512u;
     const int PW = NR + MT;  // producer warp
     long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
+    // prologue / epilogue global-timer stamps in row q: 10 entry, 11 X loaded,
+    // 12 cluster synced, 13 prologue partial pushed, 14 loop done, 15 exit
+#define GSTAMP(k) \
+    if (trc && tid == 0) trc[(size_t)q * 16 + (k)] = (long long)dev::globaltimer()
+    GSTAMP(10);
 
     auto block_of = [&](int t) { return D.forward ? q - 1 - t : t; };
     auto gstage = [&](int t) { return D.stage + ((size_t)t * C + rank) * SF; };
 
+    // the gradient kernel may launch now; it waits on the per-block counters
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
         for (int s = 0; s < NSTG + NSLOTV; ++s) dev::mbar_init(&bars[s], 1);
         dev::fence_mbar_init();
@@ -214,7 +233,11 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     __syncthreads();
     if (warp == PW && lane == 0) {
         const uint32_t stg_u32 = dev::smem_u32(stg);
+        // launched as a programmatic dependent of the builder: everything up
+        // to here overlapped its tail; its stages are read only from now on
+        if (!a.ready && a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
         for (int t = 0; t < NSTG && t < q; ++t) {
+            if (a.ready) wait_counter(a.ready + block_of(t), (unsigned)C);
             mbar_expect_u32(bar_u32 + 8u * t, stage_bytes);
             bulk_u32(stg_u32 + (uint32_t)t * stage_bytes, gstage(t), stage_bytes, bar_u32 + 8u * t);
         }
@@ -242,8 +265,10 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             }
         }
     }
+    GSTAMP(11);
     // peers' barriers armed before anyone pushes; Xn visible
     dev::cluster_sync();
+    GSTAMP(12);
 
     const uint32_t zr_u32 = dev::smem_u32(Zr);
     const int NCOMB = MT < NR ? MT : NR;  // row warps that combine + push the partial
@@ -315,12 +340,13 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
         mbar_wait_u32(bar_u32, 0);
         partial_push(0, 0);
     }
+    GSTAMP(13);
     __syncthreads();  // the combine scratch is reused by step 0's partial
 
     int st = 0, ph = 0;  // stage ring position of step t
     for (int t = 0; t < q; ++t) {
         const int i = block_of(t);
-        if (trc && tid == 0) trc[(size_t)t * 16 + 0] = clock64();
+        if (trc && tid == 0) trc[(size_t)t * 16 + 0] = clock64(), trc[(size_t)t * 16 + 8] = (long long)dev::globaltimer();
         // ---------------- phase 1 ----------------
         AFrag va[TPW][KB];  // row warps: step t's update operands, split ahead of Z_t
         if (warp < NR) {
@@ -399,6 +425,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             const int tn = t - 1 + NSTG;
             if (t > 0 && tn < q) {
                 const int sp = st == 0 ? NSTG - 1 : st - 1;
+                if (a.ready) wait_counter(a.ready + block_of(tn), (unsigned)C);
                 mbar_expect_u32(bar_u32 + 8u * sp, stage_bytes);
                 bulk_u32(dev::smem_u32(stg) + (uint32_t)sp * stage_bytes, gstage(tn), stage_bytes,
                          bar_u32 + 8u * sp);
@@ -443,7 +470,12 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             if (trc && tid == 0) trc[(size_t)t * 16 + 6] = clock64();
         }
         __syncthreads();
-        if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64();
+        if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64(), trc[(size_t)t * 16 + 9] = (long long)dev::globaltimer();
+        // block i's tape rows and Z' are stored: signal the gradient kernel
+        if (a.done && warp == PW && lane == 0) {
+            __threadfence();
+            atomicAdd(a.done + i, 1u);
+        }
         if (++st == NSTG) st = 0, ph ^= 1;
     }
 
@@ -456,12 +488,15 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
                 for (int e = 0; e < 4; ++e) {
                     const int gr = row0 + rt * 16 + g + 8 * (e >> 1), gc = col0 + 2 * tq + (e & 1);
                     if (gr < a.d && gc < a.m) D.x_out[(int64_t)gc * D.ldo + gr] = x[u][e];
+                    if (u == 0 && e == 0) GSTAMP(14);
                 }
             }
         }
     }
     // no CTA may exit while a peer could still push into it
     dev::cluster_sync();
+    GSTAMP(15);
+#undef GSTAMP
 }
 
 template <int BS, int TPW>
@@ -483,13 +518,15 @@ cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
     cfg.blockDim = dim3((NR + BS / 16 + 1) * 32, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = a.C;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = a.pdl ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 

@@ -95,6 +95,24 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     const size_t tstep = (size_t)a.ngroups * a.d_pad * 8;
     const float* tA = a.tapeA + (size_t)i * tstep;
     const float* tG = a.tapeG + (size_t)i * tstep;
+    if (!a.done && a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // sweep complete
+    if (a.done) {  // pipelined step: both sweeps have passed block i
+        if (tid == 0) {
+            unsigned v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.done + i) : "memory");
+                if (v >= a.done_target) break;
+                __nanosleep(128);
+            }
+            // the last CTA of block i to get here resets the block's counters
+            if (atomicAdd(a.dvcnt + i, 1u) == gridDim.x - 1) {
+                a.ready[i] = 0u;
+                a.done[i] = 0u;
+                a.dvcnt[i] = 0u;
+            }
+        }
+        __syncthreads();
+    }
 
     float acc[NT][4], cc[NT][4];
 #pragma unroll
@@ -250,8 +268,17 @@ cudaError_t launch_dv2_t(const DvArgs& a, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     configured = true;
-    dv2_kernel<BS><<<grid, DV_WARPS * 32, smem, s>>>(a);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(DV_WARPS * 32, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (a.done || a.pdl) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, dv2_kernel<BS>, a);
 }
 
 }  // namespace

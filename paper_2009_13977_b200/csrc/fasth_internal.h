@@ -53,6 +53,12 @@ struct Plan {
     float* Pb = nullptr;         // packed backward stages [q][CB][stage_floats]
     int CB = 8;                  // build cluster size (CTAs per block)
     long long* trace = nullptr;  // optional build phase stamps (FASTH_TRACE)
+    // pipelined step (fasth_forward_backward): per-block readiness counters,
+    // +1 per build CTA once its rows of block i's packed stages are stored;
+    // nbuild > 0 runs the builder persistent on nbuild clusters (blocks in
+    // the order the two sweeps need them).  nullptr / 0: plain launch.
+    unsigned* ready = nullptr;
+    int nbuild = 0;
 };
 
 // ---- packed chain stages (chain_v2.cu) ------------------------------------
@@ -97,6 +103,12 @@ struct SweepV2Args {
     int ndir;             // 1, or 2 (forward and backward sweeps in one launch)
     int d, d_pad, m, q, BS, C, nstg, ngroups;
     long long* trace;     // optional phase timestamps [CTA][q+1][16]
+    // pipelined step: wait for ready[i] >= C before streaming block i's
+    // stage; signal done[i] += 1 per CTA once block i's tape / Z' rows are
+    // stored (nullptr: plain launch, no waits, no signals)
+    const unsigned* ready;
+    unsigned* done;
+    int pdl;              // launched as a programmatic dependent of the builder
 };
 
 struct SweepArgs {
@@ -128,6 +140,13 @@ struct DvArgs {
     const float* zb;
     float* dV;            // column-major d x n
     int64_t lddv;
+    // pipelined step: wait for done[i] >= done_target, then the last CTA of
+    // block i resets ready[i], done[i], dvcnt[i] (nullptr: plain launch)
+    unsigned* ready;
+    unsigned* done;
+    unsigned* dvcnt;
+    unsigned done_target;
+    int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
 };
 
 // wy_build.cu

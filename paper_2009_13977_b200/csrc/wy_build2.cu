@@ -101,14 +101,22 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
     const uint32_t rank = dev::cluster_ctarank();
-    const int i = (int)dev::cluster_id_x();
     const int row0 = (int)rank * RB;
+    // the chain sweep may launch now (programmatic dependent launch): it waits
+    // on the per-block readiness counters, not on this grid's completion
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // persistent over blocks when pipelined: ticket k -> the k-th block the
+    // two sweeps need (forward from q-1 down, backward from 0 up, interleaved)
+    const int nclu = (int)(gridDim.x / CB);
+    for (int tkt = (int)dev::cluster_id_x(); tkt < p.q; tkt += nclu) {
+    const int i = p.nbuild > 0 ? ((tkt & 1) ? (tkt >> 1) : p.q - 1 - (tkt >> 1)) : tkt;
     const int w = min(p.b, p.n - i * p.b);
-    // FASTH_TRACE phase stamps: [CTA][8] clock64 (0 start, 1 loaded, 2 Gram
-    // band done, 3 reduced, 4 T~, 5 B operands, 6 W rows, 7 end)
+    // FASTH_TRACE phase stamps: [block][CTA rank][8] clock64 (0 start, 1 loaded,
+    // 2 Gram band done, 3 reduced, 4 T~, 5 B operands, 6 W rows, 7 end)
 #define BTRACE(k) \
-    if (p.trace && tid == 0) p.trace[(size_t)blockIdx.x * 8 + (k)] = clock64()
+    if (p.trace && tid == 0) p.trace[((size_t)i * CB + rank) * 10 + (k)] = clock64()
     BTRACE(0);
+    if (p.trace && tid == 0) p.trace[((size_t)i * CB + rank) * 10 + 8] = (long long)dev::globaltimer();
 
     // 1. V rows of blocks i, i-1, i+1 -> Vt[slot][j][r] (zero outside the chain / d);
     //    16-byte copies where the column is 16-byte aligned
@@ -372,8 +380,16 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
         *reinterpret_cast<float4*>(pf + soff + j * LDV + p0) = make_float4(sf[0], sf[1], sf[2], sf[3]);
         *reinterpret_cast<float4*>(pb + soff + j * LDV + p0) = make_float4(sb[0], sb[1], sb[2], sb[3]);
     }
+    // publish block i (all of this CTA's stores ordered before the counter)
+    __syncthreads();
+    if (p.ready && tid == 0) {
+        __threadfence();
+        atomicAdd(&p.ready[i], 1u);
+    }
     BTRACE(7);
+    if (p.trace && tid == 0) p.trace[((size_t)i * CB + rank) * 10 + 9] = (long long)dev::globaltimer();
 #undef BTRACE
+    }
 }
 
 template <int BS>
@@ -388,7 +404,8 @@ cudaError_t launch_build2_t(const Plan& p, const float* V, int64_t ldv, ErrWord*
         configured = L.total;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(p.q * p.CB, 1, 1);
+    const int nclu = p.nbuild > 0 ? (p.nbuild < p.q ? p.nbuild : p.q) : p.q;
+    cfg.gridDim = dim3(nclu * p.CB, 1, 1);
     cfg.blockDim = dim3(NTH, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = st;

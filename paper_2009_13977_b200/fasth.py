@@ -261,7 +261,7 @@ def fasth_forward_backward(V: torch.Tensor, X: torch.Tensor, G: torch.Tensor, bl
                            ctx: Context | None = None, want_vectors: bool = True, out=None):
     """fasth.hpp:40 + :69 as one call (``fasth_forward_backward``), for a
     caller that already holds grad_output G (the reference benchmark's
-    op=mul step, bench.hpp:140-150).  Returns (Y, BackwardResult)."""
+    op=mul step, bench.hpp:147-151).  Returns (Y, BackwardResult)."""
     X, ldx = _colmajor(X, "fasth_forward: X")
     G, ldg = _colmajor(G, "fasth_backward: grad_output")
     d, m = X.shape
@@ -282,18 +282,22 @@ def fasth_forward_backward(V: torch.Tensor, X: torch.Tensor, G: torch.Tensor, bl
     return Y, BackwardResult(dX, dV)
 
 
-def forward_backward_host(V, X, G, block_width: int, *, ctx: Context | None = None):
+def forward_backward_host(V, X, G, block_width: int, *, ctx: Context | None = None, out=None):
     """Host-buffer drop-in for fasth_forward + fasth_backward
     (``fasth_forward_backward_host``).  V: (n, d), X, G: (m, d) CPU float32
     tensors (pin them for full bandwidth) — i.e. column-major d x m.
-    Returns (Y, dX, dV) as CPU tensors of the same layouts."""
+    Returns (Y, dX, dV) as CPU tensors of the same layouts; ``out`` may hold
+    preallocated (pinned) ones."""
     c = ctx if ctx is not None else default_context()
     c.bind_stream()
     n, d = V.shape
     m = X.shape[0]
-    Y = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
-    dX = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
-    dV = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    if out is None:
+        Y = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
+        dX = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
+        dV = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
+    else:
+        Y, dX, dV = out
     _check(c.lib.fasth_forward_backward_host(c.h, _ptr(V), d, n, _ptr(X), _ptr(G), m,
                                              int(block_width), _ptr(Y), _ptr(dX), _ptr(dV)))
     return Y, dX, dV

@@ -51,7 +51,7 @@ if __name__ == "__main__":
     X = torch.randn(m, d, device="cuda").t()
     G = torch.randn(m, d, device="cuda").t()
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
-    for variant in ["", "FASTH_BUILD_V1", "FASTH_DV_V1", "FASTH_SWEEP_V1"]:
+    for variant in ["", "FASTH_NO_PIPELINE", "FASTH_BUILD_V1", "FASTH_DV_V1", "FASTH_SWEEP_V1"]:
         if variant:
             os.environ[variant] = "1"
         ctx = fb.Context(0, deferred=True)

@@ -18,6 +18,8 @@ def report_build(path):
     raw = open(path, "rb").read()
     n, k = np.frombuffer(raw[:8], dtype=np.int32)
     tr = np.frombuffer(raw[8:], dtype=np.int64).reshape(n, k).astype(np.float64)
+    tr = tr[tr[:, 0] != 0]  # blocks this launch did not build (persistent builders) stay zero
+    n = len(tr)
     names = ["load V rows", "Gram band", "cluster reduce", "degeneracy+mask", "T~ + B operands", "W rows", "stores"]
     print(f"{path}: {n} CTAs; build phases (cycles, mean / max over CTAs); total mean {np.mean(tr[:, 7] - tr[:, 0]):.0f}")
     for j, nm in enumerate(names):
@@ -38,6 +40,12 @@ def report(path):
     print(f"  cycles/step (top to top): {np.mean(np.diff(s[:, :, 0], axis=1)):.0f}"
           f"   whole sweep (top 0 -> after last barrier): {np.mean(s[:, q - 1, 7] - s[:, 0, 0]):.0f}")
     if path.endswith(".v2.bin"):
+        g = tr[:, q, :]
+        t0 = g[:, 10]
+        names = {11: "X loaded", 12: "cluster synced", 13: "prologue pushed", 14: "loop done", 15: "exit"}
+        print("  prologue/epilogue (ns from kernel entry, mean over CTAs): " +
+              ", ".join(f"{v} {np.mean(g[:, k] - t0):.0f}" for k, v in names.items()))
+        print(f"  loop: step 0 top at {np.mean(s[:, 0, 8] - t0):.0f} ns, last step end at {np.mean(s[:, q - 1, 9] - t0):.0f} ns")
         rows = [("row: partial MMAs", 1, 0, slice(0, q - 1)), ("row: combine+push", 2, 1, slice(0, q - 1)),
                 ("B: exch wait (from top)", 3, 0, slice(0, q)), ("B: reduce+scatter", 4, 3, slice(0, q)),
                 ("barrier1 (from row done)", 5, 2, slice(0, q)), ("barrier1 (from B done)", 5, 4, slice(0, q)),
@@ -55,5 +63,33 @@ def report(path):
             print(f"  {name:26s} mean {v.mean():7.0f}  p50 {np.median(v):7.0f}  max {v.max():7.0f}")
 
 
-for p in sys.argv[1:]:
-    report(p)
+def timeline(build_path, sweep_path):
+    """Global-timer view of a pipelined step: when each WY block became ready
+    (last of its CTAs) vs when the sweeps started each step (ns)."""
+    raw = open(build_path, "rb").read()
+    n, k = np.frombuffer(raw[:8], dtype=np.int32)
+    b = np.frombuffer(raw[8:], dtype=np.int64).reshape(n, k)
+    raw = open(sweep_path, "rb").read()
+    nc, q = np.frombuffer(raw[:8], dtype=np.int32)
+    s = np.frombuffer(raw[8:], dtype=np.int64).reshape(nc, q + 1, 16)
+    C = n // q
+    t0 = min(b[:, 8][b[:, 8] > 0].min(), s[:, 0, 8].min())
+    ready = (b[:, 9].reshape(q, C).max(axis=1) - t0) / 1e3
+    start = (b[:, 8].reshape(q, C).min(axis=1) - t0) / 1e3
+    print(f"timeline (us from first build CTA start), q={q}")
+    print("  block build start : " + " ".join(f"{x:5.1f}" for x in start))
+    print("  block ready       : " + " ".join(f"{x:5.1f}" for x in ready))
+    half = nc // 2
+    for name, rows in (("fwd", slice(0, half)), ("bwd", slice(half, nc))):
+        st = (s[rows, :q, 8].min(axis=0) - t0) / 1e3
+        en = (s[rows, :q, 9].max(axis=0) - t0) / 1e3
+        print(f"  {name} step start    : " + " ".join(f"{x:5.1f}" for x in st))
+        print(f"  {name} step end      : " + " ".join(f"{x:5.1f}" for x in en))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "--timeline":
+        timeline(sys.argv[2], sys.argv[3])
+    else:
+        for p in sys.argv[1:]:
+            report(p)

@@ -88,6 +88,26 @@ def test_fused_equals_two_calls_bitwise(fb, d, b, m):
         assert np.array_equal(host(u), host(w))
 
 
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (64, 8, 32), (2048, 32, 32), (200, 17, 33), (96, 8, 100),
+                                   (300, 16, 5)])
+def test_pipelined_step_equals_serial_bitwise(fb, d, b, m):
+    """The pipelined fasth_forward_backward (builder, sweeps and gradient
+    kernel overlapped through per-block counters, programmatic dependent
+    launch) must reproduce the serialised launches bit for bit, and leave
+    the counters reset: run it repeatedly."""
+    rng = np.random.default_rng(11 * d + b + m)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    ser = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
+    os.environ["FASTH_PIPELINE"] = "1"
+    try:
+        for _ in range(3):
+            pip = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
+            for u, w in zip(ser, pip):
+                assert np.array_equal(u, w)
+    finally:
+        del os.environ["FASTH_PIPELINE"]
+
+
 @pytest.mark.parametrize("env", ["FASTH_BUILD_V1", "FASTH_DV_V1"])
 @pytest.mark.parametrize("d,b,m", [(784, 32, 32), (200, 17, 33), (64, 8, 100)])
 def test_build2_dv2_match_first_kernels(fb, oracle, env, d, b, m):
