@@ -396,16 +396,33 @@ fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what)
     const int nctas = a.C * a.ngroups * a.ndir;
     const size_t n = (size_t)nctas * (a.q + 1) * 16;
     long long* tr = nullptr;
+    long long* wtr = nullptr;
+    const size_t nw = (size_t)nctas * a.q * 48;
     CU(cudaMalloc(&tr, n * sizeof(long long)));
+    CU(cudaMalloc(&wtr, nw * sizeof(long long)));
     CU(cudaMemsetAsync(tr, 0, n * sizeof(long long), c->stream));
+    CU(cudaMemsetAsync(wtr, 0, nw * sizeof(long long), c->stream));
     a.trace = tr;
+    a.wtrace = wtr;
     fasth_status s = c->timed([&] { return launch_sweep2(a, c->stream); }, what);
     a.trace = nullptr;
-    std::vector<long long> h(n);
+    a.wtrace = nullptr;
+    std::vector<long long> h(n), hw(nw);
     CU(cudaMemcpyAsync(h.data(), tr, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaMemcpyAsync(hw.data(), wtr, nw * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     cudaFree(tr);
+    cudaFree(wtr);
     c->dump_build_trace(prefix);
+    {
+        std::string wpath = std::string(prefix) + "." + what + ".warps.bin";
+        if (FILE* f = fopen(wpath.c_str(), "wb")) {
+            int hdr[2] = {nctas, a.q};
+            fwrite(hdr, sizeof(int), 2, f);
+            fwrite(hw.data(), sizeof(long long), nw, f);
+            fclose(f);
+        }
+    }
     std::string path = std::string(prefix) + "." + what + ".v2.bin";
     if (FILE* f = fopen(path.c_str(), "wb")) {
         int hdr[2] = {nctas, a.q};

@@ -216,6 +216,19 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
     // prologue / epilogue global-timer stamps in row q: 10 entry, 11 X loaded,
     // 12 cluster synced, 13 prologue partial pushed, 14 loop done, 15 exit
+    // per-warp barrier stamps (FASTH_TRACE): [CTA][step][warp < 12][arrive S1,
+    // release S1, arrive S2, release S2]; the release stamp sits behind a
+    // volatile shared load, which cannot issue before the barrier resolves
+    long long* wtr = a.wtrace ? a.wtrace + (size_t)blockIdx.x * q * 48 : nullptr;
+#define WSTAMP(k)                                                                             \
+    if (wtr && lane == 0) {                                                                   \
+        if ((k) & 1) {                                                                        \
+            unsigned dummy_;                                                                  \
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(dummy_) : "r"(bar_u32)); \
+            if (dummy_ == 0xdeadbeefu) wtr[0] = 0;                                           \
+        }                                                                                     \
+        wtr[((size_t)t * 12 + warp) * 4 + (k)] = clock64();                                  \
+    }
 #define GSTAMP(k) \
     if (trc && tid == 0) trc[(size_t)q * 16 + (k)] = (long long)dev::globaltimer()
     GSTAMP(10);
@@ -431,7 +444,9 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
                          bar_u32 + 8u * sp);
             }
         }
+        WSTAMP(0);
         __syncthreads();
+        WSTAMP(1);
         if (trc && tid == 0) trc[(size_t)t * 16 + 5] = clock64();
         // ---------------- phase 2: X^(t+1) = X^(t) + V_t (-2 Z_t) ----------------
         if (warp < NR) {
@@ -469,7 +484,9 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             __syncwarp();
             if (trc && tid == 0) trc[(size_t)t * 16 + 6] = clock64();
         }
+        WSTAMP(2);
         __syncthreads();
+        WSTAMP(3);
         if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64(), trc[(size_t)t * 16 + 9] = (long long)dev::globaltimer();
         // block i's tape rows and Z' are stored: signal the gradient kernel
         if (a.done && warp == PW && lane == 0) {
@@ -497,6 +514,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     dev::cluster_sync();
     GSTAMP(15);
 #undef GSTAMP
+#undef WSTAMP
 }
 
 template <int BS, int TPW>

@@ -103,6 +103,7 @@ struct SweepV2Args {
     int ndir;             // 1, or 2 (forward and backward sweeps in one launch)
     int d, d_pad, m, q, BS, C, nstg, ngroups;
     long long* trace;     // optional phase timestamps [CTA][q+1][16]
+    long long* wtrace;    // optional per-warp barrier stamps [CTA][q][12][4]
     // pipelined step: wait for ready[i] >= C before streaming block i's
     // stage; signal done[i] += 1 per CTA once block i's tape / Z' rows are
     // stored (nullptr: plain launch, no waits, no signals)

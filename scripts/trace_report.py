@@ -29,7 +29,35 @@ def report_build(path):
     print(f"  CTA start spread: {tr[:, 0].max() - t0:.0f} cycles (same-SM clocks only comparable)")
 
 
+def report_warps(path, nr=None):
+    """Per-warp barrier arrivals of the v2 sweep: which role arrives last at
+    each CTA barrier (the step's critical path) and how long each barrier
+    takes to release after its last arrival."""
+    raw = open(path, "rb").read()
+    nctas, q = np.frombuffer(raw[:8], dtype=np.int32)
+    w = np.frombuffer(raw[8:], dtype=np.int64).reshape(nctas, q, 12, 4).astype(np.float64)
+    used = np.where(w[:, :, :, 0].max(axis=(0, 1)) != 0)[0]
+    w = w[:, 1:q - 1, used, :]  # interior steps
+    nw = len(used)
+    print(f"{path}: {nctas} CTAs, {nw} warps (row warps, B warps, producer)")
+    for bi, (ka, kr) in enumerate(((0, 1), (2, 3))):
+        arr = w[:, :, :, ka]
+        last = arr.max(axis=2)
+        rel = w[:, :, :, kr].min(axis=2)
+        lag = last[:, :, None] - arr  # how long before the last arrival each warp arrived
+        print(f"  barrier {bi + 1}: release - last arrival mean {np.mean(rel - last):.0f} cycles; "
+              f"mean slack per warp (cycles before the last arrival): " +
+              " ".join(f"w{u}:{lag[:, :, j].mean():.0f}" for j, u in enumerate(used)))
+    # step = release S2 (t) -> release S2 (t+1)
+    r2 = w[:, :, :, 3].min(axis=2)
+    print(f"  step (S2 release to S2 release): {np.mean(np.diff(r2, axis=1)):.0f} cycles; "
+          f"S2 release -> last arrival at S1: {np.mean(w[:, 1:, :, 0].max(axis=2) - r2[:, :-1]):.0f}; "
+          f"S1 release -> last arrival at S2: {np.mean(w[:, :, :, 2].max(axis=2) - w[:, :, :, 1].min(axis=2)):.0f}")
+
+
 def report(path):
+    if path.endswith(".warps.bin"):
+        return report_warps(path)
     if path.endswith(".build.bin"):
         return report_build(path)
     raw = open(path, "rb").read()
