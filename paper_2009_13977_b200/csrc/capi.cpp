@@ -387,8 +387,21 @@ fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int WC, const char* 
     return s;
 }
 
+// Large batches run the panel kernel (chain_panel.cu: one CTA per 16-column
+// panel holding all rows, no exchange) once the cluster sweep would need more
+// than ~2 waves of clusters; FASTH_PANEL=0/1 forces the choice.
+bool use_panel(const SweepV2Args& a) {
+    if (a.ready || !panel_supported(a.BS, a.d_pad, a.m)) return false;
+    if (const char* e = getenv("FASTH_PANEL")) return atoi(e) != 0;
+    return a.m > 64;
+}
+
 fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what) {
     const char* prefix = getenv("FASTH_TRACE");
+    if (use_panel(a)) {
+        a.trace = nullptr;
+        return c->timed([&] { return launch_panel(a, c->stream); }, "panel(fwd/bwd)");
+    }
     if (!prefix) {
         a.trace = nullptr;
         return c->timed([&] { return launch_sweep2(a, c->stream); }, what);

@@ -170,6 +170,9 @@ int sweep_ldv(int BS);  // row pitch of Vbl blocks and Sf / Sb
 int sweep2_nstg(int C, int BS, int d_pad);  // 0 = geometry not supported by the v2 kernel
 size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg);
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
+// chain_panel.cu (large batch: one CTA per 16-column panel, all rows)
+bool panel_supported(int BS, int d_pad, int m);
+cudaError_t launch_panel(const SweepV2Args& a, cudaStream_t s);
 // dv.cu
 cudaError_t launch_dv(const DvArgs& a, cudaStream_t s);
 // dv2.cu (tapes with WC == 8)

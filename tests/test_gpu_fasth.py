@@ -108,6 +108,48 @@ def test_pipelined_step_equals_serial_bitwise(fb, d, b, m):
         del os.environ["FASTH_PIPELINE"]
 
 
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (256, 32, 200), (300, 32, 65), (2048, 32, 48), (128, 32, 1)])
+def test_panel_sweep_vs_oracle(fb, oracle, d, b, m):
+    """Large-batch panel sweep (chain_panel.cu, forced with FASTH_PANEL=1)
+    against the oracle and against the cluster sweep (FASTH_PANEL=0), through
+    both the one-call and the two-call entry points."""
+    port, _ = oracle
+    rng = np.random.default_rng(5 * d + m)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = port.fasth_fwd_bwd(V, X, G, b)
+    res = {}
+    for mode in ("0", "1"):
+        os.environ["FASTH_PANEL"] = mode
+        try:
+            res[mode] = [run_chain(fb, V, X, G, b, fused=f) for f in (True, False)]
+        finally:
+            del os.environ["FASTH_PANEL"]
+    for got in res["0"] + res["1"]:
+        errs = [rel(a_, w) for a_, w in zip(got, want)]
+        assert max(errs) <= TOL, errs
+    for a_, c_ in zip(res["1"][0], res["0"][0]):
+        assert rel(a_, host(c_)) <= 2e-5
+
+
+def test_panel_large_batch_default_path(fb, oracle):
+    """m = 1024 at d = 512 takes the panel kernel by default; checked on a
+    column subset against the oracle and dV against the cluster path."""
+    port, _ = oracle
+    d, b, m = 512, 32, 1024
+    rng = np.random.default_rng(77)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    Y, dX, dV = (host(t) for t in run_chain(fb, V, X, G, b, fused=True))
+    cols = [0, 1, 15, 16, 511, 1023]
+    wY, wdX, _ = port.fasth_fwd_bwd(V, X[:, cols], G[:, cols], b)
+    assert rel(Y[:, cols], wY) <= TOL and rel(dX[:, cols], wdX) <= TOL
+    os.environ["FASTH_PANEL"] = "0"
+    try:
+        _, _, dV0 = run_chain(fb, V, X, G, b, fused=True)
+    finally:
+        del os.environ["FASTH_PANEL"]
+    assert rel(dV, host(dV0)) <= 2e-5
+
+
 @pytest.mark.parametrize("env", ["FASTH_BUILD_V1", "FASTH_DV_V1"])
 @pytest.mark.parametrize("d,b,m", [(784, 32, 32), (200, 17, 33), (64, 8, 100)])
 def test_build2_dv2_match_first_kernels(fb, oracle, env, d, b, m):
