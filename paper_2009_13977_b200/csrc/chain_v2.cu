@@ -171,7 +171,6 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     GSTAMP(12);
 
     const uint32_t zr_u32 = dev::smem_u32(Zr);
-    const int NCOMB = MT < NR ? MT : NR;  // row warps that combine + push the partial
     const size_t tape_step = (size_t)a.ngroups * a.d_pad * WCV;
     float* const tape0 = D.tape ? D.tape + ((size_t)group * a.d_pad + row0) * WCV : nullptr;
 
@@ -212,27 +211,34 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
                 make_float4(pm[mt][0] + (p1[mt][0] + p2[mt][0]), pm[mt][1] + (p1[mt][1] + p2[mt][1]),
                             pm[mt][2] + (p1[mt][2] + p2[mt][2]), pm[mt][3] + (p1[mt][3] + p2[mt][3]));
         if (trc && tid == 0) trc[(size_t)(s > 0 ? s - 1 : q) * 16 + 1] = clock64();
-        if (warp < NCOMB) {
-            dev::named_bar_sync<1>(NR * 32);
-            // one float4 of the CTA's partial per thread, summed in fixed order
-            // over the row warps, pushed to every CTA of the cluster
-            const int slot = s % NSLOTV;
-            const uint32_t rbar_l = exb_u32 + 8u * slot;
-            for (int k = tid; k < MT * 32; k += NCOMB * 32) {
-                float sum[4];
-                lds_vec<4>(sum, red + k * 4);
-                for (int w = 1; w < NR; ++w) {
-                    float p[4];
-                    lds_vec<4>(p, red + w * MT * 128 + k * 4);
+        // every row warp forms the CTA's sum (fixed order over the row warps;
+        // all loads in flight) and pushes it to its own destinations
+        // (warp, warp + NR, ...): the pushes are spread over the row warps
+        dev::named_bar_sync<1>(NR * 32);
+        if (warp < C) {
+            float sum[MT][4];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) sum[e] += p[e];
-                }
-                const uint32_t off = zr_u32 + (uint32_t)(((slot * C + (int)rank) * MT * 128 + k * 4) * 4);
-                for (int dst = 0; dst < C; ++dst)
-                    push4(dev::mapa(off, dst), sum, dev::mapa(rbar_l, dst));
+            for (int mt = 0; mt < MT; ++mt) {
+                float part[MAXNR][4];
+#pragma unroll
+                for (int w = 0; w < MAXNR; ++w)
+                    if (w < NR) lds_vec<4>(part[w], red + (w * MT + mt) * 128 + lane * 4);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) sum[mt][e] = part[0][e];
+#pragma unroll
+                for (int w = 1; w < MAXNR; ++w)
+                    if (w < NR)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) sum[mt][e] += part[w][e];
             }
-        } else {
-            asm volatile("bar.arrive 1, %0;" ::"r"(NR * 32) : "memory");
+            const int slot = s % NSLOTV;
+            const uint32_t off = zr_u32 + (uint32_t)((((slot * C + (int)rank) * MT) * 128 + lane * 4) * 4);
+            const uint32_t rbar_l = exb_u32 + 8u * slot;
+            for (int dst = warp; dst < C; dst += NR) {
+                const uint32_t rz = dev::mapa(off, dst), rb = dev::mapa(rbar_l, dst);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) push4(rz + mt * 512u, sum[mt], rb);
+            }
         }
     };
 
