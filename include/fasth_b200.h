@@ -182,6 +182,31 @@ fasth_status fasth_apply_cayley(fasth_ctx ctx, const fasth_svd_param* p, const f
                                 int64_t ldx, int m, int block_width, float* Y, int64_t ldy);
 fasth_status fasth_log_abs_det(fasth_ctx ctx, const fasth_svd_param* p, double* out);
 
+/* ---- OSVD checkpoints (svd_layer.hpp:204-290) -------------------------------
+ * The reference's flat little-endian format: "OSVD", version u32 (= 1),
+ * out_dim, in_dim, nU, nV (u32), then the U vectors, the V vectors (each
+ * d f64 values, chain order) and sigma (min(out_dim, in_dim) f64).
+ * fasth_svd_file_info  reads the header (no device work).
+ * fasth_svd_load       replaces load_svd_param_file (svd_layer.hpp:282): U, V
+ *   (device, column-major, column k = vector k) and sigma (device) receive the
+ *   payload rounded to fp32; same errors as the reference (bad magic, version,
+ *   truncation -> FASTH_ERR_INVALID; a vector with ||v||^2 <= 1e-30 ->
+ *   FASTH_ERR_DEGENERATE, householder.hpp:28).
+ * fasth_svd_save       replaces save_svd_param_file (svd_layer.hpp:276): the
+ *   device parameter widened to f64.  save(load(f)) reproduces f bit for bit
+ *   whenever f holds fp32-representable values (files this library wrote). */
+fasth_status fasth_svd_file_info(const char* path, int* out_dim, int* in_dim, int* nu, int* nv);
+fasth_status fasth_svd_load(fasth_ctx ctx, const char* path, float* U, int64_t ldu, float* V,
+                            int64_t ldv, float* sigma);
+fasth_status fasth_svd_save(fasth_ctx ctx, const fasth_svd_param* p, const char* path);
+
+/* ---- block width (fasth.hpp:147-196, tune_block_width) ----------------------
+ * timed = 0: the reference's analytic choice round(sqrt(d)).  timed != 0:
+ * fasth_forward_backward on a seeded synthetic chain for every candidate in
+ * {2, ..., 2 ceil(sqrt(d))} plus m (when m <= d), timed on the device with
+ * CUDA events; the fastest is cached per (d, m) for the process. */
+fasth_status fasth_tune_block_width(fasth_ctx ctx, int d, int m, int timed, uint64_t seed, int* out);
+
 #ifdef __cplusplus
 }
 #endif

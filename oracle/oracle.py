@@ -218,6 +218,22 @@ class Ref:
                                          _p(X), _p(G)))
         return U, V, s, X, G
 
+    # ---- OSVD files (svd_layer.hpp:204-290) ---------------------------------
+    def svd_save(self, path, U, V, sigma, out_dim, in_dim):
+        U, V, s = _f64(U), _f64(V), _f64(sigma)
+        self._chk(self.lib.ref_svd_save(str(path).encode(), _SZ(out_dim), _SZ(in_dim), _SZ(U.shape[0]),
+                                        _SZ(V.shape[0]), _p(U) if U.size else None, _p(V) if V.size else None,
+                                        _p(s)))
+
+    def svd_load(self, path):
+        dims = (C.c_size_t * 4)()
+        self._chk(self.lib.ref_svd_load(str(path).encode(), dims, None, None, None))
+        out_dim, in_dim, nu, nv = (int(x) for x in dims)
+        U, V, s = np.empty((nu, out_dim)), np.empty((nv, in_dim)), np.empty(min(out_dim, in_dim))
+        self._chk(self.lib.ref_svd_load(str(path).encode(), dims, _p(U) if nu else None, _p(V) if nv else None,
+                                        _p(s)))
+        return out_dim, in_dim, U, V, s
+
     # ---- algorithms -------------------------------------------------------
     def fasth_fwd_bwd(self, V, X, G, b):
         V, X = _f64(V), _f64(X)

@@ -363,4 +363,25 @@ int ref_verify(int* passed, int* total) {
     });
 }
 
+/// save_svd_param_file (svd_layer.hpp:276) of a parameter given as arrays.
+int ref_svd_save(const char* path, std::size_t out, std::size_t in, std::size_t nu, std::size_t nv,
+                 const double* U, const double* V, const double* sigma) {
+    return guarded([&] { save_svd_param_file(param_in(out, in, nu, nv, U, V, sigma), path); });
+}
+
+/// load_svd_param_file (svd_layer.hpp:282): header into dims[4], payload into
+/// U / V / sigma when they are non-null (call once for the dims, then again).
+int ref_svd_load(const char* path, std::size_t* dims, double* U, double* V, double* sigma) {
+    return guarded([&] {
+        SvdParam p = load_svd_param_file(path);
+        dims[0] = p.out_dim;
+        dims[1] = p.in_dim;
+        dims[2] = p.U.size();
+        dims[3] = p.V.size();
+        if (U) chain_out(p.U, U);
+        if (V) chain_out(p.V, V);
+        if (sigma) std::memcpy(sigma, p.sigma.data(), p.sigma.size() * sizeof(double));
+    });
+}
+
 } // extern "C"

@@ -62,6 +62,10 @@ SIGNATURES = {
     "fasth_apply_exponential": (C.c_int, [VP, C.POINTER(SvdParamC), VP, I64, C.c_int, C.c_int, VP,
                                           I64]),
     "fasth_apply_cayley": (C.c_int, [VP, C.POINTER(SvdParamC), VP, I64, C.c_int, C.c_int, VP, I64]),
+    "fasth_svd_file_info": (C.c_int, [C.c_char_p] + [C.POINTER(C.c_int)] * 4),
+    "fasth_svd_load": (C.c_int, [VP, C.c_char_p, VP, I64, VP, I64, VP]),
+    "fasth_svd_save": (C.c_int, [VP, C.POINTER(SvdParamC), C.c_char_p]),
+    "fasth_tune_block_width": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_int)]),
     "fasth_log_abs_det": (C.c_int, [VP, C.POINTER(SvdParamC), C.POINTER(C.c_double)]),
 }
 

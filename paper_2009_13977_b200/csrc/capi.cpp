@@ -12,8 +12,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -272,7 +274,9 @@ int next_pow2_min16(int x) {
 // kernel's shared-memory stages in budget) sub-blocks: the same product.
 int internal_b(int d, int n, int b_user) {
     const int b = std::min(std::max(b_user, 1), n);
-    return std::min(b, d > 1536 ? 32 : kMaxBS);
+    // 64-wide blocks only at d <= 512: beyond it the chain kernel's stages and
+    // exchange slots no longer fit shared memory (same product either way)
+    return std::min(b, d > 512 ? 32 : kMaxBS);
 }
 
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row
@@ -1201,6 +1205,193 @@ fasth_status fasth_log_abs_det(fasth_ctx c, const fasth_svd_param* p, double* ou
     fasth_status s = c->harvest();  // the value is host-visible: always synchronise
     if (s == FASTH_ERR_SINGULAR) return fail(s, "log_abs_det: zero singular value");
     return s;
+}
+
+}  // extern "C"
+
+// ---- OSVD checkpoints (svd_layer.hpp:204-290) --------------------------------
+namespace {
+bool read_u32(std::ifstream& is, uint32_t* x) {
+    is.read(reinterpret_cast<char*>(x), 4);
+    return (bool)is;
+}
+fasth_status read_osvd_header(std::ifstream& is, const char* path, uint32_t h[4]) {
+    char magic[4] = {};
+    is.read(magic, 4);
+    if (!is || std::memcmp(magic, "OSVD", 4) != 0) return fail(FASTH_ERR_INVALID, "load_svd_param: bad magic (%s)", path);
+    uint32_t version = 0;
+    if (!read_u32(is, &version)) return fail(FASTH_ERR_INVALID, "SvdParam load: truncated header");
+    if (version != 1) return fail(FASTH_ERR_INVALID, "load_svd_param: unsupported version %u", version);
+    for (int k = 0; k < 4; ++k)
+        if (!read_u32(is, &h[k])) return fail(FASTH_ERR_INVALID, "SvdParam load: truncated header");
+    if (h[0] == 0 || h[1] == 0) return fail(FASTH_ERR_DIMENSION, "SvdParam: zero dimension");
+    return FASTH_OK;
+}
+}  // namespace
+
+extern "C" {
+
+fasth_status fasth_svd_file_info(const char* path, int* out_dim, int* in_dim, int* nu, int* nv) {
+    if (!path) return fail(FASTH_ERR_INVALID, "null path");
+    std::ifstream is(path, std::ios::binary);
+    if (!is) return fail(FASTH_ERR_INVALID, "load_svd_param_file: cannot open %s", path);
+    uint32_t h[4];
+    TRY(read_osvd_header(is, path, h));
+    if (out_dim) *out_dim = (int)h[0];
+    if (in_dim) *in_dim = (int)h[1];
+    if (nu) *nu = (int)h[2];
+    if (nv) *nv = (int)h[3];
+    return FASTH_OK;
+}
+
+fasth_status fasth_svd_load(fasth_ctx c, const char* path, float* U, int64_t ldu, float* V, int64_t ldv,
+                            float* sigma) {
+    if (!c || !path) return fail(FASTH_ERR_INVALID, "null argument");
+    std::ifstream is(path, std::ios::binary);
+    if (!is) return fail(FASTH_ERR_INVALID, "load_svd_param_file: cannot open %s", path);
+    uint32_t h[4];
+    TRY(read_osvd_header(is, path, h));
+    const int out_dim = (int)h[0], in_dim = (int)h[1], nu = (int)h[2], nv = (int)h[3];
+    const int k = std::min(out_dim, in_dim);
+    TRY(check_mat("svd_load: U", U, ldu, out_dim, nu));
+    TRY(check_mat("svd_load: V", V, ldv, in_dim, nv));
+    if (k && !sigma) return fail(FASTH_ERR_INVALID, "svd_load: null sigma");
+    auto read_vectors = [&](int dim, int n, float* dev, int64_t ld, int chain) -> fasth_status {
+        if (n == 0) return FASTH_OK;
+        std::vector<double> buf((size_t)dim);
+        std::vector<float> host((size_t)dim * n);
+        for (int j = 0; j < n; ++j) {
+            is.read(reinterpret_cast<char*>(buf.data()), (std::streamsize)(dim * sizeof(double)));
+            if (!is) return fail(FASTH_ERR_INVALID, "SvdParam load: truncated payload");
+            double nn = 0.0;
+            bool finite = true;
+            for (int r = 0; r < dim; ++r) {
+                finite = finite && std::isfinite(buf[r]);
+                nn += buf[r] * buf[r];
+                host[(size_t)j * dim + r] = (float)buf[r];
+            }
+            if (!finite) return fail(FASTH_ERR_INVALID, "HouseholderVector: non-finite entry (chain %s vector %d)",
+                                     chain ? "V" : "U", j);
+            if (!(nn > 1e-30))
+                return fail(FASTH_ERR_DEGENERATE, "HouseholderVector: ||v||^2 below degeneracy threshold 1e-30 "
+                            "(chain %s vector %d)", chain ? "V" : "U", j);
+        }
+        CU(cudaMemcpy2DAsync(dev, ld * sizeof(float), host.data(), dim * sizeof(float), dim * sizeof(float), n,
+                             cudaMemcpyHostToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        return FASTH_OK;
+    };
+    TRY(read_vectors(out_dim, nu, U, ldu, 0));
+    TRY(read_vectors(in_dim, nv, V, ldv, 1));
+    if (k) {
+        std::vector<double> sd((size_t)k);
+        is.read(reinterpret_cast<char*>(sd.data()), (std::streamsize)(k * sizeof(double)));
+        if (!is) return fail(FASTH_ERR_INVALID, "SvdParam load: truncated payload");
+        std::vector<float> sf(sd.begin(), sd.end());
+        CU(cudaMemcpyAsync(sigma, sf.data(), k * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+    }
+    return FASTH_OK;
+}
+
+fasth_status fasth_svd_save(fasth_ctx c, const fasth_svd_param* p, const char* path) {
+    if (!c || !path) return fail(FASTH_ERR_INVALID, "null argument");
+    TRY(check_param("save_svd_param", p));
+    const int k = std::min(p->out_dim, p->in_dim);
+    std::vector<float> U((size_t)p->out_dim * p->nu), V((size_t)p->in_dim * p->nv), sg((size_t)k);
+    if (p->nu)
+        CU(cudaMemcpy2DAsync(U.data(), p->out_dim * sizeof(float), p->U, p->ldu * sizeof(float),
+                             p->out_dim * sizeof(float), p->nu, cudaMemcpyDeviceToHost, c->stream));
+    if (p->nv)
+        CU(cudaMemcpy2DAsync(V.data(), p->in_dim * sizeof(float), p->V, p->ldv * sizeof(float),
+                             p->in_dim * sizeof(float), p->nv, cudaMemcpyDeviceToHost, c->stream));
+    if (k) CU(cudaMemcpyAsync(sg.data(), p->sigma, k * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    std::ofstream os(path, std::ios::binary);
+    if (!os) return fail(FASTH_ERR_INVALID, "save_svd_param_file: cannot open %s", path);
+    os.write("OSVD", 4);
+    const uint32_t h[5] = {1u, (uint32_t)p->out_dim, (uint32_t)p->in_dim, (uint32_t)p->nu, (uint32_t)p->nv};
+    os.write(reinterpret_cast<const char*>(h), sizeof(h));
+    auto put = [&](const std::vector<float>& v) {
+        std::vector<double> d(v.begin(), v.end());
+        os.write(reinterpret_cast<const char*>(d.data()), (std::streamsize)(d.size() * sizeof(double)));
+    };
+    put(U);
+    put(V);
+    put(sg);
+    if (!os) return fail(FASTH_ERR_INVALID, "save_svd_param: write failure");
+    return FASTH_OK;
+}
+
+fasth_status fasth_tune_block_width(fasth_ctx c, int d, int m, int timed, uint64_t seed, int* out) {
+    if (!c || !out || d < 1 || m < 0) return fail(FASTH_ERR_INVALID, "fasth_tune_block_width: bad argument");
+    if (!timed) {  // fasth.hpp:149-152
+        *out = std::max(1, (int)std::lround(std::sqrt((double)d)));
+        return FASTH_OK;
+    }
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find({d, m});
+        if (it != cache.end()) {
+            *out = it->second;
+            return FASTH_OK;
+        }
+    }
+    // seeded synthetic chain and data (fasth.hpp:163-174), fp32 on the device
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    const int mm = std::max(m, 1);
+    std::vector<float> hv((size_t)d * d), hx((size_t)d * mm), hg((size_t)d * mm);
+    for (auto& x : hv) x = (float)gauss(rng);
+    for (auto& x : hx) x = (float)gauss(rng);
+    for (auto& x : hg) x = (float)gauss(rng);
+    float *v = nullptr, *x = nullptr, *g = nullptr, *y = nullptr, *dx = nullptr, *dv = nullptr;
+    TRY(c->alloc_n(hv.size(), &v));
+    TRY(c->alloc_n(hx.size(), &x));
+    TRY(c->alloc_n(hx.size(), &g));
+    TRY(c->alloc_n(hx.size(), &y));
+    TRY(c->alloc_n(hx.size(), &dx));
+    TRY(c->alloc_n(hv.size(), &dv));
+    CU(cudaMemcpyAsync(v, hv.data(), hv.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(x, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(g, hg.data(), hg.size() * 4, cudaMemcpyHostToDevice, c->stream));
+    std::vector<int> cand;
+    const int root = (int)std::ceil(std::sqrt((double)d));
+    for (int b = 2; b <= 2 * root && b <= d; ++b) cand.push_back(b);
+    if (m >= 1 && m <= d) cand.push_back(m);
+    if (cand.empty()) cand.push_back(1);
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    const int saved = c->check_mode;
+    c->check_mode = FASTH_CHECK_DEFERRED;
+    int best = cand.front();
+    float best_ms = -1.f;
+    fasth_status s = FASTH_OK;
+    for (int b : cand) {
+        for (int rep = 0; rep < 2 && s == FASTH_OK; ++rep) {  // warm, then timed
+            CU(cudaEventRecord(e0, c->stream));
+            s = fasth_forward_backward(c, v, d, d, d, x, d, g, d, mm, b, y, d, dx, d, dv, d);
+            CU(cudaEventRecord(e1, c->stream));
+        }
+        if (s != FASTH_OK) break;
+        CU(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        if (best_ms < 0.f || ms < best_ms) best_ms = ms, best = b;
+    }
+    c->check_mode = saved;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (float* ptr : {v, x, g, y, dx, dv}) c->release(ptr);
+    TRY(s);
+    TRY(c->harvest());
+    std::lock_guard<std::mutex> lk(mu);
+    cache[{d, m}] = best;
+    *out = best;
+    return FASTH_OK;
 }
 
 }  // extern "C"

@@ -456,3 +456,44 @@ def log_abs_det(p: SvdParam, *, ctx=None) -> float:
     out = C.c_double()
     _check(c.lib.fasth_log_abs_det(c.h, C.byref(pc), C.byref(out)))
     return out.value
+
+
+# ---- OSVD checkpoints (svd_layer.hpp:204-290) -----------------------------
+
+
+def svd_file_info(path: str) -> tuple[int, int, int, int]:
+    """(out_dim, in_dim, nU, nV) of an OSVD file (header only)."""
+    h = [C.c_int() for _ in range(4)]
+    _check(_lib.load().fasth_svd_file_info(str(path).encode(), *[C.byref(x) for x in h]))
+    return tuple(x.value for x in h)
+
+
+def load_svd_param_file(path: str, *, device: int | None = None, ctx: Context | None = None) -> SvdParam:
+    """svd_layer.hpp:282 — the checkpoint straight into device buffers (fp32)."""
+    out_dim, in_dim, nu, nv = svd_file_info(path)
+    c = ctx if ctx is not None else default_context(device)
+    c.bind_stream()
+    dev = torch.device("cuda", c.device)
+    U = torch.empty((nu, out_dim), dtype=torch.float32, device=dev)
+    V = torch.empty((nv, in_dim), dtype=torch.float32, device=dev)
+    sigma = torch.empty((min(out_dim, in_dim),), dtype=torch.float32, device=dev)
+    _check(c.lib.fasth_svd_load(c.h, str(path).encode(), _ptr(U), out_dim, _ptr(V), in_dim, _ptr(sigma)))
+    return SvdParam(out_dim, in_dim, U, V, sigma)
+
+
+def save_svd_param_file(p: SvdParam, path: str, *, ctx: Context | None = None):
+    """svd_layer.hpp:276 — the device parameter written as the reference's f64 OSVD file."""
+    pc = p._c()
+    c = _ctx(ctx, p.sigma)
+    _check(c.lib.fasth_svd_save(c.h, C.byref(pc), str(path).encode()))
+
+
+def tune_block_width(d: int, m: int, timed: bool = False, seed: int = 0x5EED, *,
+                     ctx: Context | None = None) -> int:
+    """fasth.hpp:147 — analytic round(sqrt(d)), or the fastest block width of a
+    timed search on the device (cached per (d, m))."""
+    c = ctx if ctx is not None else default_context()
+    c.bind_stream()
+    out = C.c_int()
+    _check(c.lib.fasth_tune_block_width(c.h, int(d), int(m), 1 if timed else 0, int(seed), C.byref(out)))
+    return out.value

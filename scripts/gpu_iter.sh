@@ -1,5 +1,5 @@
 mkdir -p gpurun_out/it
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/it/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/it/pytest_gpu.log
-tail -n 2 gpurun_out/it/pytest_gpu.log
-FASTH_TRACE=gpurun_out/it/w python scripts/trace_fused.py > /dev/null 2>&1; python scripts/trace_report.py "gpurun_out/it/w.sweep(fwd+bwd).warps.bin" 2>&1 | head -5
-timeout 300 python bench.py --steps 100 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; l=json.loads(sys.stdin.read()); print(l['value'], l['two_call_us_per_step'], l['e2e']['value'], l['kernel_us'], l['parity_max_rel_err'])"
+tail -n 15 gpurun_out/it/pytest_gpu.log
+python tools/fasth_bench_b200.py --d 256:256:4 --reps 20 --algo fasth,ref-fasth 2>&1 | tail -12
+python tools/fasth_bench_b200.py --d 784 --reps 20 --op layer --k 32 2>&1 | tail -3
