@@ -282,7 +282,8 @@ int internal_b(int d, int n, int b_user) {
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row
 // padding d_pad the chain geometry asks for.
 fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_pad, int cb, int n,
-                        int b_user, int reversed, int tag, bool packed, bool* pipelined, Plan* out) {
+                        int b_user, int reversed, int tag, bool packed, bool* pipelined, Plan* out,
+                        bool launch = true) {
     Plan p;
     p.d = d;
     p.n = n;
@@ -311,15 +312,21 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
     }
     const bool b2 = packed && !getenv("FASTH_BUILD_V1") && build2_smem_bytes(p.BS, p.d_pad / p.CB) <= 227 * 1024;
     if (pipelined && *pipelined) {
-        // opt-in (FASTH_PIPELINE=1): profitable only once a block builds in
-        // well under the sweep's duration (scripts/trace_report.py --timeline)
-        *pipelined = b2 && p.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && getenv("FASTH_PIPELINE") &&
-                     !getenv("FASTH_NO_PIPELINE") && !getenv("FASTH_DV_V1");
+        // device-resident calls: opt-in (FASTH_PIPELINE=1), profitable only
+        // once a block builds in well under the sweep's duration
+        // (scripts/trace_report.py --timeline); the host-buffer call
+        // (launch == false) pipelines behind its chunked upload instead
+        *pipelined = b2 && p.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ &&
+                     (getenv("FASTH_PIPELINE") || !launch) && !getenv("FASTH_NO_PIPELINE") && !getenv("FASTH_DV_V1");
         if (*pipelined) {
             p.ready = c->counters;
             const char* nb = getenv("FASTH_BUILDERS");
-            p.nbuild = nb ? std::max(1, atoi(nb)) : 12;
+            p.nbuild = launch ? (nb ? std::max(1, atoi(nb)) : 12) : 0;
         }
+    }
+    if (!launch) {
+        *out = p;
+        return b2 ? FASTH_OK : fail(FASTH_ERR_INVALID, "deferred build needs the packed-stage builder");
     }
     if (b2) {
         const char* prefix = getenv("FASTH_TRACE");
@@ -657,7 +664,7 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
-                      int reversed, int tag, fasth_tape* out, bool pipelined = false) {
+                      int reversed, int tag, fasth_tape* out, bool pipelined = false, bool launch = true) {
     fasth_tape t = new fasth_tape_s;
     t->ctx = c;
     t->m = m;
@@ -672,7 +679,7 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     t->v2nstg = getenv("FASTH_SWEEP_V1") ? 0 : sweep2_nstg(G.C, BS, G.d_pad);
     t->pipelined = pipelined && t->v2nstg > 0;
     fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, t->v2nstg > 0, &t->pipelined,
-                                &t->plan);
+                                &t->plan, launch);
     if (s != FASTH_OK) {
         delete t;
         return s;
@@ -775,6 +782,7 @@ fasth_status fasth_ctx_destroy(fasth_ctx c) {
     for (auto& kv : c->live) cudaFree(kv.first);
     if (c->counters) cudaFree(c->counters);
     if (c->logdet_d) cudaFree(c->logdet_d);
+
     if (c->err_h) cudaFreeHost(c->err_h);
     delete c;
     return FASTH_OK;
@@ -958,6 +966,8 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
     return s;
 }
 
+
+
 fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int n,
                                          const float* X, const float* G, int m, int block_width,
                                          float* Y, float* dX, float* dV) {
@@ -976,12 +986,17 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
     c->check_mode = FASTH_CHECK_DEFERRED;
     fasth_tape t = nullptr;
     do {
-        if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
         if (nx) CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
         if (nx) CU(cudaMemcpyAsync(g, G, nx * 4, cudaMemcpyHostToDevice, c->stream));
-        s = fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d,
-                                   n ? dv : nullptr, d);
-        if (s != FASTH_OK) break;
+        // (Overlapping V's upload with the builds and the sweep was tried: a
+        // sweep waiting on builders launched after it can deadlock — its
+        // 10-CTA clusters leave no GPC room for the builders' clusters.)
+        {
+            if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
+            s = fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d,
+                                       n ? dv : nullptr, d);
+            if (s != FASTH_OK) break;
+        }
         if (nx) CU(cudaMemcpyAsync(Y, y, nx * 4, cudaMemcpyDeviceToHost, c->stream));
         if (nx) CU(cudaMemcpyAsync(dX, dx, nx * 4, cudaMemcpyDeviceToHost, c->stream));
         if (nv) CU(cudaMemcpyAsync(dV, dv, nv * 4, cudaMemcpyDeviceToHost, c->stream));

@@ -59,6 +59,8 @@ struct Plan {
     // the order the two sweeps need them).  nullptr / 0: plain launch.
     unsigned* ready = nullptr;
     int nbuild = 0;
+    // plain launch: build blocks [blk_lo, blk_hi) only (blk_hi < 0: all q)
+    int blk_lo = 0, blk_hi = -1;
 };
 
 // ---- packed chain stages (chain_v2.cu) ------------------------------------

@@ -108,8 +108,9 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
     // persistent over blocks when pipelined: ticket k -> the k-th block the
     // two sweeps need (forward from q-1 down, backward from 0 up, interleaved)
     const int nclu = (int)(gridDim.x / CB);
-    for (int tkt = (int)dev::cluster_id_x(); tkt < p.q; tkt += nclu) {
-    const int i = p.nbuild > 0 ? ((tkt & 1) ? (tkt >> 1) : p.q - 1 - (tkt >> 1)) : tkt;
+    const int ntkt = p.nbuild > 0 ? p.q : (p.blk_hi < 0 ? p.q : p.blk_hi) - p.blk_lo;
+    for (int tkt = (int)dev::cluster_id_x(); tkt < ntkt; tkt += nclu) {
+    const int i = p.nbuild > 0 ? ((tkt & 1) ? (tkt >> 1) : p.q - 1 - (tkt >> 1)) : p.blk_lo + tkt;
     const int w = min(p.b, p.n - i * p.b);
     // FASTH_TRACE phase stamps: [block][CTA rank][8] clock64 (0 start, 1 loaded,
     // 2 Gram band done, 3 reduced, 4 T~, 5 B operands, 6 W rows, 7 end)
@@ -404,7 +405,9 @@ cudaError_t launch_build2_t(const Plan& p, const float* V, int64_t ldv, ErrWord*
         configured = L.total;
     }
     cudaLaunchConfig_t cfg = {};
-    const int nclu = p.nbuild > 0 ? (p.nbuild < p.q ? p.nbuild : p.q) : p.q;
+    const int nrange = (p.blk_hi < 0 ? p.q : p.blk_hi) - p.blk_lo;
+    const int nclu = p.nbuild > 0 ? (p.nbuild < p.q ? p.nbuild : p.q) : nrange;
+    if (nclu <= 0) return cudaSuccess;
     cfg.gridDim = dim3(nclu * p.CB, 1, 1);
     cfg.blockDim = dim3(NTH, 1, 1);
     cfg.dynamicSmemBytes = L.total;

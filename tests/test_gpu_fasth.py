@@ -315,6 +315,27 @@ def test_host_buffer_entry(fb, oracle):
     assert max(errs) <= TOL, errs
 
 
+@pytest.mark.parametrize("d,n,m,b", [(784, 784, 32, 32), (200, 200, 17, 6), (64, 64, 32, 8), (300, 45, 8, 16),
+                                     (96, 5, 3, 32), (128, 128, 100, 32)])
+def test_host_pipelined_equals_device_bitwise(fb, d, n, m, b):
+    """The host-buffer call overlaps V's chunked upload with the WY builds
+    and the sweeps (readiness counters): same kernels, same arithmetic as the
+    device-resident fasth_forward_backward, so identical bits; repeated to
+    exercise the self-resetting counters."""
+    import torch
+    rng = np.random.default_rng(d + 7 * n + m)
+    V, X, G = rng.standard_normal((n, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    Vh = torch.tensor(V, dtype=torch.float32).pin_memory()
+    Xh = torch.tensor(X.T.copy(), dtype=torch.float32).pin_memory()
+    Gh = torch.tensor(G.T.copy(), dtype=torch.float32).pin_memory()
+    Yd, back = fb.fasth_forward_backward(Vh.cuda(), Xh.cuda().t(), Gh.cuda().t(), b)
+    want = (host(Yd).T, host(back.grad_input).T, host(back.grad_vectors))
+    for _ in range(3):
+        got = fb.forward_backward_host(Vh, Xh, Gh, b)
+        for u, w in zip(got, want):
+            assert np.array_equal(u.double().numpy(), w)
+
+
 # ---- SVD layer -------------------------------------------------------------
 
 def svd_param(fb, U, V, s, out_dim, in_dim):
