@@ -70,8 +70,8 @@ struct B2Smem {
         vt = o;   o += (size_t)3 * BS * P * 4;                 // V^T rows of blocks i, i-1, i+1
         gp = o;   o += (size_t)BS * BS * 8 + 2 * BS * BS * 4;  // partial band: G_ii f64 | G_off f32
         gr = o;   o += (size_t)BS * BS * 8 + 2 * BS * BS * 4;  // reduced band
-        t = o;    o += (size_t)BS * BS * 4;                    // T~ (f32, row-major)
-        bn = o;   o += (size_t)2 * (BS / 8) * (BS / 8) * 128 * 4;  // T~^T, T~ pre-split B operands
+        t = bn = o;  // rinv (BS) + M2 (BS x BS), fp32
+        o += (size_t)(BS + BS * BS) * 4;
         total = o;
         // [Wf | Sf^T] and [Wb | Sb^T] rows (pitch BS+4) alias blocks i-1, i+1
         // and the partial band, all dead by then
@@ -95,8 +95,6 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
     float* Gpo = reinterpret_cast<float*>(smem + L.gp + (size_t)BS * BS * 8);
     double* Gr = reinterpret_cast<double*>(smem + L.gr);
     float* Gro = reinterpret_cast<float*>(smem + L.gr + (size_t)BS * BS * 8);
-    float* Tf = reinterpret_cast<float*>(smem + L.t);
-    float* Bn = reinterpret_cast<float*>(smem + L.bn);
     float* Wsm = reinterpret_cast<float*>(smem + L.ws);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
@@ -244,16 +242,15 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
     dev::cluster_sync();
     BTRACE(3);
 
-    // 4. degeneracy (rank 0 reports) and T~ = M^{-1}, M = diag(G) + 2 striu(G),
-    //    by one warp in f64: lane j back-substitutes column j (right-looking:
-    //    after T[k][j] is known, acc[r] += M[r][k] T[k][j] for r < k)
-    // rinv[k] = 1 / G_kk and M2[r][k] = 2 G_rk (f64), in the dead partial band
-    double* rinv = reinterpret_cast<double*>(smem + L.gp);
-    double* M2 = rinv + BS;
-    for (int idx = tid; idx < BS * BS; idx += NTH) M2[idx] = 2.0 * Gr[idx];
+    // 4. degeneracy (rank 0 reports); rinv[k] = 1 / G_kk and M2[r][k] = 2 G_rk
+    //    (M = diag(G) + 2 striu(G)), rounded to fp32, in their own region (the
+    //    staging rows of step 5 alias the partial band)
+    float* rinv = reinterpret_cast<float*>(smem + L.t);
+    float* M2 = rinv + BS;
+    for (int idx = tid; idx < BS * BS; idx += NTH) M2[idx] = (float)(2.0 * Gr[idx]);
     if (tid < BS) {
         const double gjj = Gr[tid * BS + tid];
-        rinv[tid] = tid < w ? 1.0 / gjj : 0.0;
+        rinv[tid] = tid < w ? (float)(1.0 / gjj) : 0.f;
         if (rank == 0 && tid < w && (!(gjj > 1e-30) || !isfinite(gjj))) {
             atomicOr(&err->flags, isfinite(gjj) ? kErrDegenerate : kErrNonFinite);
             const int kc = i * p.b + tid;
@@ -262,77 +259,56 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
         }
     }
     __syncthreads();
-    if (warp == 0) {
-        const int col = lane;
-        double acc[BS];
-#pragma unroll
-        for (int r = 0; r < BS; ++r) acc[r] = 0.0;
-#pragma unroll
-        for (int k = BS - 1; k >= 0; --k) {
-            // T[k][col]: zero below the diagonal and outside the block width
-            const double t = (k <= col && col < w) ? ((k == col ? 1.0 : 0.0) - acc[k]) * rinv[k] : 0.0;
-            if (col < BS) Tf[k * BS + col] = (float)t;
-#pragma unroll
-            for (int r = 0; r < k; ++r) acc[r] = fma(M2[r * BS + k], t, acc[r]);
-        }
-    }
-    __syncthreads();
     BTRACE(4);
-    // T~ (fp32) -> pre-split B operands: Bn[0] = T~^T (Wf = V T~^T), Bn[1] = T~ (Wb = V T~)
-    for (int idx = tid; idx < 2 * BS * BS; idx += NTH) {
-        const int which = idx / (BS * BS), e = idx - which * BS * BS;
-        const int a1 = e / BS, a2 = e - a1 * BS;  // consecutive threads: consecutive Tf
-        const int k = which == 0 ? a2 : a1, j = which == 0 ? a1 : a2;  // B[k][j]
-        const float v = Tf[a1 * BS + a2];  // which 0: T~[j][k]; 1: T~[k][j]
-        const int ks = k >> 3, k_in = k & 7, nt = j >> 3;
-        float* pb = Bn + (((size_t)which * KB + ks) * NT + nt) * 128 + ((j & 7) * 4 + (k_in & 3)) * 4;
-        const uint32_t hb = hi_rn(v);
-        pb[(k_in >> 2) & 1] = __uint_as_float(hb);
-        pb[2 + ((k_in >> 2) & 1)] = v - __uint_as_float(hb);
-    }
-    if (rank == 0)
-        for (int idx = tid; idx < BS * BS; idx += NTH) p.Tt[(size_t)i * BS * BS + idx] = Tf[idx];
-    __syncthreads();
-    BTRACE(5);
 
-    // 5. [V rows ; G_{i,i+1}^T] T~^T = [Wf ; Sf^T] and [V rows ; G_{i,i-1}^T] T~ = [Wb ; Sb^T]
-    //    (Sf = T~ G_{i,i+1} = Wf^T V_{i+1}, Sb = T~^T G_{i,i-1} = Wb^T V_{i-1})
+    // 5. one row per thread, triangular solves in f64 (T~ = M^{-1} never formed):
+    //      Wf = V T~^T  <=>  w M^T = v   (back substitution)
+    //      Wb = V T~    <=>  w M   = v   (forward substitution)
+    //    on the rows of V, of G_{i,i+1}^T (-> Sf^T = G_{i,i+1}^T T~^T, i.e.
+    //    Sf = T~ G_{i,i+1} = Wf^T V_{i+1}) and of G_{i,i-1}^T (-> Sb^T), plus
+    //    (rank 0) the unit rows for T~^T (diagnostics).  Right-looking: once
+    //    w_j is known, its column updates the remaining right-hand sides, all
+    //    independent FMAs.  fp32 arithmetic on the f64-reduced Gram (B200's
+    //    FP64 vector rate made an f64 solve ~9 us per block).
+    BTRACE(5);
     {
-        const int RT = RB / 16 + BS / 16;  // row tiles incl. the S^T rows
-        for (int u = warp; u < 2 * RT; u += NTH / 32) {
-            const int which = u / RT, rt = u % RT;
-            const bool srow = rt >= RB / 16;
-            float m[NT][4], c[NT][4];
+        const int ntask = 2 * (RB + BS) + (rank == 0 ? BS : 0);
+        for (int task = tid; task < ntask; task += NTH) {
+            // tasks: [0, RB+BS) forward chain rows (V then G_{i,i+1}^T), then
+            // [RB+BS, 2(RB+BS)) backward rows (V then G_{i,i-1}^T), then T~^T rows
+            const bool fwd = task < RB + BS || task >= 2 * (RB + BS);
+            const int row = task < RB + BS ? task : (task < 2 * (RB + BS) ? task - (RB + BS) : task - 2 * (RB + BS));
+            const bool trow = task >= 2 * (RB + BS);
+            float acc[BS];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
+            for (int c = 0; c < BS; ++c) {
+                float v;
+                if (trow) v = (c == row) ? 1.f : 0.f;
+                else if (row < RB) v = Vc[(size_t)c * P + row];
+                else v = Gro[(fwd ? 0 : BS * BS) + c * BS + (row - RB)];  // G_off^T row = G_off column
+                acc[c] = v;
+            }
+            // results straight out: the staging row, or (T~^T rows) column `row` of T~
+            float* wr = trow ? p.Tt + (size_t)i * BS * BS + row
+                             : Wsm + (size_t)(fwd ? 0 : 1) * (RB + BS) * LDS_ + (size_t)row * LDS_;
+            const int ws = trow ? BS : 1;
+            if (fwd) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) m[nt][e] = c[nt][e] = 0.f;
+                for (int j = BS - 1; j >= 0; --j) {
+                    const float wj = j < w ? acc[j] * rinv[j] : 0.f;
+                    wr[j * ws] = wj;
 #pragma unroll
-            for (int ks = 0; ks < KB; ++ks) {
-                AF af;
-                if (!srow) {  // A = V rows: A[r][l] = Vc[l][r]
-                    const float* a = Vc + (size_t)(ks * 8 + tq) * P + rt * 16 + g;
-                    af = split4(a[0], a[8], a[4 * P], a[4 * P + 8]);
-                } else {  // A = G_off^T: A[k][l] = G_off[l][k]
-                    const float* go = Gro + which * BS * BS;
-                    const int k0 = (rt - RB / 16) * 16 + g, l0 = ks * 8 + tq;
-                    af = split4(go[l0 * BS + k0], go[l0 * BS + k0 + 8], go[(l0 + 4) * BS + k0],
-                                go[(l0 + 4) * BS + k0 + 8]);
+                    for (int r = 0; r < j; ++r) acc[r] = fmaf(-M2[r * BS + j], wj, acc[r]);
                 }
+            } else {
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    const float4 b = *reinterpret_cast<const float4*>(Bn + (((size_t)which * KB + ks) * NT + nt) * 128 + lane * 4);
-                    hmma(m[nt], af.h[0], af.h[1], af.h[2], af.h[3], __float_as_uint(b.x), __float_as_uint(b.y));
-                    hmma(c[nt], af.h[0], af.h[1], af.h[2], af.h[3], __float_as_uint(b.z), __float_as_uint(b.w));
-                    hmma(c[nt], af.l[0], af.l[1], af.l[2], af.l[3], __float_as_uint(b.x), __float_as_uint(b.y));
+                for (int j = 0; j < BS; ++j) {
+                    const float wj = j < w ? acc[j] * rinv[j] : 0.f;
+                    wr[j * ws] = wj;
+#pragma unroll
+                    for (int r = j + 1; r < BS; ++r) acc[r] = fmaf(-M2[j * BS + r], wj, acc[r]);
                 }
             }
-            float* wr = Wsm + (size_t)which * (RB + BS) * LDS_;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    wr[(rt * 16 + g + 8 * (e >> 1)) * LDS_ + nt * 8 + 2 * tq + (e & 1)] = m[nt][e] + c[nt][e];
         }
     }
     __syncthreads();
