@@ -274,9 +274,10 @@ int next_pow2_min16(int x) {
 // kernel's shared-memory stages in budget) sub-blocks: the same product.
 int internal_b(int d, int n, int b_user) {
     const int b = std::min(std::max(b_user, 1), n);
-    // 64-wide blocks only at d <= 512: beyond it the chain kernel's stages and
-    // exchange slots no longer fit shared memory (same product either way)
-    return std::min(b, d > 512 ? 32 : kMaxBS);
+    // 64-wide blocks only at d <= 512, 16-wide beyond d = 2048: past those
+    // sizes the chain kernel's stages and exchange slots no longer fit shared
+    // memory (the same product either way)
+    return std::min(b, d > 2048 ? 16 : d > 512 ? 32 : kMaxBS);
 }
 
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row

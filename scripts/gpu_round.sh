@@ -1,11 +1,19 @@
+# Round evidence: GPU parity tests, bench (+ reference arm), launch list and
+# ncu --set full of each kernel, secondary configs.  Outputs in gpurun_out/round/.
 set -x
-mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
-timeout 600 python bench.py > gpurun_out/bench.log 2>&1
-timeout 300 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 20 -c 2 -o gpurun_out/sweep_full python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_full.log 2>&1
-timeout 600 python scripts/bench_configs.py --quick > gpurun_out/configs.log 2>&1
-tail -3 gpurun_out/*.log
+mkdir -p gpurun_out/round
+R=gpurun_out/round
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $R/smi.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q --timeout 240 > $R/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $R/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $R/smoke.log 2>&1
+timeout 600 python bench.py > $R/bench.log 2>&1
+timeout 300 python bench.py --impl reference --steps 10 --warmup 3 > $R/bench_ref.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $R/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > $R/b_ncu.log 2>&1
+for k in sweep2 build2 dv2; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 -o $R/${k}_full python bench.py --steps 2 --warmup 3 --no-cpu > $R/ncu_$k.log 2>&1
+done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:panel -s 2 -c 1 -o $R/panel_full python scripts/bench_config5.py --m-per-gpu 1024 --steps 1 --warmup 1 > $R/ncu_panel.log 2>&1
+for m in 1024 8192; do timeout 300 python scripts/bench_config5.py --m-per-gpu $m --steps 3 --warmup 1 >> $R/config5.log 2>&1; done
+timeout 900 python scripts/bench_configs.py > $R/configs.log 2>&1
+timeout 300 python tools/fasth_bench_b200.py --d 256:256:4 --reps 20 --algo fasth,ref-fasth > $R/cli_mul.csv 2>&1
+ls -la $R
