@@ -11,7 +11,8 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfasth_b200.so")
+# FASTH_LIB selects an alternative in-tree build (tuning variants under lib/variants/)
+LIB_PATH = os.environ.get("FASTH_LIB") or os.path.join(HERE, "lib", "libfasth_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fasth_b200.h")
 
 FP = C.POINTER(C.c_float)

@@ -6,6 +6,7 @@
 // CUDA device is usable.
 #include "fasth_b200.h"
 #include "fasth_internal.h"
+#include "lb.h"
 
 #include <algorithm>
 #include <cmath>
@@ -939,6 +940,37 @@ fasth_status fasth_tape_info(fasth_tape t, int* d, int* n, int* m, int* block_wi
     return FASTH_OK;
 }
 
+// Large-batch path (lb.h): the chain re-blocked into 512-wide WY blocks, every
+// step a tcgen05 GEMM.  Chosen when the batch is wide enough for the GEMMs to
+// fill the GPU (m >= 1024 here; FASTH_LB=0/1 forces the choice) and the shapes
+// meet its alignment (n a multiple of 128, d and m multiples of 4).
+bool use_large_batch(int d, int n, int m, const float* Y, int64_t ldy, const float* dX, int64_t lddx) {
+    if (!fasthb::lb::supported(d, n, m)) return false;
+    if (!dX || (ldy % 4) || (lddx % 4) || (reinterpret_cast<uintptr_t>(Y) & 15) ||
+        (reinterpret_cast<uintptr_t>(dX) & 15))
+        return false;
+    if (const char* e = getenv("FASTH_LB")) return atoi(e) != 0;
+    return m >= 1024 && d >= 512;
+}
+
+fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx,
+                             const float* G, int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx,
+                             float* dV, int64_t lddv) {
+    float* ws = nullptr;
+    TRY(c->alloc_n(fasthb::lb::workspace_floats(d, n, m, dV != nullptr), &ws));
+    int nl = 1;
+    fasth_status s = c->timed(
+        [&] {
+            return fasthb::lb::forward_backward(V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy, dX, lddx, dV, lddv, ws,
+                                                c->err_d, c->stream, c->num_sms, &nl);
+        },
+        "large_batch(fwd+bwd)");
+    c->launches += nl - 1;
+    c->release(ws);  // pool reuse is stream ordered
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
 fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, int d, int n,
                                     const float* X, int64_t ldx, const float* G, int64_t ldg,
                                     int m, int block_width, float* Y, int64_t ldy, float* dX,
@@ -959,6 +991,8 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
         free_tape(t);
         return s;
     }
+    if (use_large_batch(d, n, m, Y, ldy, dX, lddx)) return run_large_batch(c, V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy,
+                                                                         dX, lddx, dV, lddv);
     fasth_tape t = nullptr;
     TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr));
     fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);

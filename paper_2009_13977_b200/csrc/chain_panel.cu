@@ -24,8 +24,14 @@ namespace fasthb {
 namespace {
 using namespace fo;
 
-constexpr int PWARPS = 8;  // warps per CTA
-constexpr int PNT = 2;     // n-tiles per panel
+#ifndef PANEL_WARPS
+#define PANEL_WARPS 8
+#endif
+#ifndef PANEL_NT
+#define PANEL_NT 2
+#endif
+constexpr int PWARPS = PANEL_WARPS;  // warps per CTA
+constexpr int PNT = PANEL_NT;        // n-tiles per panel
 constexpr int PCOLS = 8 * PNT;
 constexpr int PRING = 3;   // per-warp ring depth (row-tile operand chunks)
 constexpr int PBS = 32;    // block width handled (MT = 2, KB = 4)

@@ -1,0 +1,98 @@
+// Large-batch path (internal, non-ABI): FastH re-blocked into wide WY blocks
+// so that every chain step is a large GEMM on the 5th-generation tensor cores.
+//
+// Memory is batch-major, as the C ABI hands it over (column-major d x m:
+// sample c is the contiguous row X[c][0..d)).  With B-wide blocks
+// (B in {512, 256, 128}, vectors jB..jB+B-1 of the chain) and
+//   WfR_j = T~_j V_j,  WbR_j = T~_j^T V_j      (B x d; V_j = the block's rows)
+// one forward block step is, for the m x d activations Xm,
+//   ZfT = Xm WfR_j^T            (m x B)   GEMM  M=m N=B K=d
+//   Xm <- Xm - 2 ZfT VT_j^T     (m x d)   GEMM  M=m N=d K=B  (VT = V^T, d x n)
+// and one backward step, for the m x d gradient Gm and the block's output
+// activations Am (the forward tape),
+//   ZbT = Gm WbR_j^T
+//   Q   = Zf Zb^T               (B x B)   GEMM  K=m (Zf, Zb: the B x m copies)
+//   dV_j = -2 (Zb Am + Zf Gm) - 4 K'^T V_j,   K' = striu(Q - Q^T)
+//   Gm <- Gm - 2 ZbT VT_j^T
+// — exactly tests/algo_model.py's algebra with block width B (the product is
+// independent of the blocking; the reference's own results agree across block
+// widths to 1e-10).
+//
+// Every operand of every product is stored pre-split for 3xTF32 (hi = RN to
+// tf32, lo = x - hi, both fp32 containers); the GEMM epilogues emit the split
+// form of whatever feeds a later product.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "fasth_internal.h"
+
+namespace fasthb {
+namespace lb {
+
+constexpr int BM = 128;   // UMMA M (one CTA, cta_group::1)
+constexpr int BN = 256;   // UMMA N
+constexpr int BK = 32;    // K per stage: one 128-byte swizzle atom of fp32
+constexpr int STAGES = 2;
+
+struct Operand {          // row-major matrix of fp32, pre-split
+    const float* hi = nullptr;
+    const float* lo = nullptr;
+    int64_t rows = 0, cols = 0, ld = 0;
+};
+
+struct Segment {          // one K range of the product
+    Operand A;            // M x K, K contiguous (K-major)
+    Operand B;            // N x K (K-major) or K x N (MN-major)
+    int K = 0;
+    int a_row0 = 0, a_col0 = 0;   // A coordinates of (m = 0, k = 0)
+    int b_row0 = 0, b_col0 = 0;   // B coordinates of (n = 0, k = 0) / (k = 0, n = 0)
+};
+
+struct Gemm {
+    int M = 0, N = 0;
+    int nseg = 1;
+    Segment seg[3];
+    bool b_mn = false;    // B stored K x N (N contiguous)
+    int ksplit = 1;       // > 1 (or partial != nullptr): raw partials per K split
+    int nz = 1;           // batched products, coordinates advance per z:
+    int z_a_row = 0, z_a_col = 0, z_b_row = 0, z_b_col = 0;
+    int64_t z_out = 0;    // output element offset per z (direct and partial outputs)
+    float alpha = 1.f, beta = 0.f;
+    // epilogue (direct): D = alpha acc + beta (C_hi + C_lo)
+    const float *c_hi = nullptr, *c_lo = nullptr;
+    int64_t ldc = 0;
+    float* d_f32 = nullptr;
+    int64_t ldd = 0;
+    float *d_hi = nullptr, *d_lo = nullptr;
+    int64_t lds = 0;
+    float *t_hi = nullptr, *t_lo = nullptr;  // transposed split copy D^T (N x M)
+    int64_t ldt = 0;
+    float* partial = nullptr;                // [nz][ksplit][M][N]
+    int debug_swap = 0;                      // test hook: MN-major LBO/SBO swap
+};
+
+// One launch of the persistent tcgen05 3xTF32 GEMM.  g.ksplit is updated to the
+// split count actually used (no empty K splits).
+cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms);
+
+// The whole large-batch step (lb_run.cu).
+int pick_block(int n);
+bool supported(int d, int n, int m);
+size_t workspace_floats(int d, int n, int m, bool want_dv);
+cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
+                             int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
+                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch);
+
+// Elementwise helpers (lb_path.cu).
+// split rows x cols (ld_in) into hi/lo (ld_out)
+cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, float* lo,
+                  int64_t ldo, cudaStream_t s);
+// VT = V^T split: V is n x d (ldv), VT d x n
+cudaError_t split_transpose(const float* v, int64_t ldv, int n, int d, float* hi, float* lo,
+                            int64_t ldo, cudaStream_t s);
+
+}  // namespace lb
+}  // namespace fasthb

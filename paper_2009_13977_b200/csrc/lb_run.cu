@@ -1,0 +1,466 @@
+// Large-batch FastH step (forward + backward) on the tcgen05 GEMM — see lb.h
+// for the algebra.  Block j covers chain vectors [jB, jB+B); the forward
+// applies blocks nb-1 .. 0 (H_n first, as the reference's fasth.hpp:40 chain),
+// the backward walks 0 .. nb-1.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "lb.h"
+
+namespace fasthb {
+namespace lb {
+namespace {
+
+__device__ __forceinline__ float rn_hi(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
+// M_z = diag(G_z) + 2 striu(G_z), G_z = sum of the ks Gram partials
+// (flags a degenerate / non-finite ||v_i||^2 like the block builder)
+__global__ void gram_reduce_kernel(const float* __restrict__ part, int ks, int B, int nz, float* __restrict__ Mm,
+                                   ErrWord* err) {
+    const int64_t per = (int64_t)B * B, total = per * nz;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = e / per, w = e % per;
+        const int i = (int)(w / B), j = (int)(w % B);
+        float g = 0.f;
+        if (j >= i)
+            for (int s = 0; s < ks; ++s) g += part[(z * ks + s) * per + w];
+        Mm[e] = j > i ? 2.f * g : (j == i ? g : 0.f);
+        if (j == i && (!(g > 1e-30f) || !isfinite(g))) {
+            atomicOr(&err->flags, isfinite(g) ? kErrDegenerate : kErrNonFinite);
+            atomicMin(&err->index, (int)(z * B + i));
+            err->chain = 0;
+        }
+    }
+}
+
+// Inverses of the 32 x 32 diagonal blocks of M_z (upper triangular), lane =
+// column of the inverse, back substitution.  grid (B/32, nz), 32 threads.
+__global__ void diag_inv_kernel(const float* __restrict__ Mm, int B, float* __restrict__ Dinv) {
+    __shared__ float U[32][33];
+    const int rc = blockIdx.x, z = blockIdx.y, lane = threadIdx.x;
+    const float* M = Mm + (int64_t)z * B * B + (int64_t)rc * 32 * B + rc * 32;
+    for (int i = 0; i < 32; ++i) U[i][lane] = M[(int64_t)i * B + lane];
+    __syncwarp();
+    float x[32];
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+        float s = i == lane ? 1.f : 0.f;
+#pragma unroll
+        for (int k = i + 1; k < 32; ++k) s = fmaf(-U[i][k], x[k], s);
+        x[i] = s / U[i][i];
+    }
+    float* D = Dinv + ((int64_t)z * (B / 32) + rc) * 1024;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) D[i * 32 + lane] = x[i];
+}
+
+// T_z = M_z^{-1} by blocked back-substitution over 32-row chunks:
+//   T[rc][cc] = Dinv_rc (E - sum_{k > rc} M[rc][k] T[k][cc]).
+// One CTA per pair of 32-column chunks (cc, B/32-1-cc) for balanced work;
+// the M row panel of each step is staged in shared memory (coalesced).  Writes
+// T and T^T, both split.  grid (B/64, nz), 256 threads.
+__global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ Mm, const float* __restrict__ Dinv,
+                                                      int B, float* __restrict__ Th, float* __restrict__ Tl,
+                                                      float* __restrict__ TTh, float* __restrict__ TTl) {
+    extern __shared__ float sm[];
+    float* Tc = sm;                // [B][32] solution chunk
+    float* R = Tc + B * 32;        // [32][33] right-hand side
+    float* Mp = R + 32 * 33;       // [32][B] staged row panel (pitch B + 4)
+    const int MP = B + 4;
+    const int z = blockIdx.y, nchunk = B / 32;
+    const float* M = Mm + (int64_t)z * B * B;
+    const int tid = threadIdx.x;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int cc = pass == 0 ? blockIdx.x : nchunk - 1 - blockIdx.x;
+        const int c0 = cc * 32;
+        __syncthreads();
+        for (int e = tid; e < B * 32; e += 256) Tc[e] = 0.f;
+        __syncthreads();
+        for (int rc = cc; rc >= 0; --rc) {
+            const int r0 = rc * 32, k0 = (rc + 1) * 32, k1 = c0 + 32;
+            for (int e = tid; e < 32 * (k1 - k0); e += 256) {
+                const int i = e / (k1 - k0), k = k0 + e % (k1 - k0);
+                Mp[i * MP + k] = M[(int64_t)(r0 + i) * B + k];
+            }
+            __syncthreads();
+            {
+                const int r = tid >> 3, c4 = (tid & 7) * 4;
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                for (int k = k0; k < k1; ++k) {
+                    const float mv = Mp[r * MP + k];
+                    const float4 t = *reinterpret_cast<const float4*>(Tc + k * 32 + c4);
+                    a0 = fmaf(mv, t.x, a0);
+                    a1 = fmaf(mv, t.y, a1);
+                    a2 = fmaf(mv, t.z, a2);
+                    a3 = fmaf(mv, t.w, a3);
+                }
+                const int gr = r0 + r;
+                R[r * 33 + c4 + 0] = (gr == c0 + c4 + 0 ? 1.f : 0.f) - a0;
+                R[r * 33 + c4 + 1] = (gr == c0 + c4 + 1 ? 1.f : 0.f) - a1;
+                R[r * 33 + c4 + 2] = (gr == c0 + c4 + 2 ? 1.f : 0.f) - a2;
+                R[r * 33 + c4 + 3] = (gr == c0 + c4 + 3 ? 1.f : 0.f) - a3;
+            }
+            __syncthreads();
+            {
+                const int r = tid >> 3, c4 = (tid & 7) * 4;
+                const float* D = Dinv + ((int64_t)z * nchunk + rc) * 1024 + r * 32;
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 8
+                for (int k = r; k < 32; ++k) {  // Dinv upper triangular
+                    const float dv = __ldg(D + k);
+                    a0 = fmaf(dv, R[k * 33 + c4 + 0], a0);
+                    a1 = fmaf(dv, R[k * 33 + c4 + 1], a1);
+                    a2 = fmaf(dv, R[k * 33 + c4 + 2], a2);
+                    a3 = fmaf(dv, R[k * 33 + c4 + 3], a3);
+                }
+                *reinterpret_cast<float4*>(Tc + (r0 + r) * 32 + c4) = make_float4(a0, a1, a2, a3);
+            }
+            __syncthreads();
+        }
+        float* th = Th + (int64_t)z * B * B;
+        float* tl = Tl + (int64_t)z * B * B;
+        float* tth = TTh + (int64_t)z * B * B;
+        float* ttl = TTl + (int64_t)z * B * B;
+        for (int e = tid; e < B * 32; e += 256) {
+            const int r = e >> 5, c = e & 31;
+            const float v = Tc[e];
+            const float h = rn_hi(v);
+            th[(int64_t)r * B + c0 + c] = h;
+            tl[(int64_t)r * B + c0 + c] = v - h;
+        }
+        for (int e = tid; e < B * 32; e += 256) {
+            const int c = e / B, r = e % B;  // coalesced along r
+            const float v = Tc[r * 32 + c];
+            const float h = rn_hi(v);
+            tth[(int64_t)(c0 + c) * B + r] = h;
+            ttl[(int64_t)(c0 + c) * B + r] = v - h;
+        }
+    }
+}
+
+// S = 2 K'^T (the dV product's alpha = -2 makes it -4 K'^T), K' = striu(Q - Q^T),
+// Q = sum of ks partials (B x B); split.
+// 32 x 32 tiles: the (a, b) and (b, a) tiles are summed into shared memory
+// with coalesced reads.  grid (B/32, B/32), 32 x 8 threads.
+__global__ void q_reduce_kernel(const float* __restrict__ part, int ks, int B, float* __restrict__ Sh,
+                                float* __restrict__ Sl) {
+    __shared__ float qt[32][33], qtt[32][33];
+    const int64_t per = (int64_t)B * B;
+    const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32, tx = threadIdx.x;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        float s1 = 0.f, s2 = 0.f;
+        for (int k = 0; k < ks; ++k) {
+            s1 += part[k * per + (int64_t)(a0 + r) * B + b0 + tx];  // Q[a0+r][b0+tx]
+            s2 += part[k * per + (int64_t)(b0 + r) * B + a0 + tx];  // Q[b0+r][a0+tx]
+        }
+        qt[r][tx] = s1;
+        qtt[r][tx] = s2;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int a = a0 + r, b = b0 + tx;
+        const float v = b < a ? 2.f * (qtt[tx][r] - qt[r][tx]) : 0.f;  // 2 (Q[b][a] - Q[a][b])
+        const float h = rn_hi(v);
+        Sh[(int64_t)a * B + b] = h;
+        Sl[(int64_t)a * B + b] = v - h;
+    }
+}
+
+// dV rows (B x d) = sum of ks partials
+__global__ void dv_reduce_kernel(const float* __restrict__ part, int ks, int B, int d, float* __restrict__ dV,
+                                 int64_t lddv) {
+    const int64_t per = (int64_t)B * d;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int k = 0; k < ks; ++k) s += part[k * per + e];
+        dV[(e / d) * lddv + e % d] = s;
+    }
+}
+
+int grid_for(int64_t work) { return (int)std::min<int64_t>((work + 255) / 256, 148 * 16); }
+
+}  // namespace
+
+int pick_block(int n) {
+    for (int B : {512, 256, 128})
+        if (n % B == 0) return B;
+    return 0;
+}
+
+bool supported(int d, int n, int m) {
+    return d >= 128 && d % 4 == 0 && n >= 128 && pick_block(n) > 0 && m >= 128 && m % 4 == 0;
+}
+
+size_t workspace_floats(int d, int n, int m, bool want_dv) {
+    const int B = pick_block(n), nb = n / B;
+    const size_t nd = (size_t)n * d, md = (size_t)m * d, bb = (size_t)B * B;
+    size_t f = 0;
+    f += 4 * nd;                    // V, V^T split
+    f += (size_t)nb * 4 * bb;       // Gram partials (ks <= 4)
+    f += (size_t)nb * bb;           // M
+    f += (size_t)nb * 32 * B;       // diagonal block inverses
+    f += 4 * (size_t)nb * bb;       // T, T^T split
+    f += 4 * nd;                    // WfR, WbR split
+    f += 2 * (size_t)(nb + 1) * md;  // forward stages split
+    f += 2 * (size_t)m * B * 2;     // ZfT, ZbT split
+    f += 2 * (size_t)n * m;         // Zf (natural, all blocks) split
+    f += 2 * (size_t)B * m;         // Zb natural split
+    f += 4 * md;                    // two gradient buffers split
+    if (want_dv) {
+        f += 16 * bb + 2 * bb;      // Q partials, S split
+        f += 8 * (size_t)B * d;     // dV partials
+    }
+    return f + 256 * 32;            // alignment slack
+}
+
+struct Carver {
+    float* p;
+    float* take(size_t n) {
+        float* r = p;
+        p += (n + 31) / 32 * 32;  // 128-byte aligned pieces
+        return r;
+    }
+};
+
+cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
+                             int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
+                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch) {
+    int nl = 0;
+    const int B = pick_block(n), nb = n / B;
+    const bool want_dv = dV != nullptr;
+    if (!B || !supported(d, n, m)) return cudaErrorInvalidValue;
+    if ((ldy % 4) || (lddx % 4) || (reinterpret_cast<uintptr_t>(Y) & 15) || (reinterpret_cast<uintptr_t>(dX) & 15))
+        return cudaErrorInvalidValue;
+    const size_t nd = (size_t)n * d, md = (size_t)m * d, bb = (size_t)B * B;
+    Carver c{ws};
+    float *Vh = c.take(nd), *Vl = c.take(nd), *VTh = c.take(nd), *VTl = c.take(nd);
+    const int ksG = 4;
+    float* Gp = c.take((size_t)nb * ksG * bb);
+    float* Mm = c.take((size_t)nb * bb);
+    float* Dinv = c.take((size_t)nb * 32 * B);
+    float *Th = c.take(nb * bb), *Tl = c.take(nb * bb), *TTh = c.take(nb * bb), *TTl = c.take(nb * bb);
+    float *WfH = c.take(nd), *WfL = c.take(nd), *WbH = c.take(nd), *WbL = c.take(nd);
+    float *Sth[64], *Stl[64];
+    if (nb + 1 > 64) return cudaErrorInvalidValue;
+    for (int j = 0; j <= nb; ++j) {
+        Sth[j] = c.take(md);
+        Stl[j] = c.take(md);
+    }
+    float *ZfTh = c.take((size_t)m * B), *ZfTl = c.take((size_t)m * B);
+    float *ZbTh = c.take((size_t)m * B), *ZbTl = c.take((size_t)m * B);
+    float *Zfh = c.take((size_t)n * m), *Zfl = c.take((size_t)n * m);
+    float *Zbh = c.take((size_t)B * m), *Zbl = c.take((size_t)B * m);
+    float *Gh[2] = {c.take(md), c.take(md)}, *Gl[2] = {c.take(md), c.take(md)};
+    const int ksQ = 16, ksV = 4;  // 128 CTAs each: one tile per CTA, dual accumulators
+    float *Qp = nullptr, *Sh = nullptr, *Sl = nullptr, *dVp = nullptr;
+    if (want_dv) {
+        Qp = c.take(ksQ * bb);
+        Sh = c.take(bb);
+        Sl = c.take(bb);
+        dVp = c.take((size_t)(ksV + 1) * B * d);
+    }
+    cudaError_t e;
+#define LBTRY(x)                            \
+    do {                                    \
+        if ((e = (x)) != cudaSuccess) return e; \
+    } while (0)
+    // ---- build: split V and V^T, Gram per block, T~, WfR = T~ V_j, WbR = T~^T V_j
+    ++nl;
+    LBTRY(split(V, ldv, n, d, Vh, Vl, d, s));
+    ++nl;
+    LBTRY(split_transpose(V, ldv, n, d, VTh, VTl, n, s));
+    int g_ks = ksG;
+    {
+        Gemm g;
+        g.M = g.N = B;
+        g.seg[0].A = Operand{Vh, Vl, n, d, d};
+        g.seg[0].B = Operand{Vh, Vl, n, d, d};
+        g.seg[0].K = d;
+        g.nz = nb;
+        g.z_a_row = B;
+        g.z_b_row = B;
+        g.partial = Gp;
+        g.ksplit = ksG;
+        LBTRY(gemm(g, s, num_sms));
+        ++nl;
+        g_ks = g.ksplit;
+    }
+    ++nl;
+    gram_reduce_kernel<<<grid_for(nb * bb), 256, 0, s>>>(Gp, g_ks, B, nb, Mm, err);
+    {
+        ++nl;
+        diag_inv_kernel<<<dim3(B / 32, nb), 32, 0, s>>>(Mm, B, Dinv);
+        const int smem = (B * 32 + 32 * 33 + 32 * (B + 4)) * 4;
+        static int attr = 0;
+        if (attr < smem) {
+            LBTRY(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            attr = smem;
+        }
+        ++nl;
+        tri_inv_kernel<<<dim3(B / 64, nb), 256, smem, s>>>(Mm, Dinv, B, Th, Tl, TTh, TTl);
+        LBTRY(cudaGetLastError());
+    }
+    for (int w = 0; w < 2; ++w) {  // WfR = T V_j, WbR = T^T V_j  (B x d per block)
+        Gemm g;
+        g.M = B;
+        g.N = d;
+        g.seg[0].A = w == 0 ? Operand{Th, Tl, (int64_t)nb * B, B, B} : Operand{TTh, TTl, (int64_t)nb * B, B, B};
+        g.seg[0].B = Operand{VTh, VTl, d, n, n};  // (n = d index, k = chain index) K-major
+        g.seg[0].K = B;
+        g.nz = nb;
+        g.z_a_row = B;
+        g.z_b_col = B;
+        g.z_out = B;
+        g.d_hi = w == 0 ? WfH : WbH;
+        g.d_lo = w == 0 ? WfL : WbL;
+        g.lds = d;
+        LBTRY(gemm(g, s, num_sms));
+        ++nl;
+    }
+    // ---- forward: stage nb = split X; stage j = output of block j
+    ++nl;
+    LBTRY(split(X, ldx, m, d, Sth[nb], Stl[nb], d, s));
+    for (int j = nb - 1; j >= 0; --j) {
+        {
+            Gemm g;  // ZfT = A WfR_j^T (m x B), Zf_j = its transpose (B x m)
+            g.M = m;
+            g.N = B;
+            g.seg[0].A = Operand{Sth[j + 1], Stl[j + 1], m, d, d};
+            g.seg[0].B = Operand{WfH, WfL, n, d, d};
+            g.seg[0].b_row0 = j * B;
+            g.seg[0].K = d;
+            g.d_hi = ZfTh;
+            g.d_lo = ZfTl;
+            g.lds = B;
+            g.t_hi = Zfh + (size_t)j * B * m;
+            g.t_lo = Zfl + (size_t)j * B * m;
+            g.ldt = m;
+            LBTRY(gemm(g, s, num_sms));
+        ++nl;
+        }
+        {
+            Gemm g;  // A_j = A_{j+1} - 2 ZfT VT_j^T
+            g.M = m;
+            g.N = d;
+            g.seg[0].A = Operand{ZfTh, ZfTl, m, B, B};
+            g.seg[0].B = Operand{VTh, VTl, d, n, n};
+            g.seg[0].b_col0 = j * B;
+            g.seg[0].K = B;
+            g.alpha = -2.f;
+            g.beta = 1.f;
+            g.c_hi = Sth[j + 1];
+            g.c_lo = Stl[j + 1];
+            g.ldc = d;
+            g.d_hi = Sth[j];
+            g.d_lo = Stl[j];
+            g.lds = d;
+            if (j == 0) {
+                g.d_f32 = Y;
+                g.ldd = ldy;
+            }
+            LBTRY(gemm(g, s, num_sms));
+        ++nl;
+        }
+    }
+    // ---- backward
+    ++nl;
+    LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s));
+    int cur = 0;
+    for (int j = 0; j < nb; ++j) {
+        {
+            Gemm g;  // ZbT = G WbR_j^T, Zb = transpose
+            g.M = m;
+            g.N = B;
+            g.seg[0].A = Operand{Gh[cur], Gl[cur], m, d, d};
+            g.seg[0].B = Operand{WbH, WbL, n, d, d};
+            g.seg[0].b_row0 = j * B;
+            g.seg[0].K = d;
+            g.d_hi = ZbTh;
+            g.d_lo = ZbTl;
+            g.lds = B;
+            g.t_hi = Zbh;
+            g.t_lo = Zbl;
+            g.ldt = m;
+            LBTRY(gemm(g, s, num_sms));
+        ++nl;
+        }
+        if (want_dv) {
+            int q_ks = ksQ, v_ks = ksV;
+            {
+                Gemm g;  // Q = Zf_j Zb^T (split K)
+                g.M = g.N = B;
+                g.seg[0].A = Operand{Zfh, Zfl, n, m, m};
+                g.seg[0].a_row0 = j * B;
+                g.seg[0].B = Operand{Zbh, Zbl, B, m, m};
+                g.seg[0].K = m;
+                g.partial = Qp;
+                g.ksplit = ksQ;
+                LBTRY(gemm(g, s, num_sms));
+        ++nl;
+                q_ks = g.ksplit;
+            }
+            ++nl;
+    q_reduce_kernel<<<dim3(B / 32, B / 32), dim3(32, 8), 0, s>>>(Qp, q_ks, B, Sh, Sl);
+            {
+                Gemm g;  // dV_j partials = -2 (Zb A_j + Zf_j G) + S V_j   (S = -4 K'^T pre-scaled by -1/2)
+                g.M = B;
+                g.N = d;
+                g.nseg = 3;
+                g.b_mn = true;
+                g.seg[0].A = Operand{Zbh, Zbl, B, m, m};
+                g.seg[0].B = Operand{Sth[j], Stl[j], m, d, d};
+                g.seg[0].K = m;
+                g.seg[1].A = Operand{Zfh, Zfl, n, m, m};
+                g.seg[1].a_row0 = j * B;
+                g.seg[1].B = Operand{Gh[cur], Gl[cur], m, d, d};
+                g.seg[1].K = m;
+                g.seg[2].A = Operand{Sh, Sl, B, B, B};
+                g.seg[2].B = Operand{Vh, Vl, n, d, d};  // V_j rows: K x N, N contiguous
+                g.seg[2].b_row0 = j * B;
+                g.seg[2].K = B;
+                g.alpha = -2.f;
+                g.partial = dVp;
+                g.ksplit = ksV;
+                LBTRY(gemm(g, s, num_sms));
+        ++nl;
+                v_ks = g.ksplit;
+            }
+            ++nl;
+    dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, s>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv,
+                                                                       lddv);
+        }
+        {
+            Gemm g;  // G <- G - 2 ZbT VT_j^T
+            g.M = m;
+            g.N = d;
+            g.seg[0].A = Operand{ZbTh, ZbTl, m, B, B};
+            g.seg[0].B = Operand{VTh, VTl, d, n, n};
+            g.seg[0].b_col0 = j * B;
+            g.seg[0].K = B;
+            g.alpha = -2.f;
+            g.beta = 1.f;
+            g.c_hi = Gh[cur];
+            g.c_lo = Gl[cur];
+            g.ldc = d;
+            g.d_hi = Gh[cur ^ 1];
+            g.d_lo = Gl[cur ^ 1];
+            g.lds = d;
+            if (j == nb - 1) {
+                g.d_f32 = dX;
+                g.ldd = lddx;
+            }
+            LBTRY(gemm(g, s, num_sms));
+        ++nl;
+        }
+        cur ^= 1;
+    }
+#undef LBTRY
+    if (nlaunch) *nlaunch = nl;
+    return cudaGetLastError();
+}
+
+}  // namespace lb
+}  // namespace fasthb

@@ -73,7 +73,8 @@ def main():
     if rank == 0:
         print(json.dumps({"config": 5, "d": d, "b": b, "m_per_gpu": m, "global_batch": m * world, "n_gpus": world,
                           "us_per_step": ms * 1e3, "tflops": tf, "frac_3xtf32_peak": tf / peak,
-                          "scaling": "weak", "data": "synthetic N(0,1) on device"}))
+                          "scaling": "weak", "data": "synthetic N(0,1) on device",
+                          "path": {"0": "chain/panel", "1": "large_batch"}.get(os.environ.get("FASTH_LB", ""), "auto")}))
     if world > 1:
         dist.destroy_process_group()
 

@@ -1,0 +1,128 @@
+"""Large-batch path (csrc/lb_*.cu): the chain re-blocked into wide WY blocks
+on the tcgen05 3xTF32 GEMM.  Checked against a float64 restatement of the
+blocked algebra (tests/algo_model.py's, in torch on the GPU so that the
+reference-scale shapes finish in milliseconds) and against the chain path."""
+import ctypes as C
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4  # north_star: max relative error on UX, dX, dV
+
+
+def model64(V, X, G, B):
+    """tests/algo_model.fwd_bwd in float64 torch.  V: (n, d); X, G: (d, m)."""
+    V, X, G = V.double(), X.double(), G.double()
+    n, d = V.shape
+    Vt = V.t()
+    bl = [(lo, min(lo + B, n)) for lo in range(0, n, B)]
+    Ts = []
+    for lo, hi in bl:
+        Vb = Vt[:, lo:hi]
+        Gm = Vb.t() @ Vb
+        M = torch.diag(torch.diag(Gm)) + 2 * torch.triu(Gm, 1)
+        Ts.append(torch.linalg.inv(M))
+    A = X.clone()
+    acts, zf = [None] * len(bl), [None] * len(bl)
+    for i in reversed(range(len(bl))):
+        lo, hi = bl[i]
+        Vb = Vt[:, lo:hi]
+        Zp = Ts[i] @ (Vb.t() @ A)
+        A = A - 2 * Vb @ Zp
+        acts[i], zf[i] = A, Zp
+    Y = A
+    Gs = G.clone()
+    dV = torch.zeros_like(V)
+    for i in range(len(bl)):
+        lo, hi = bl[i]
+        Vb = Vt[:, lo:hi]
+        Zb = Ts[i].t() @ (Vb.t() @ Gs)
+        Q = zf[i] @ Zb.t()
+        Kp = torch.triu(Q - Q.t(), 1)
+        dV[lo:hi] = (-2 * (acts[i] @ Zb.t() + Gs @ zf[i].t() + 2 * Vb @ Kp)).t()
+        Gs = Gs - 2 * Vb @ Zb
+    return Y, Gs, dV
+
+
+def rel(a, b):
+    return float((a.double() - b).norm() / b.norm())
+
+
+def inputs(n, d, m, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    V = torch.randn(n, d, device="cuda", generator=g)
+    X = torch.randn(m, d, device="cuda", generator=g).t()
+    G = torch.randn(m, d, device="cuda", generator=g).t()
+    return V, X, G
+
+
+@pytest.mark.parametrize("n,d,m", [(512, 512, 1024), (1024, 1024, 2048), (384, 256, 640), (2048, 2048, 4096)])
+def test_large_batch_matches_f64(n, d, m, monkeypatch):
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.setenv("FASTH_LB", "1")
+    V, X, G = inputs(n, d, m)
+    ctx = fb.Context(0)
+    n0 = ctx.launch_count
+    Y, back = fb.fasth_forward_backward(V, X, G, 32, ctx=ctx)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count - n0
+    Yr, dXr, dVr = model64(V, X, G, 64)
+    errs = (rel(Y, Yr), rel(back.grad_input, dXr), rel(back.grad_vectors, dVr))
+    print(f"n={n} d={d} m={m}: rel err Y {errs[0]:.2e} dX {errs[1]:.2e} dV {errs[2]:.2e}, {launches} launches")
+    assert launches > 10  # the multi-kernel large-batch step ran, not the chain sweep
+    assert max(errs) <= TOL, errs
+
+
+def test_large_batch_agrees_with_chain_path(monkeypatch):
+    from paper_2009_13977_b200 import fasth as fb
+    V, X, G = inputs(1024, 1024, 1024, seed=3)
+    monkeypatch.setenv("FASTH_LB", "1")
+    Y1, b1 = fb.fasth_forward_backward(V, X, G, 32)
+    monkeypatch.setenv("FASTH_LB", "0")
+    Y0, b0 = fb.fasth_forward_backward(V, X, G, 32)
+    torch.cuda.synchronize()
+    for a, b in ((Y1, Y0), (b1.grad_input, b0.grad_input), (b1.grad_vectors, b0.grad_vectors)):
+        assert rel(a, b.double()) <= TOL
+
+
+def test_large_batch_degenerate_vector_reported(monkeypatch):
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.setenv("FASTH_LB", "1")
+    V, X, G = inputs(512, 512, 1024, seed=5)
+    V[300].zero_()
+    with pytest.raises(fb.DegenerateVectorError) as ei:
+        fb.fasth_forward_backward(V, X, G, 32, ctx=fb.Context(0))
+    assert "300" in str(ei.value)
+
+
+def test_gemm_hook_tcgen05():
+    """The GEMM alone (K-major and MN-major B, transposed output, split K)."""
+    from paper_2009_13977_b200 import _lib
+    lib = _lib.load()
+    f = lib.fasthb_lb_gemm_test
+    P, I64, I, F = C.c_void_p, C.c_int64, C.c_int, C.c_float
+    f.argtypes = [P, I64, P, I64, I, I, I, I, P, I64, F, F, P, I64, P, P, I64, P, P, I64, P, I, I]
+    f.restype = I
+    p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for M, N, K, mn in ((256, 512, 256, 0), (200, 300, 100, 0), (256, 512, 256, 1), (384, 768, 96, 1)):
+        A = torch.randn(M, K, device="cuda", generator=g)
+        B = torch.randn(K, N, device="cuda", generator=g) if mn else torch.randn(N, K, device="cuda", generator=g)
+        Cm = torch.randn(M, N, device="cuda", generator=g)
+        ref = -2.0 * (A.double() @ (B.double() if mn else B.double().t())) + Cm.double()
+        D = torch.zeros(M, N, device="cuda")
+        assert f(p(A), K, p(B), N if mn else K, mn, M, N, K, p(Cm), N, -2.0, 1.0, p(D), N, None, None, N, None,
+                 None, M, None, 1, 0) == 0
+        assert rel(D, ref) < 1e-5
+        Th, Tl = torch.zeros(N, M, device="cuda"), torch.zeros(N, M, device="cuda")
+        part = torch.zeros(3, M, N, device="cuda")
+        ref2 = A.double() @ (B.double() if mn else B.double().t())
+        assert f(p(A), K, p(B), N if mn else K, mn, M, N, K, None, N, 1.0, 0.0, None, N, None, None, N, p(Th),
+                 p(Tl), M, None, 1, 0) == 0
+        assert rel((Th.double() + Tl.double()).t(), ref2) < 1e-5
+        if K >= 96:
+            assert f(p(A), K, p(B), N if mn else K, mn, M, N, K, None, N, 1.0, 0.0, None, N, None, None, N, None,
+                     None, M, p(part), 3, 0) == 0
+            assert rel(part.sum(0), ref2) < 1e-5
