@@ -19,6 +19,8 @@
 // Tiles (z, split, n, m) are dealt round-robin over the persistent CTAs, m
 // fastest, so CTAs running together share the B tile in L2.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "lb.h"
@@ -37,7 +39,7 @@ constexpr int TMEM_COLS = 512;
 
 struct Params {
     CUtensorMap ta_hi[3], ta_lo[3], tb_hi[3], tb_lo[3];
-    int M, N, nseg, ksplit, nz, mt, nt, total, kb_per_split;
+    int M, N, nseg, ksplit, nz, mt, nt, total, kb_per_split, tile_m;
     int nkb[3], tot_kb;
     int a_row0[3], a_col0[3], b_row0[3], b_col0[3];
     int z_a_row, z_a_col, z_b_row, z_b_col;
@@ -68,6 +70,7 @@ __device__ __forceinline__ void mb_expect(uint32_t a, uint32_t bytes) {
 __device__ __forceinline__ void mb_arrive(uint32_t a) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
+#ifndef LB_HANG_DEBUG
 __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
     asm volatile(
         "{\n.reg .pred P;\nLW_%=:\n"
@@ -76,12 +79,51 @@ __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#else  // bounded wait: report the stuck barrier and trap (debug builds only)
+__device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
+    for (long long i = 0;; ++i) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred P;\nmbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\nselp.u32 %0, 1, 0, P;\n}\n"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (i == (1ll << 22)) {
+            uint32_t rk;
+            asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rk));
+            printf("LB hang: block %d rank %u warp %d lane %d bar 0x%x parity %u\n", blockIdx.x, rk,
+                   (int)(threadIdx.x >> 5), (int)(threadIdx.x & 31), a, parity);
+            __trap();
+        }
+    }
+}
+#endif
+template <bool PAIR>
 __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            dst),
-        "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
-        : "memory");
+    if constexpr (PAIR)  // the mbarrier may sit in the peer (leader) CTA
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                dst),
+            "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+            : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                dst),
+            "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar)
+            : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
+    uint32_t o;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(rank));
+    return o;
+}
+__device__ __forceinline__ void mb_arrive_cluster(uint32_t a) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // UMMA shared-memory descriptor, sm_100 version field = 1.  layout 2: 128-byte
 // swizzle (K-major operands); layout 1: 128-byte swizzle with 32-byte atoms, the
@@ -90,16 +132,33 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (layout << 61);
 }
+template <bool PAIR>
 __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
+    if constexpr (PAIR)
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
+    else
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+            "l"(a), "l"(b), "r"(idesc), "r"(acc)
+            : "memory");
 }
+// commit: arrive on `bar` once the issued MMAs complete (both CTAs of a pair)
+template <bool PAIR>
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
+    if constexpr (PAIR)
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                bar),
+            "h"((uint16_t)3)
+            : "memory");
+    else
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                     : "memory");
 }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -135,33 +194,50 @@ __device__ __forceinline__ TileInfo decode(const Params& p, int t) {
     r /= p.nt;
     ti.split = r % p.ksplit;
     ti.z = r / p.ksplit;
-    ti.m0 = mi * BM;
+    ti.m0 = mi * p.tile_m;
     ti.n0 = ni * BN;
     ti.kb_lo = ti.split * p.kb_per_split;
     ti.kb_hi = min(p.tot_kb, ti.kb_lo + p.kb_per_split);
     return ti;
 }
 
-template <bool B_MN>
+template <bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Params p) {
+    // PAIR: a 2-CTA cluster runs one 256 x 256 tile with tcgen05.mma.cta_group::2;
+    // each CTA loads its 128 A rows and its half (128 rows) of the B tile
+    constexpr int CM = PAIR ? 2 : 1;
+    constexpr int BNC = BN / CM;                // B rows (N) per CTA
+    constexpr int B_T = BNC * BK * 4;
+    constexpr int STG = 2 * A_TILE + 2 * B_T;   // 96 KB single, 64 KB pair
+    constexpr int NST = PAIR ? 3 : 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    float* epi = reinterpret_cast<float*>(smem + STAGES * STAGE);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE + EPI_BYTES);
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
-    const uint32_t full0 = su32(bars), empty0 = su32(bars + STAGES);
-    const uint32_t tfull0 = su32(bars + 2 * STAGES), tempty0 = su32(bars + 2 * STAGES + 2);
+    float* epi = reinterpret_cast<float*>(smem + NST * STG);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NST * STG + EPI_BYTES);
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * NST + 4);
+    const uint32_t full0 = su32(bars), empty0 = su32(bars + NST);
+    const uint32_t tfull0 = su32(bars + 2 * NST), tempty0 = su32(bars + 2 * NST + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool dual = p.total <= (int)gridDim.x;  // one tile per CTA: both accumulators on it
+    uint32_t rank = 0;
+    if constexpr (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const bool leader = rank == 0;
+    const int cid = PAIR ? (int)blockIdx.x / 2 : (int)blockIdx.x;
+    const int ncl = PAIR ? (int)gridDim.x / 2 : (int)gridDim.x;
+    const bool dual = p.total <= ncl;  // one tile per CTA (pair): both accumulators on it
+#ifdef LB_HANG_DEBUG
+    if (PAIR && threadIdx.x == 0 && blockIdx.x < 2)
+        printf("LB pair: block %d rank %u full0 0x%x mapa0 0x%x mapa1 0x%x\n", blockIdx.x, rank, su32(smem),
+               mapa_u32(su32(smem), 0), mapa_u32(su32(smem), 1));
+#endif
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mb_init(full0 + 8 * s, 1);
             mb_init(empty0 + 8 * s, 1);
         }
         for (int a = 0; a < 2; ++a) {
             mb_init(tfull0 + 8 * a, 1);
-            mb_init(tempty0 + 8 * a, 4);
+            mb_init(tempty0 + 8 * a, 4 * CM);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int sg = 0; sg < p.nseg; ++sg) {
@@ -172,13 +248,23 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         }
     }
     if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_holder)),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
     }
     fence_before();
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync();
+    else
+        __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_holder;
 
@@ -186,7 +272,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         // ---------------- TMA producer ----------------
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = blockIdx.x; t < p.total; t += gridDim.x) {
+        for (int t = cid; t < p.total; t += ncl) {
             const TileInfo ti = decode(p, t);
             for (int kb = ti.kb_lo; kb < ti.kb_hi; ++kb) {
                 int sg = 0, kbase = 0;
@@ -194,41 +280,42 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 const int k0 = (kb - kbase) * BK;
                 if (lane == 0) {
                     mb_wait(empty0 + 8 * stage, phase ^ 1);
-                    const uint32_t fb = full0 + 8 * stage;
-                    mb_expect(fb, STAGE);
-                    const uint32_t base = su32(smem + stage * STAGE);
-                    const int ar = p.a_row0[sg] + ti.z * p.z_a_row + ti.m0;
+                    uint32_t fb = full0 + 8 * stage;
+                    if (leader) mb_expect(fb, STG * CM);  // the pair's bytes land on the leader's barrier
+                    if constexpr (PAIR) fb = (p.debug_swap & 4) ? (fb & 0xFEFFFFFFu) : mapa_u32(fb, 0);
+                    const uint32_t base = su32(smem + stage * STG);
+                    const int ar = p.a_row0[sg] + ti.z * p.z_a_row + ti.m0 + (int)rank * BM;
                     const int ac = p.a_col0[sg] + ti.z * p.z_a_col + k0;
-                    tma2d(base, &p.ta_hi[sg], ac, ar, fb);
-                    tma2d(base + A_TILE, &p.ta_lo[sg], ac, ar, fb);
+                    tma2d<PAIR>(base, &p.ta_hi[sg], ac, ar, fb);
+                    tma2d<PAIR>(base + A_TILE, &p.ta_lo[sg], ac, ar, fb);
                     if constexpr (!B_MN) {
-                        const int br = p.b_row0[sg] + ti.z * p.z_b_row + ti.n0;
+                        const int br = p.b_row0[sg] + ti.z * p.z_b_row + ti.n0 + (int)rank * BNC;
                         const int bc = p.b_col0[sg] + ti.z * p.z_b_col + k0;
-                        tma2d(base + 2 * A_TILE, &p.tb_hi[sg], bc, br, fb);
-                        tma2d(base + 2 * A_TILE + B_TILE, &p.tb_lo[sg], bc, br, fb);
+                        tma2d<PAIR>(base + 2 * A_TILE, &p.tb_hi[sg], bc, br, fb);
+                        tma2d<PAIR>(base + 2 * A_TILE + B_T, &p.tb_lo[sg], bc, br, fb);
                     } else {
-                        // K x N storage: 8 boxes of (32 n) x (32 k), chunk c at c * 4 KB
+                        // K x N storage: boxes of (32 n) x (32 k), chunk c at c * 4 KB
                         const int br = p.b_row0[sg] + ti.z * p.z_b_row + k0;
-                        const int bc = p.b_col0[sg] + ti.z * p.z_b_col + ti.n0;
+                        const int bc = p.b_col0[sg] + ti.z * p.z_b_col + ti.n0 + (int)rank * BNC;
 #pragma unroll
-                        for (int c = 0; c < BN / 32; ++c) {
-                            tma2d(base + 2 * A_TILE + c * (BK * 128), &p.tb_hi[sg], bc + 32 * c, br, fb);
-                            tma2d(base + 2 * A_TILE + B_TILE + c * (BK * 128), &p.tb_lo[sg], bc + 32 * c, br, fb);
+                        for (int c = 0; c < BNC / 32; ++c) {
+                            tma2d<PAIR>(base + 2 * A_TILE + c * (BK * 128), &p.tb_hi[sg], bc + 32 * c, br, fb);
+                            tma2d<PAIR>(base + 2 * A_TILE + B_T + c * (BK * 128), &p.tb_lo[sg], bc + 32 * c, br, fb);
                         }
                     }
                 }
                 __syncwarp();
-                if (++stage == STAGES) {
+                if (++stage == NST) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 && leader) {
         // ---------------- MMA issuer ----------------
         // instruction descriptor: D f32, A/B tf32, A K-major, B K- or MN-major, N=256, M=128
         const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((B_MN && !(p.debug_swap & 2) ? 1u : 0u) << 16) |
-                               ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                               ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CM) >> 4) << 24);
         uint32_t b_lbo = 0, b_sbo = 1024;
         const uint64_t b_layout = B_MN ? 1 : 2;
         if (B_MN) {
@@ -242,7 +329,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+        for (int t = cid; t < p.total; t += ncl, ++it) {
             const TileInfo ti = decode(p, t);
             const int acc = dual ? 0 : (it & 1);
             mb_wait(tempty0 + 8 * acc, ((it >> 1) & 1) ^ 1);
@@ -256,9 +343,9 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 mb_wait(full0 + 8 * stage, phase);
                 fence_after();
                 if (lane == 0) {
-                    const uint32_t base = su32(smem + stage * STAGE);
+                    const uint32_t base = su32(smem + stage * STG);
                     const uint32_t ah = base, al = base + A_TILE;
-                    const uint32_t bh = base + 2 * A_TILE, bl = bh + B_TILE;
+                    const uint32_t bh = base + 2 * A_TILE, bl = bh + B_T;
 #pragma unroll
                     for (int ks = 0; ks < BK / 8; ++ks) {
                         const uint64_t dah = sdesc(ah + ks * 32, 0, 1024);
@@ -267,19 +354,19 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                         const uint64_t dbh = sdesc(bh + boff, b_lbo, b_sbo, b_layout);
                         const uint64_t dbl = sdesc(bl + boff, b_lbo, b_sbo, b_layout);
                         const uint32_t first = (fresh && ks == 0) ? 0u : 1u;
-                        mma_tf32(dtm, dal, dbh, idesc, first);
-                        mma_tf32(dtm, dah, dbl, idesc, 1u);
-                        mma_tf32(dtm, dah, dbh, idesc, 1u);
+                        mma_tf32<PAIR>(dtm, dal, dbh, idesc, first);
+                        mma_tf32<PAIR>(dtm, dah, dbl, idesc, 1u);
+                        mma_tf32<PAIR>(dtm, dah, dbh, idesc, 1u);
                     }
-                    umma_commit(empty0 + 8 * stage);
+                    umma_commit<PAIR>(empty0 + 8 * stage);
                 }
                 __syncwarp();
-                if (++stage == STAGES) {
+                if (++stage == NST) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) umma_commit(tfull0 + 8 * acc);
+            if (lane == 0) umma_commit<PAIR>(tfull0 + 8 * acc);
             __syncwarp();
         }
     } else if (warp >= 4) {
@@ -287,14 +374,15 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         const int q = warp & 3;  // TMEM lane quarter this warp may access
         float* st = epi + q * 32 * EPI_PITCH;
         int it = 0;
-        for (int t = blockIdx.x; t < p.total; t += gridDim.x, ++it) {
+        for (int t = cid; t < p.total; t += ncl, ++it) {
             const TileInfo ti = decode(p, t);
             const int acc = dual ? 0 : (it & 1);
             const bool two = dual && ti.kb_hi - ti.kb_lo > 1;
             mb_wait(tfull0 + 8 * acc, (it >> 1) & 1);
             fence_after();
-            const int row_t = q * 32 + lane;  // this lane's tile row
-            const int64_t grow_l = (int64_t)ti.z * p.z_out + ti.m0 + row_t;
+            const int mrow0 = ti.m0 + (int)rank * BM;  // this CTA's 128 rows of the tile
+            const int row_t = q * 32 + lane;           // this lane's row
+            const int64_t grow_l = (int64_t)ti.z * p.z_out + mrow0 + row_t;
             for (int c = 0; c < BN / 32; ++c) {
                 // C operand of this chunk first: 16 independent 16-byte loads in
                 // flight per lane while the accumulator is read back
@@ -302,7 +390,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 if (p.c_hi && !p.partial) {
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        const int grow = ti.m0 + q * 32 + i * 4 + (lane >> 3);
+                        const int grow = mrow0 + q * 32 + i * 4 + (lane >> 3);
                         const int gcol = ti.n0 + c * 32 + (lane & 7) * 4;
                         if (grow < p.M && gcol < p.N) {
                             const int64_t off = ((int64_t)ti.z * p.z_out + grow) * p.ldc + gcol;
@@ -320,7 +408,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                     for (int j = 0; j < 32; ++j) v[j] += v1[j];
                 }
                 const int ncol0 = ti.n0 + c * 32;
-                if (p.t_hi && ti.m0 + row_t < p.M) {
+                if (p.t_hi && mrow0 + row_t < p.M) {
                     // transposed split copy: element (n, row) at t[n * ldt + row]
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -335,7 +423,12 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 if (c == BN / 32 - 1) {  // accumulator fully read: hand it back to the MMA warp
                     fence_before();
                     __syncwarp();
-                    if (lane == 0) mb_arrive(tempty0 + 8 * acc);
+                    if (lane == 0) {
+                        if constexpr (PAIR)
+                            mb_arrive_cluster(mapa_u32(tempty0 + 8 * acc, 0));
+                        else
+                            mb_arrive(tempty0 + 8 * acc);
+                    }
                 }
 #pragma unroll
                 for (int j = 0; j < 32; j += 4)
@@ -345,7 +438,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 for (int i = 0; i < 8; ++i) {
                     const int r = i * 4 + (lane >> 3);
                     const int cc = (lane & 7) * 4;
-                    const int grow = ti.m0 + q * 32 + r;
+                    const int grow = mrow0 + q * 32 + r;
                     const int gcol = ncol0 + cc;
                     if (grow < p.M && gcol < p.N) {
                         float4 a = *reinterpret_cast<const float4*>(st + r * EPI_PITCH + cc);
@@ -380,10 +473,17 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         }
     }
     fence_before();
-    __syncthreads();
+    if constexpr (PAIR)
+        cluster_sync();
+    else
+        __syncthreads();
     fence_after();
-    if (warp == 2)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    if (warp == 2) {
+        if constexpr (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+    }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -423,6 +523,9 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.M = g.M;
     p.N = g.N;
     p.nseg = g.nseg;
+    // CTA pairs (256-row tiles) once M is large enough to keep 74 pairs busy
+    static const int pair_env = getenv("FASTH_LB_PAIR") ? atoi(getenv("FASTH_LB_PAIR")) : -1;
+    const bool pair = pair_env >= 0 ? (pair_env != 0 && g.M > BM) : g.M >= 1024;
     int tot_kb = 0;
     for (int sg = 0; sg < g.nseg; ++sg) {
         const Segment& S = g.seg[sg];
@@ -436,8 +539,8 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
         bool ok = make_map(&p.ta_hi[sg], S.A.hi, S.A.rows, S.A.cols, S.A.ld, BK, BM) &&
                   make_map(&p.ta_lo[sg], S.A.lo, S.A.rows, S.A.cols, S.A.ld, BK, BM);
         if (!g.b_mn)
-            ok = ok && make_map(&p.tb_hi[sg], S.B.hi, S.B.rows, S.B.cols, S.B.ld, BK, BN) &&
-                 make_map(&p.tb_lo[sg], S.B.lo, S.B.rows, S.B.cols, S.B.ld, BK, BN);
+            ok = ok && make_map(&p.tb_hi[sg], S.B.hi, S.B.rows, S.B.cols, S.B.ld, BK, pair ? BN / 2 : BN) &&
+                 make_map(&p.tb_lo[sg], S.B.lo, S.B.rows, S.B.cols, S.B.ld, BK, pair ? BN / 2 : BN);
         else
             ok = ok && make_map(&p.tb_hi[sg], S.B.hi, S.B.rows, S.B.cols, S.B.ld, 32, BK, true) &&
                  make_map(&p.tb_lo[sg], S.B.lo, S.B.rows, S.B.cols, S.B.ld, 32, BK, true);
@@ -450,7 +553,8 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.ksplit = (tot_kb + p.kb_per_split - 1) / p.kb_per_split;  // no empty splits
     g.ksplit = p.ksplit;
     p.nz = std::max(1, g.nz);
-    p.mt = (g.M + BM - 1) / BM;
+    p.tile_m = pair ? 2 * BM : BM;
+    p.mt = (g.M + p.tile_m - 1) / p.tile_m;
     p.nt = (g.N + BN - 1) / BN;
     p.total = p.nz * p.ksplit * p.mt * p.nt;
     p.z_a_row = g.z_a_row;
@@ -473,18 +577,36 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.ldt = g.ldt;
     p.partial = g.partial;
     p.debug_swap = g.debug_swap;
-    const int grid = std::min(p.total, std::max(num_sms, 1));
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[g.b_mn]) {
-        cudaError_t e = g.b_mn ? cudaFuncSetAttribute(gemm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES)
-                               : cudaFuncSetAttribute(gemm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set[g.b_mn] = true;
+    static bool attr_set[4] = {false, false, false, false};
+    const int which = (g.b_mn ? 1 : 0) + (pair ? 2 : 0);
+    void (*kern)(Params) = nullptr;
+    switch (which) {
+        case 0: kern = gemm_kernel<false, false>; break;
+        case 1: kern = gemm_kernel<true, false>; break;
+        case 2: kern = gemm_kernel<false, true>; break;
+        default: kern = gemm_kernel<true, true>; break;
     }
-    if (g.b_mn)
-        gemm_kernel<true><<<grid, 256, SMEM_BYTES, s>>>(p);
-    else
-        gemm_kernel<false><<<grid, 256, SMEM_BYTES, s>>>(p);
+    if (!attr_set[which]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set[which] = true;
+    }
+    const int units = pair ? std::max(num_sms / 2, 1) : std::max(num_sms, 1);
+    const int grid = std::min(p.total, units) * (pair ? 2 : 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pair ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -81,9 +81,24 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
         __syncthreads();
         for (int rc = cc; rc >= 0; --rc) {
             const int r0 = rc * 32, k0 = (rc + 1) * 32, k1 = c0 + 32;
-            for (int e = tid; e < 32 * (k1 - k0); e += 256) {
-                const int i = e / (k1 - k0), k = k0 + e % (k1 - k0);
-                Mp[i * MP + k] = M[(int64_t)(r0 + i) * B + k];
+            {  // rows i = warp + 8 u, float4 columns k0 + 4 lane + 128 v: all loads in flight
+                const int warp = tid >> 5, lane = tid & 31;
+                float4 buf[4][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int k = k0 + 4 * lane + 128 * v;
+                        if (k < k1)
+                            buf[u][v] = __ldg(reinterpret_cast<const float4*>(M + (int64_t)(r0 + warp + 8 * u) * B + k));
+                    }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        const int k = k0 + 4 * lane + 128 * v;
+                        if (k < k1) *reinterpret_cast<float4*>(Mp + (warp + 8 * u) * MP + k) = buf[u][v];
+                    }
             }
             __syncthreads();
             {
@@ -132,7 +147,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
             tl[(int64_t)r * B + c0 + c] = v - h;
         }
         for (int e = tid; e < B * 32; e += 256) {
-            const int c = e / B, r = e % B;  // coalesced along r
+            const int c = e / B, r = e % B;  // coalesced along r (smem column read, 32-way conflicts are cheap here)
             const float v = Tc[r * 32 + c];
             const float h = rn_hi(v);
             tth[(int64_t)(c0 + c) * B + r] = h;
@@ -150,11 +165,14 @@ __global__ void q_reduce_kernel(const float* __restrict__ part, int ks, int B, f
     __shared__ float qt[32][33], qtt[32][33];
     const int64_t per = (int64_t)B * B;
     const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32, tx = threadIdx.x;
-    for (int r = threadIdx.y; r < 32; r += 8) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int r = threadIdx.y + 8 * u;
         float s1 = 0.f, s2 = 0.f;
+#pragma unroll 8
         for (int k = 0; k < ks; ++k) {
-            s1 += part[k * per + (int64_t)(a0 + r) * B + b0 + tx];  // Q[a0+r][b0+tx]
-            s2 += part[k * per + (int64_t)(b0 + r) * B + a0 + tx];  // Q[b0+r][a0+tx]
+            s1 += __ldg(part + k * per + (int64_t)(a0 + r) * B + b0 + tx);  // Q[a0+r][b0+tx]
+            s2 += __ldg(part + k * per + (int64_t)(b0 + r) * B + a0 + tx);  // Q[b0+r][a0+tx]
         }
         qt[r][tx] = s1;
         qtt[r][tx] = s2;
@@ -175,7 +193,8 @@ __global__ void dv_reduce_kernel(const float* __restrict__ part, int ks, int B, 
     const int64_t per = (int64_t)B * d;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
         float s = 0.f;
-        for (int k = 0; k < ks; ++k) s += part[k * per + e];
+#pragma unroll 4
+        for (int k = 0; k < ks; ++k) s += __ldg(part + k * per + e);
         dV[(e / d) * lddv + e % d] = s;
     }
 }

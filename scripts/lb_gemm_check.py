@@ -98,6 +98,13 @@ def main():
         dict(M=512, N=512, K=2048, b_mn=False, ksplit=8),
         dict(M=512, N=1024, K=2048, b_mn=True, ksplit=4),
         dict(M=1000, N=1000, K=1000, b_mn=False),
+        # M >= 1024: CTA-pair (cta_group::2) tiles
+        dict(M=1024, N=512, K=256, b_mn=False),
+        dict(M=1024, N=512, K=256, b_mn=True),
+        dict(M=2048, N=768, K=96, b_mn=False, alpha=-2.0, beta=1.0, with_c=True),
+        dict(M=1100, N=300, K=200, b_mn=False, trans=True),
+        dict(M=1024, N=1024, K=2048, b_mn=True, ksplit=4),
+        dict(M=8192, N=512, K=2048, b_mn=False),
     ]
     for c in cases:
         try:
