@@ -59,20 +59,24 @@ __global__ void diag_inv_kernel(const float* __restrict__ Mm, int B, float* __re
 
 // T_z = M_z^{-1} by blocked back-substitution over 32-row chunks:
 //   T[rc][cc] = Dinv_rc (E - sum_{k > rc} M[rc][k] T[k][cc]).
-// One CTA per pair of 32-column chunks (cc, B/32-1-cc) for balanced work;
-// the M row panel of each step is staged in shared memory (coalesced).  Writes
-// T and T^T, both split.  grid (B/64, nz), 256 threads.
+// One CTA per pair of 32-column chunks (cc, B/32-1-cc) for balanced work.
+// The update product is register blocked: 64 threads x (4 rows x 4 columns)
+// cover the 32 x 32 block, 4 thread groups split k; the M row panel is staged
+// transposed ([k][row]) so both operands are 16-byte shared loads.  Writes T
+// and T^T, both split.  grid (B/64, nz), 256 threads.
 __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ Mm, const float* __restrict__ Dinv,
                                                       int B, float* __restrict__ Th, float* __restrict__ Tl,
                                                       float* __restrict__ TTh, float* __restrict__ TTl) {
     extern __shared__ float sm[];
-    float* Tc = sm;                // [B][32] solution chunk
-    float* R = Tc + B * 32;        // [32][33] right-hand side
-    float* Mp = R + 32 * 33;       // [32][B] staged row panel (pitch B + 4)
-    const int MP = B + 4;
+    float* Tc = sm;                 // [B][32] solution chunk
+    float* MpT = Tc + B * 32;       // [B][36] staged row panel, transposed
+    float* red = MpT + B * 36;      // [4][32][33] k-split partial sums
+    float* R = red + 4 * 32 * 33;   // [32][33] right-hand side
+    float* Dd = R + 32 * 33;        // [32][33] diagonal-block inverse
     const int z = blockIdx.y, nchunk = B / 32;
     const float* M = Mm + (int64_t)z * B * B;
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int kq = tid >> 6, t64 = tid & 63, rg = t64 >> 3, cg = t64 & 7;
     for (int pass = 0; pass < 2; ++pass) {
         const int cc = pass == 0 ? blockIdx.x : nchunk - 1 - blockIdx.x;
         const int c0 = cc * 32;
@@ -81,8 +85,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
         __syncthreads();
         for (int rc = cc; rc >= 0; --rc) {
             const int r0 = rc * 32, k0 = (rc + 1) * 32, k1 = c0 + 32;
-            {  // rows i = warp + 8 u, float4 columns k0 + 4 lane + 128 v: all loads in flight
-                const int warp = tid >> 5, lane = tid & 31;
+            {  // stage M[r0 + i][k0..k1) transposed, and Dinv_rc
                 float4 buf[4][4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -92,44 +95,60 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
                         if (k < k1)
                             buf[u][v] = __ldg(reinterpret_cast<const float4*>(M + (int64_t)(r0 + warp + 8 * u) * B + k));
                     }
+                const float* D = Dinv + ((int64_t)z * nchunk + rc) * 1024;
+                float dv[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u = 0; u < 4; ++u) dv[u] = __ldg(D + (warp + 8 * u) * 32 + lane);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = warp + 8 * u;
 #pragma unroll
                     for (int v = 0; v < 4; ++v) {
                         const int k = k0 + 4 * lane + 128 * v;
-                        if (k < k1) *reinterpret_cast<float4*>(Mp + (warp + 8 * u) * MP + k) = buf[u][v];
+                        if (k < k1) {
+                            MpT[(k + 0) * 36 + i] = buf[u][v].x;
+                            MpT[(k + 1) * 36 + i] = buf[u][v].y;
+                            MpT[(k + 2) * 36 + i] = buf[u][v].z;
+                            MpT[(k + 3) * 36 + i] = buf[u][v].w;
+                        }
                     }
-            }
-            __syncthreads();
-            {
-                const int r = tid >> 3, c4 = (tid & 7) * 4;
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-                for (int k = k0; k < k1; ++k) {
-                    const float mv = Mp[r * MP + k];
-                    const float4 t = *reinterpret_cast<const float4*>(Tc + k * 32 + c4);
-                    a0 = fmaf(mv, t.x, a0);
-                    a1 = fmaf(mv, t.y, a1);
-                    a2 = fmaf(mv, t.z, a2);
-                    a3 = fmaf(mv, t.w, a3);
+                    Dd[i * 33 + lane] = dv[u];
                 }
-                const int gr = r0 + r;
-                R[r * 33 + c4 + 0] = (gr == c0 + c4 + 0 ? 1.f : 0.f) - a0;
-                R[r * 33 + c4 + 1] = (gr == c0 + c4 + 1 ? 1.f : 0.f) - a1;
-                R[r * 33 + c4 + 2] = (gr == c0 + c4 + 2 ? 1.f : 0.f) - a2;
-                R[r * 33 + c4 + 3] = (gr == c0 + c4 + 3 ? 1.f : 0.f) - a3;
             }
             __syncthreads();
-            {
+            {  // partial products over k = k0 + kq, k0 + kq + 4, ...
+                float acc[4][4] = {};
+                for (int k = k0 + kq; k < k1; k += 4) {
+                    const float4 m4 = *reinterpret_cast<const float4*>(MpT + k * 36 + 4 * rg);
+                    const float4 t4 = *reinterpret_cast<const float4*>(Tc + k * 32 + 4 * cg);
+                    const float mv[4] = {m4.x, m4.y, m4.z, m4.w}, tv[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(mv[a], tv[b], acc[a][b]);
+                }
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) red[(kq * 32 + 4 * rg + a) * 33 + 4 * cg + b] = acc[a][b];
+            }
+            __syncthreads();
+            for (int e = tid; e < 1024; e += 256) {
+                const int r = e >> 5, c = e & 31;
+                const float sum = red[(0 * 32 + r) * 33 + c] + red[(1 * 32 + r) * 33 + c] +
+                                  red[(2 * 32 + r) * 33 + c] + red[(3 * 32 + r) * 33 + c];
+                R[r * 33 + c] = (r0 + r == c0 + c ? 1.f : 0.f) - sum;
+            }
+            __syncthreads();
+            {  // T[rc] = Dinv_rc R  (Dinv upper triangular)
                 const int r = tid >> 3, c4 = (tid & 7) * 4;
-                const float* D = Dinv + ((int64_t)z * nchunk + rc) * 1024 + r * 32;
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll 8
-                for (int k = r; k < 32; ++k) {  // Dinv upper triangular
-                    const float dv = __ldg(D + k);
-                    a0 = fmaf(dv, R[k * 33 + c4 + 0], a0);
-                    a1 = fmaf(dv, R[k * 33 + c4 + 1], a1);
-                    a2 = fmaf(dv, R[k * 33 + c4 + 2], a2);
-                    a3 = fmaf(dv, R[k * 33 + c4 + 3], a3);
+                for (int k = r; k < 32; ++k) {
+                    const float d = Dd[r * 33 + k];
+                    a0 = fmaf(d, R[k * 33 + c4 + 0], a0);
+                    a1 = fmaf(d, R[k * 33 + c4 + 1], a1);
+                    a2 = fmaf(d, R[k * 33 + c4 + 2], a2);
+                    a3 = fmaf(d, R[k * 33 + c4 + 3], a3);
                 }
                 *reinterpret_cast<float4*>(Tc + (r0 + r) * 32 + c4) = make_float4(a0, a1, a2, a3);
             }
@@ -147,7 +166,7 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
             tl[(int64_t)r * B + c0 + c] = v - h;
         }
         for (int e = tid; e < B * 32; e += 256) {
-            const int c = e / B, r = e % B;  // coalesced along r (smem column read, 32-way conflicts are cheap here)
+            const int c = e / B, r = e % B;  // coalesced along r
             const float v = Tc[r * 32 + c];
             const float h = rn_hi(v);
             tth[(int64_t)(c0 + c) * B + r] = h;
@@ -156,26 +175,29 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
     }
 }
 
-// S = 2 K'^T (the dV product's alpha = -2 makes it -4 K'^T), K' = striu(Q - Q^T),
-// Q = sum of ks partials (B x B); split.
-// 32 x 32 tiles: the (a, b) and (b, a) tiles are summed into shared memory
-// with coalesced reads.  grid (B/32, B/32), 32 x 8 threads.
-__global__ void q_reduce_kernel(const float* __restrict__ part, int ks, int B, float* __restrict__ Sh,
-                                float* __restrict__ Sl) {
-    __shared__ float qt[32][33], qtt[32][33];
-    const int64_t per = (int64_t)B * B;
-    const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32, tx = threadIdx.x;
+// Q = sum of the ks split-K partials (B x B), one element per thread, all
+// partial loads independent.
+__global__ void q_sum_kernel(const float* __restrict__ part, int ks, int64_t per, float* __restrict__ Q) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= per) return;
+    float v[16];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int r = threadIdx.y + 8 * u;
-        float s1 = 0.f, s2 = 0.f;
-#pragma unroll 8
-        for (int k = 0; k < ks; ++k) {
-            s1 += __ldg(part + k * per + (int64_t)(a0 + r) * B + b0 + tx);  // Q[a0+r][b0+tx]
-            s2 += __ldg(part + k * per + (int64_t)(b0 + r) * B + a0 + tx);  // Q[b0+r][a0+tx]
-        }
-        qt[r][tx] = s1;
-        qtt[r][tx] = s2;
+    for (int k = 0; k < 16; ++k) v[k] = k < ks ? __ldg(part + k * per + e) : 0.f;
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s += v[k];
+    for (int k = 16; k < ks; ++k) s += part[k * per + e];
+    Q[e] = s;
+}
+
+// S = 2 K'^T (the dV product's alpha = -2 makes it -4 K'^T), K' = striu(Q - Q^T);
+// split.  32 x 32 tiles through shared memory.  grid (B/32, B/32), 32 x 8 threads.
+__global__ void s_from_q_kernel(const float* __restrict__ Q, int B, float* __restrict__ Sh, float* __restrict__ Sl) {
+    __shared__ float qt[32][33], qtt[32][33];
+    const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32, tx = threadIdx.x;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        qt[r][tx] = Q[(int64_t)(a0 + r) * B + b0 + tx];   // Q[a0+r][b0+tx]
+        qtt[r][tx] = Q[(int64_t)(b0 + r) * B + a0 + tx];  // Q[b0+r][a0+tx]
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += 8) {
@@ -229,7 +251,7 @@ size_t workspace_floats(int d, int n, int m, bool want_dv) {
     f += 2 * (size_t)B * m;         // Zb natural split
     f += 4 * md;                    // two gradient buffers split
     if (want_dv) {
-        f += 16 * bb + 2 * bb;      // Q partials, S split
+        f += 16 * bb + 3 * bb;      // Q partials, Q, S split
         f += 8 * (size_t)B * d;     // dV partials
     }
     return f + 256 * 32;            // alignment slack
@@ -274,9 +296,10 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
     float *Zbh = c.take((size_t)B * m), *Zbl = c.take((size_t)B * m);
     float *Gh[2] = {c.take(md), c.take(md)}, *Gl[2] = {c.take(md), c.take(md)};
     const int ksQ = 16, ksV = 4;  // 128 CTAs each: one tile per CTA, dual accumulators
-    float *Qp = nullptr, *Sh = nullptr, *Sl = nullptr, *dVp = nullptr;
+    float *Qp = nullptr, *Qs = nullptr, *Sh = nullptr, *Sl = nullptr, *dVp = nullptr;
     if (want_dv) {
         Qp = c.take(ksQ * bb);
+        Qs = c.take(bb);
         Sh = c.take(bb);
         Sl = c.take(bb);
         dVp = c.take((size_t)(ksV + 1) * B * d);
@@ -312,7 +335,7 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
     {
         ++nl;
         diag_inv_kernel<<<dim3(B / 32, nb), 32, 0, s>>>(Mm, B, Dinv);
-        const int smem = (B * 32 + 32 * 33 + 32 * (B + 4)) * 4;
+        const int smem = (B * 32 + B * 36 + 4 * 32 * 33 + 2 * 32 * 33) * 4;
         static int attr = 0;
         if (attr < smem) {
             LBTRY(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -422,7 +445,9 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
                 q_ks = g.ksplit;
             }
             ++nl;
-    q_reduce_kernel<<<dim3(B / 32, B / 32), dim3(32, 8), 0, s>>>(Qp, q_ks, B, Sh, Sl);
+    q_sum_kernel<<<(int)((bb + 255) / 256), 256, 0, s>>>(Qp, q_ks, (int64_t)bb, Qs);
+            ++nl;
+            s_from_q_kernel<<<dim3(B / 32, B / 32), dim3(32, 8), 0, s>>>(Qs, B, Sh, Sl);
             {
                 Gemm g;  // dV_j partials = -2 (Zb A_j + Zf_j G) + S V_j   (S = -4 K'^T pre-scaled by -1/2)
                 g.M = B;
