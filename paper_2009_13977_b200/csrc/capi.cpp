@@ -229,6 +229,7 @@ struct fasth_tape_s {
     float* zb = nullptr;
     const float* scale = nullptr;  // Sigma-scaled input rows (SVD U leg)
     int n_valid = 0;
+    float* lb_ws = nullptr;  // large-batch path (lb.h): workspace holding the forward stages
 };
 
 struct fasth_svd_tape_s {
@@ -261,6 +262,7 @@ void free_tape(fasth_tape t) {
     c->release(t->zf);
     c->release(t->tapeG);
     c->release(t->zb);
+    c->release(t->lb_ws);
     delete t;
 }
 
@@ -872,6 +874,104 @@ fasth_status fasth_ctx_trim(fasth_ctx c) {
     return FASTH_OK;
 }
 
+// Large-batch path (lb.h): the chain re-blocked into 512-wide WY blocks, every
+// step a tcgen05 GEMM.  Chosen when the batch is wide enough for the GEMMs to
+// fill the GPU (m >= 1024 and d >= 512 here; FASTH_LB=0/1 forces the choice)
+// and the shapes meet its alignment (n a multiple of 128, d and m of 4).
+bool use_large_batch(int d, int n, int m) {
+    if (!fasthb::lb::supported(d, n, m)) return false;
+    if (const char* e = getenv("FASTH_LB")) return atoi(e) != 0;
+    return m >= 1024 && d >= 512;
+}
+
+bool vec_ok(const float* p, int64_t ld) { return !p || ((ld % 4) == 0 && !(reinterpret_cast<uintptr_t>(p) & 15)); }
+
+// Output `out` (d x m, column-major, ld) through a packed temporary when the
+// epilogue's 16-byte stores cannot write it in place.
+struct OutBuf {
+    fasth_ctx c;
+    float* user;
+    int64_t ld;
+    float* tmp = nullptr;
+    float* ptr() const { return tmp ? tmp : user; }
+    int64_t pitch(int d) const { return tmp ? d : ld; }
+    fasth_status open(int d, int m) {
+        if (user && !vec_ok(user, ld)) TRY(c->alloc_n((size_t)d * m, &tmp));
+        return FASTH_OK;
+    }
+    fasth_status close(int d, int m) {
+        if (tmp) {
+            CU(cudaMemcpy2DAsync(user, ld * 4, tmp, (size_t)d * 4, (size_t)d * 4, m, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+            c->release(tmp);
+            tmp = nullptr;
+        }
+        return FASTH_OK;
+    }
+};
+
+fasth_status lb_status(fasth_ctx c, cudaError_t e, const char* what) {
+    return e == cudaSuccess ? FASTH_OK : fail(FASTH_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx,
+                             const float* G, int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx,
+                             float* dV, int64_t lddv) {
+    float* ws = nullptr;
+    TRY(c->alloc_n(fasthb::lb::workspace_floats(d, n, m, dV != nullptr), &ws));
+    OutBuf y{c, Y, ldy}, dx{c, dX, lddx};
+    fasth_status s = y.open(d, m);
+    if (s == FASTH_OK) s = dx.open(d, m);
+    int nl = 1;
+    if (s == FASTH_OK)
+        s = c->timed(
+            [&] {
+                return fasthb::lb::forward_backward(V, ldv, d, n, X, ldx, G, ldg, m, y.ptr(), y.pitch(d), dx.ptr(),
+                                                    dx.pitch(d), dV, lddv, ws, c->err_d, c->stream, c->num_sms, &nl);
+            },
+            "large_batch(fwd+bwd)");
+    c->launches += nl - 1;
+    if (s == FASTH_OK) s = y.close(d, m);
+    if (s == FASTH_OK) s = dx.close(d, m);
+    c->release(ws);  // pool reuse is stream ordered
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
+// fasth_forward on the large-batch path: the tape owns the workspace (forward
+// stages, Zf, WY blocks) that fasth_backward consumes.
+fasth_status lb_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m,
+                        int block_width, float* Y, int64_t ldy, fasth_tape* tape) {
+    fasth_tape t = new fasth_tape_s;
+    t->ctx = c;
+    t->m = m;
+    t->b_user = block_width;
+    t->plan.d = d;
+    t->plan.n = n;
+    const int bw = std::min(std::max(block_width, 1), n);
+    t->plan.b = bw;
+    t->plan.q = (n + bw - 1) / bw;
+    fasth_status s = c->alloc_n(fasthb::lb::workspace_floats(d, n, m, true), &t->lb_ws);
+    OutBuf y{c, Y, ldy};
+    if (s == FASTH_OK) s = y.open(d, m);
+    int nl = 1;
+    if (s == FASTH_OK)
+        s = c->timed(
+            [&] {
+                return fasthb::lb::forward(V, ldv, d, n, X, ldx, m, y.ptr(), y.pitch(d), t->lb_ws, c->err_d,
+                                           c->stream, c->num_sms, &nl);
+            },
+            "large_batch(fwd)");
+    c->launches += nl - 1;
+    if (s == FASTH_OK) s = y.close(d, m);
+    if (s == FASTH_OK) s = c->finish();
+    if (s == FASTH_OK && tape)
+        *tape = t;
+    else
+        free_tape(t);
+    return s;
+}
+
 fasth_status fasth_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X,
                            int64_t ldx, int m, int block_width, float* Y, int64_t ldy,
                            fasth_tape* tape) {
@@ -895,6 +995,7 @@ fasth_status fasth_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int 
         else free_tape(t);
         return s;
     }
+    if (use_large_batch(d, n, m)) return lb_forward(c, V, ldv, d, n, X, ldx, m, block_width, Y, ldy, tape);
     fasth_tape t = nullptr;
     TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t));
     fasth_status s = run_forward(c, t, X, ldx, Y, ldy, tape != nullptr);
@@ -921,6 +1022,20 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
         if (dV) CU(cudaMemset2DAsync(dV, lddv * sizeof(float), 0, d * sizeof(float), n, c->stream));
         return c->finish();
     }
+    if (t->lb_ws) {
+        OutBuf dx{c, dX, lddx};
+        TRY(dx.open(d, m));
+        int nl = 1;
+        TRY(c->timed(
+            [&] {
+                return fasthb::lb::backward(d, n, m, G, ldg, dx.ptr(), dx.pitch(d), dV, lddv, t->lb_ws, c->stream,
+                                            c->num_sms, &nl);
+            },
+            "large_batch(bwd)"));
+        c->launches += nl - 1;
+        TRY(dx.close(d, m));
+        return c->finish();
+    }
     TRY(run_backward(c, t, G, ldg, d, nullptr, dX, lddx, dV, lddv));
     return c->finish();
 }
@@ -938,37 +1053,6 @@ fasth_status fasth_tape_info(fasth_tape t, int* d, int* n, int* m, int* block_wi
     if (block_width) *block_width = t->plan.n ? std::min(std::max(t->b_user, 1), t->plan.n) : t->b_user;
     if (q) *q = t->plan.q;
     return FASTH_OK;
-}
-
-// Large-batch path (lb.h): the chain re-blocked into 512-wide WY blocks, every
-// step a tcgen05 GEMM.  Chosen when the batch is wide enough for the GEMMs to
-// fill the GPU (m >= 1024 here; FASTH_LB=0/1 forces the choice) and the shapes
-// meet its alignment (n a multiple of 128, d and m multiples of 4).
-bool use_large_batch(int d, int n, int m, const float* Y, int64_t ldy, const float* dX, int64_t lddx) {
-    if (!fasthb::lb::supported(d, n, m)) return false;
-    if (!dX || (ldy % 4) || (lddx % 4) || (reinterpret_cast<uintptr_t>(Y) & 15) ||
-        (reinterpret_cast<uintptr_t>(dX) & 15))
-        return false;
-    if (const char* e = getenv("FASTH_LB")) return atoi(e) != 0;
-    return m >= 1024 && d >= 512;
-}
-
-fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx,
-                             const float* G, int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx,
-                             float* dV, int64_t lddv) {
-    float* ws = nullptr;
-    TRY(c->alloc_n(fasthb::lb::workspace_floats(d, n, m, dV != nullptr), &ws));
-    int nl = 1;
-    fasth_status s = c->timed(
-        [&] {
-            return fasthb::lb::forward_backward(V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy, dX, lddx, dV, lddv, ws,
-                                                c->err_d, c->stream, c->num_sms, &nl);
-        },
-        "large_batch(fwd+bwd)");
-    c->launches += nl - 1;
-    c->release(ws);  // pool reuse is stream ordered
-    if (s == FASTH_OK) s = c->finish();
-    return s;
 }
 
 fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, int d, int n,
@@ -991,8 +1075,8 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
         free_tape(t);
         return s;
     }
-    if (use_large_batch(d, n, m, Y, ldy, dX, lddx)) return run_large_batch(c, V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy,
-                                                                         dX, lddx, dV, lddv);
+    if (use_large_batch(d, n, m))
+        return run_large_batch(c, V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy, dX, lddx, dV, lddv);
     fasth_tape t = nullptr;
     TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr));
     fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);

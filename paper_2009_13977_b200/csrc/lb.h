@@ -82,6 +82,12 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms);
 int pick_block(int n);
 bool supported(int d, int n, int m);
 size_t workspace_floats(int d, int n, int m, bool want_dv);
+// The two halves (fasth_forward / fasth_backward): `ws` carries the forward
+// stages from one to the other.
+cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
+                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch);
+cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
+                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch);
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch);

@@ -250,10 +250,9 @@ size_t workspace_floats(int d, int n, int m, bool want_dv) {
     f += 2 * (size_t)n * m;         // Zf (natural, all blocks) split
     f += 2 * (size_t)B * m;         // Zb natural split
     f += 4 * md;                    // two gradient buffers split
-    if (want_dv) {
-        f += 16 * bb + 3 * bb;      // Q partials, Q, S split
-        f += 8 * (size_t)B * d;     // dV partials
-    }
+    (void)want_dv;                  // the forward carves the backward's buffers too
+    f += 16 * bb + 3 * bb;          // Q partials, Q, S split
+    f += 8 * (size_t)B * d;         // dV partials
     return f + 256 * 32;            // alignment slack
 }
 
@@ -266,49 +265,81 @@ struct Carver {
     }
 };
 
-cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
-                             int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
-                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch) {
-    int nl = 0;
-    const int B = pick_block(n), nb = n / B;
-    const bool want_dv = dV != nullptr;
-    if (!B || !supported(d, n, m)) return cudaErrorInvalidValue;
-    if ((ldy % 4) || (lddx % 4) || (reinterpret_cast<uintptr_t>(Y) & 15) || (reinterpret_cast<uintptr_t>(dX) & 15))
-        return cudaErrorInvalidValue;
-    const size_t nd = (size_t)n * d, md = (size_t)m * d, bb = (size_t)B * B;
+namespace {
+constexpr int kMaxStages = 65;
+
+struct Bufs {
+    int B = 0, nb = 0;
+    size_t nd = 0, md = 0, bb = 0;
+    float *Vh, *Vl, *VTh, *VTl, *Gp, *Mm, *Dinv, *Th, *Tl, *TTh, *TTl, *WfH, *WfL, *WbH, *WbL;
+    float *Sth[kMaxStages], *Stl[kMaxStages];
+    float *ZfTh, *ZfTl, *ZbTh, *ZbTl, *Zfh, *Zfl, *Zbh, *Zbl, *Gh[2], *Gl[2];
+    float *Qp, *Qs, *Sh, *Sl, *dVp;
+};
+constexpr int ksG = 4, ksQ = 16, ksV = 4;  // split-K counts (128 CTAs each: one tile per CTA)
+
+// The workspace is carved identically by the forward and the backward half.
+bool carve(float* ws, int d, int n, int m, Bufs& b) {
+    b.B = pick_block(n);
+    if (!b.B) return false;
+    b.nb = n / b.B;
+    if (b.nb + 1 > kMaxStages) return false;
+    const int B = b.B, nb = b.nb;
+    const size_t nd = b.nd = (size_t)n * d, md = b.md = (size_t)m * d, bb = b.bb = (size_t)B * B;
     Carver c{ws};
-    float *Vh = c.take(nd), *Vl = c.take(nd), *VTh = c.take(nd), *VTl = c.take(nd);
-    const int ksG = 4;
-    float* Gp = c.take((size_t)nb * ksG * bb);
-    float* Mm = c.take((size_t)nb * bb);
-    float* Dinv = c.take((size_t)nb * 32 * B);
-    float *Th = c.take(nb * bb), *Tl = c.take(nb * bb), *TTh = c.take(nb * bb), *TTl = c.take(nb * bb);
-    float *WfH = c.take(nd), *WfL = c.take(nd), *WbH = c.take(nd), *WbL = c.take(nd);
-    float *Sth[64], *Stl[64];
-    if (nb + 1 > 64) return cudaErrorInvalidValue;
+    b.Vh = c.take(nd), b.Vl = c.take(nd), b.VTh = c.take(nd), b.VTl = c.take(nd);
+    b.Gp = c.take((size_t)nb * ksG * bb);
+    b.Mm = c.take((size_t)nb * bb);
+    b.Dinv = c.take((size_t)nb * 32 * B);
+    b.Th = c.take(nb * bb), b.Tl = c.take(nb * bb), b.TTh = c.take(nb * bb), b.TTl = c.take(nb * bb);
+    b.WfH = c.take(nd), b.WfL = c.take(nd), b.WbH = c.take(nd), b.WbL = c.take(nd);
     for (int j = 0; j <= nb; ++j) {
-        Sth[j] = c.take(md);
-        Stl[j] = c.take(md);
+        b.Sth[j] = c.take(md);
+        b.Stl[j] = c.take(md);
     }
-    float *ZfTh = c.take((size_t)m * B), *ZfTl = c.take((size_t)m * B);
-    float *ZbTh = c.take((size_t)m * B), *ZbTl = c.take((size_t)m * B);
-    float *Zfh = c.take((size_t)n * m), *Zfl = c.take((size_t)n * m);
-    float *Zbh = c.take((size_t)B * m), *Zbl = c.take((size_t)B * m);
-    float *Gh[2] = {c.take(md), c.take(md)}, *Gl[2] = {c.take(md), c.take(md)};
-    const int ksQ = 16, ksV = 4;  // 128 CTAs each: one tile per CTA, dual accumulators
-    float *Qp = nullptr, *Qs = nullptr, *Sh = nullptr, *Sl = nullptr, *dVp = nullptr;
-    if (want_dv) {
-        Qp = c.take(ksQ * bb);
-        Qs = c.take(bb);
-        Sh = c.take(bb);
-        Sl = c.take(bb);
-        dVp = c.take((size_t)(ksV + 1) * B * d);
-    }
-    cudaError_t e;
-#define LBTRY(x)                            \
-    do {                                    \
+    b.ZfTh = c.take((size_t)m * B), b.ZfTl = c.take((size_t)m * B);
+    b.ZbTh = c.take((size_t)m * B), b.ZbTl = c.take((size_t)m * B);
+    b.Zfh = c.take((size_t)n * m), b.Zfl = c.take((size_t)n * m);
+    b.Zbh = c.take((size_t)B * m), b.Zbl = c.take((size_t)B * m);
+    b.Gh[0] = c.take(md), b.Gh[1] = c.take(md), b.Gl[0] = c.take(md), b.Gl[1] = c.take(md);
+    b.Qp = c.take(ksQ * bb);
+    b.Qs = c.take(bb);
+    b.Sh = c.take(bb);
+    b.Sl = c.take(bb);
+    b.dVp = c.take((size_t)(ksV + 1) * B * d);
+    return true;
+}
+
+#define LBTRY(x)                                \
+    do {                                        \
         if ((e = (x)) != cudaSuccess) return e; \
     } while (0)
+#define LB_ALIASES                                                                                           \
+    const int B = b.B, nb = b.nb;                                                                            \
+    const size_t bb = b.bb;                                                                                  \
+    (void)bb;                                                                                                \
+    float *Vh = b.Vh, *Vl = b.Vl, *VTh = b.VTh, *VTl = b.VTl, *Gp = b.Gp, *Mm = b.Mm, *Dinv = b.Dinv;       \
+    float *Th = b.Th, *Tl = b.Tl, *TTh = b.TTh, *TTl = b.TTl, *WfH = b.WfH, *WfL = b.WfL, *WbH = b.WbH;      \
+    float *WbL = b.WbL, **Sth = b.Sth, **Stl = b.Stl, *ZfTh = b.ZfTh, *ZfTl = b.ZfTl, *ZbTh = b.ZbTh;       \
+    float *ZbTl = b.ZbTl, *Zfh = b.Zfh, *Zfl = b.Zfl, *Zbh = b.Zbh, *Zbl = b.Zbl, **Gh = b.Gh, **Gl = b.Gl; \
+    float *Qp = b.Qp, *Qs = b.Qs, *Sh = b.Sh, *Sl = b.Sl, *dVp = b.dVp;                                    \
+    (void)Vh, (void)Vl, (void)VTh, (void)VTl, (void)Gp, (void)Mm, (void)Dinv, (void)Th, (void)Tl, (void)TTh; \
+    (void)TTl, (void)WfH, (void)WfL, (void)WbH, (void)WbL, (void)Sth, (void)Stl, (void)ZfTh, (void)ZfTl;     \
+    (void)ZbTh, (void)ZbTl, (void)Zfh, (void)Zfl, (void)Zbh, (void)Zbl, (void)Gh, (void)Gl, (void)Qp;       \
+    (void)Qs, (void)Sh, (void)Sl, (void)dVp
+
+}  // namespace
+
+// Build (V -> T~, WfR, WbR) and the forward chain; the workspace keeps every
+// forward stage for the backward half.
+cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
+                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch) {
+    int nl = 0;
+    Bufs b;
+    if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
+    if (Y && ((ldy % 4) || (reinterpret_cast<uintptr_t>(Y) & 15))) return cudaErrorInvalidValue;
+    LB_ALIASES;
+    cudaError_t e;
     // ---- build: split V and V^T, Gram per block, T~, WfR = T~ V_j, WbR = T~^T V_j
     ++nl;
     LBTRY(split(V, ldv, n, d, Vh, Vl, d, s));
@@ -407,6 +438,20 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
         ++nl;
         }
     }
+    if (nlaunch) *nlaunch = nl;
+    return cudaGetLastError();
+}
+
+// Backward chain and dV from the forward's workspace (same d, n, m).
+cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
+                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch) {
+    int nl = 0;
+    Bufs b;
+    if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
+    if (dX && ((lddx % 4) || (reinterpret_cast<uintptr_t>(dX) & 15))) return cudaErrorInvalidValue;
+    const bool want_dv = dV != nullptr;
+    LB_ALIASES;
+    cudaError_t e;
     // ---- backward
     ++nl;
     LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s));
@@ -501,10 +546,21 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
         }
         cur ^= 1;
     }
-#undef LBTRY
     if (nlaunch) *nlaunch = nl;
     return cudaGetLastError();
 }
+
+cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
+                             int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
+                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch) {
+    int n1 = 0, n2 = 0;
+    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1);
+    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2);
+    if (nlaunch) *nlaunch = n1 + n2;
+    return e;
+}
+#undef LBTRY
+#undef LB_ALIASES
 
 }  // namespace lb
 }  // namespace fasthb

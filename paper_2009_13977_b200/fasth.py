@@ -184,6 +184,15 @@ def _new_out(d: int, m: int, like: torch.Tensor) -> torch.Tensor:
     return torch.empty((m, d), dtype=torch.float32, device=like.device).t()
 
 
+def _out_ld(T, d: int, m: int, what: str) -> int:
+    """Leading dimension of a caller-provided (d, m) output with column-major storage."""
+    if T is None:
+        return max(d, 1)
+    if tuple(T.shape) != (d, m) or (m > 1 and d > 1 and T.stride(0) != 1):
+        raise DimensionError(f"out {what}: expected a column-major ({d}, {m}) tensor")
+    return max(T.stride(1) if m > 1 else d, d, 1)
+
+
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else None
 
@@ -276,9 +285,11 @@ def fasth_forward_backward(V: torch.Tensor, X: torch.Tensor, G: torch.Tensor, bl
         dV = torch.empty((n, d), dtype=torch.float32, device=X.device) if want_vectors else None
     else:
         Y, dX, dV = out
+    ldy, lddx = _out_ld(Y, d, m, "Y"), _out_ld(dX, d, m, "dX")
+    lddv = max(dV.stride(0), d, 1) if dV is not None and dV.dim() == 2 and dV.stride(1) == 1 else max(d, 1)
     _check(c.lib.fasth_forward_backward(c.h, _ptr(V), ldv, d, n, _ptr(X), ldx, _ptr(G), ldg, m,
-                                        int(block_width), _ptr(Y), max(d, 1), _ptr(dX), max(d, 1),
-                                        _ptr(dV), max(d, 1)))
+                                        int(block_width), _ptr(Y), ldy, _ptr(dX), lddx,
+                                        _ptr(dV), lddv))
     return Y, BackwardResult(dX, dV)
 
 

@@ -138,15 +138,21 @@ def test_panel_large_batch_default_path(fb, oracle):
     d, b, m = 512, 32, 1024
     rng = np.random.default_rng(77)
     V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
-    Y, dX, dV = (host(t) for t in run_chain(fb, V, X, G, b, fused=True))
+    os.environ["FASTH_LB"] = "0"  # the tcgen05 large-batch path would take this shape (test_gpu_lb.py)
+    try:
+        Y, dX, dV = (host(t) for t in run_chain(fb, V, X, G, b, fused=True))
+    finally:
+        del os.environ["FASTH_LB"]
     cols = [0, 1, 15, 16, 511, 1023]
     wY, wdX, _ = port.fasth_fwd_bwd(V, X[:, cols], G[:, cols], b)
     assert rel(Y[:, cols], wY) <= TOL and rel(dX[:, cols], wdX) <= TOL
     os.environ["FASTH_PANEL"] = "0"
+    os.environ["FASTH_LB"] = "0"
     try:
         _, _, dV0 = run_chain(fb, V, X, G, b, fused=True)
     finally:
         del os.environ["FASTH_PANEL"]
+        del os.environ["FASTH_LB"]
     assert rel(dV, host(dV0)) <= 2e-5
 
 

@@ -126,3 +126,41 @@ def test_gemm_hook_tcgen05():
             assert f(p(A), K, p(B), N if mn else K, mn, M, N, K, None, N, 1.0, 0.0, None, N, None, None, N, None,
                      None, M, p(part), 3, 0) == 0
             assert rel(part.sum(0), ref2) < 1e-5
+
+
+def test_large_batch_two_call_equals_fused(monkeypatch):
+    """fasth_forward + fasth_backward (tape = the forward stages) run the same
+    kernels as the fused call: bitwise equal; the tape is reusable."""
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.delenv("FASTH_LB", raising=False)  # default selection: m >= 1024, d >= 512
+    V, X, G = inputs(1024, 1024, 2048, seed=9)
+    Yf, bf = fb.fasth_forward_backward(V, X, G, 32)
+    tape = fb.fasth_forward(V, X, 32)
+    b1 = fb.fasth_backward(tape, G)
+    b2 = fb.fasth_backward(tape, G)
+    torch.cuda.synchronize()
+    assert torch.equal(tape.output(), Yf)
+    for a in (b1, b2):
+        assert torch.equal(a.grad_input, bf.grad_input)
+        assert torch.equal(a.grad_vectors, bf.grad_vectors)
+    Yr, dXr, dVr = model64(V, X, G, 64)
+    assert max(rel(Yf, Yr), rel(bf.grad_input, dXr), rel(bf.grad_vectors, dVr)) <= TOL
+
+
+def test_large_batch_unaligned_outputs(monkeypatch):
+    """Output pitches that the 16-byte epilogue stores cannot take go through
+    packed temporaries (OutBuf)."""
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.setenv("FASTH_LB", "1")
+    n = d = 512
+    m = 1024
+    V, X, G = inputs(n, d, m, seed=11)
+    Y0, b0 = fb.fasth_forward_backward(V, X, G, 32)
+    big = torch.zeros(m, d + 3, device="cuda")  # ld = d + 3
+    Y = big[:, :d].t()
+    big2 = torch.zeros(m, d + 3, device="cuda")
+    dX = big2[:, :d].t()
+    dV = torch.empty(n, d, device="cuda")
+    fb.fasth_forward_backward(V, X, G, 32, out=(Y, dX, dV))
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Y0) and torch.equal(dX, b0.grad_input) and torch.equal(dV, b0.grad_vectors)
