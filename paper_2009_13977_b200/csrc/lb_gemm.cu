@@ -523,9 +523,10 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.M = g.M;
     p.N = g.N;
     p.nseg = g.nseg;
-    // CTA pairs (256-row tiles) once M is large enough to keep 74 pairs busy
+    // CTA pairs (256-row tiles) from M = 512 on (B-row products run 64 pairs)
     static const int pair_env = getenv("FASTH_LB_PAIR") ? atoi(getenv("FASTH_LB_PAIR")) : -1;
-    const bool pair = pair_env >= 0 ? (pair_env != 0 && g.M > BM) : g.M >= 1024;
+    static const int pair_min = getenv("FASTH_LB_PAIR_MIN") ? atoi(getenv("FASTH_LB_PAIR_MIN")) : 512;
+    const bool pair = pair_env >= 0 ? (pair_env != 0 && g.M > BM) : g.M >= pair_min;
     int tot_kb = 0;
     for (int sg = 0; sg < g.nseg; ++sg) {
         const Segment& S = g.seg[sg];
