@@ -68,6 +68,10 @@ struct Gemm {
     int64_t ldd = 0;
     float *d_hi = nullptr, *d_lo = nullptr;
     int64_t lds = 0;
+    // split_trunc: D written as (x, x - trunc_tf32(x)) instead of (RN hi, lo):
+    // the tensor core truncates x itself, so the pair is still an exact split,
+    // and a later epilogue reads the value back as one array (c_single: C = c_hi)
+    bool split_trunc = false, c_single = false;
     float *t_hi = nullptr, *t_lo = nullptr;  // transposed split copy D^T (N x M)
     int64_t ldt = 0;
     float* partial = nullptr;                // [nz][ksplit][M][N]
@@ -94,8 +98,9 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
 
 // Elementwise helpers (lb_path.cu).
 // split rows x cols (ld_in) into hi/lo (ld_out)
+// (trunc: the (x, x - trunc_tf32(x)) form, see Gemm::split_trunc)
 cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, float* lo,
-                  int64_t ldo, cudaStream_t s);
+                  int64_t ldo, cudaStream_t s, bool trunc = false);
 // VT = V^T split: V is n x d (ldv), VT d x n
 cudaError_t split_transpose(const float* v, int64_t ldv, int n, int d, float* hi, float* lo,
                             int64_t ldo, cudaStream_t s);

@@ -51,6 +51,7 @@ struct Params {
     int64_t ldd;
     float *d_hi, *d_lo;
     int64_t lds;
+    int split_trunc, c_single;
     float *t_hi, *t_lo;
     int64_t ldt;
     float* partial;
@@ -67,8 +68,11 @@ __device__ __forceinline__ void mb_expect(uint32_t a, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
                  : "memory");
 }
+// Relaxed arrives: the epilogue signals "accumulator read back" (its
+// tcgen05.ld already waited); a release arrive would stall on the warp's
+// outstanding global stores (MEMBAR) before signalling.
 __device__ __forceinline__ void mb_arrive(uint32_t a) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 #ifndef LB_HANG_DEBUG
 __device__ __forceinline__ void mb_wait(uint32_t a, uint32_t parity) {
@@ -120,7 +124,7 @@ __device__ __forceinline__ uint32_t mapa_u32(uint32_t a, uint32_t rank) {
     return o;
 }
 __device__ __forceinline__ void mb_arrive_cluster(uint32_t a) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -181,6 +185,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 
 __device__ __forceinline__ float rn_hi(float x) {  // round to nearest tf32 (10-bit mantissa)
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+__device__ __forceinline__ float tr_hi(float x) {  // what the tensor core reads of x
+    return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
 struct TileInfo {
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                         if (grow < p.M && gcol < p.N) {
                             const int64_t off = ((int64_t)ti.z * p.z_out + grow) * p.ldc + gcol;
                             chv[i] = __ldcs(reinterpret_cast<const float4*>(p.c_hi + off));
-                            clv[i] = __ldcs(reinterpret_cast<const float4*>(p.c_lo + off));
+                            if (!p.c_single) clv[i] = __ldcs(reinterpret_cast<const float4*>(p.c_lo + off));
                         }
                     }
                 }
@@ -452,18 +459,29 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                         } else {
                             const int64_t gr = (int64_t)ti.z * p.z_out + grow;
                             if (p.c_hi) {
-                                const float4 ch = chv[i], cl = clv[i];
-                                a.x += p.beta * (ch.x + cl.x);
-                                a.y += p.beta * (ch.y + cl.y);
-                                a.z += p.beta * (ch.z + cl.z);
-                                a.w += p.beta * (ch.w + cl.w);
+                                float4 c = chv[i];
+                                if (!p.c_single) {
+                                    const float4 cl = clv[i];
+                                    c = make_float4(c.x + cl.x, c.y + cl.y, c.z + cl.z, c.w + cl.w);
+                                }
+                                a.x += p.beta * c.x;
+                                a.y += p.beta * c.y;
+                                a.z += p.beta * c.z;
+                                a.w += p.beta * c.w;
                             }
                             if (p.d_f32) *reinterpret_cast<float4*>(p.d_f32 + gr * p.ldd + gcol) = a;
                             if (p.d_hi) {
-                                const float4 h = make_float4(rn_hi(a.x), rn_hi(a.y), rn_hi(a.z), rn_hi(a.w));
-                                *reinterpret_cast<float4*>(p.d_hi + gr * p.lds + gcol) = h;
-                                *reinterpret_cast<float4*>(p.d_lo + gr * p.lds + gcol) =
-                                    make_float4(a.x - h.x, a.y - h.y, a.z - h.z, a.w - h.w);
+                                const float4 h = p.split_trunc ? make_float4(tr_hi(a.x), tr_hi(a.y), tr_hi(a.z), tr_hi(a.w))
+                                                               : make_float4(rn_hi(a.x), rn_hi(a.y), rn_hi(a.z), rn_hi(a.w));
+                                if (p.split_trunc) {  // (x, x - trunc(x))
+                                    *reinterpret_cast<float4*>(p.d_hi + gr * p.lds + gcol) = a;
+                                    *reinterpret_cast<float4*>(p.d_lo + gr * p.lds + gcol) =
+                                        make_float4(a.x - h.x, a.y - h.y, a.z - h.z, a.w - h.w);
+                                } else {
+                                    *reinterpret_cast<float4*>(p.d_hi + gr * p.lds + gcol) = h;
+                                    *reinterpret_cast<float4*>(p.d_lo + gr * p.lds + gcol) =
+                                        make_float4(a.x - h.x, a.y - h.y, a.z - h.z, a.w - h.w);
+                                }
                             }
                         }
                     }
@@ -573,6 +591,8 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.d_hi = g.d_hi;
     p.d_lo = g.d_lo;
     p.lds = g.lds;
+    p.split_trunc = g.split_trunc ? 1 : 0;
+    p.c_single = g.c_single ? 1 : 0;
     p.t_hi = g.t_hi;
     p.t_lo = g.t_lo;
     p.ldt = g.ldt;

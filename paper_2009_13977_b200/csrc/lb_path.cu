@@ -11,28 +11,35 @@ namespace {
 __device__ __forceinline__ float rn_hi(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
 }
+// (x, x - trunc(x)) when `trunc`: hi stays x (the tensor core truncates it)
+__device__ __forceinline__ float split_hi(float x, bool trunc) {
+    return trunc ? x : rn_hi(x);
+}
+__device__ __forceinline__ float split_lo(float x, bool trunc) {
+    return trunc ? x - __uint_as_float(__float_as_uint(x) & 0xffffe000u) : x - rn_hi(x);
+}
 
 __global__ void split_kernel(const float* __restrict__ x, int64_t ldx, int rows, int cols, float* __restrict__ hi,
-                             float* __restrict__ lo, int64_t ldo) {
+                             float* __restrict__ lo, int64_t ldo, bool trunc) {
     const int64_t total = (int64_t)rows * cols;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / cols), c = (int)(i % cols);
         const float v = x[r * ldx + c];
-        const float h = rn_hi(v);
-        hi[r * ldo + c] = h;
-        lo[r * ldo + c] = v - h;
+        hi[r * ldo + c] = split_hi(v, trunc);
+        lo[r * ldo + c] = split_lo(v, trunc);
     }
 }
 
 __global__ void split4_kernel(const float4* __restrict__ x, int64_t ldx4, int rows, int cols4, float4* __restrict__ hi,
-                              float4* __restrict__ lo, int64_t ldo4) {
+                              float4* __restrict__ lo, int64_t ldo4, bool trunc) {
     const int64_t total = (int64_t)rows * cols4;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int r = (int)(i / cols4), c = (int)(i % cols4);
         const float4 v = x[r * ldx4 + c];
-        const float4 h = make_float4(rn_hi(v.x), rn_hi(v.y), rn_hi(v.z), rn_hi(v.w));
-        hi[r * ldo4 + c] = h;
-        lo[r * ldo4 + c] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        hi[r * ldo4 + c] = make_float4(split_hi(v.x, trunc), split_hi(v.y, trunc), split_hi(v.z, trunc),
+                                       split_hi(v.w, trunc));
+        lo[r * ldo4 + c] = make_float4(split_lo(v.x, trunc), split_lo(v.y, trunc), split_lo(v.z, trunc),
+                                       split_lo(v.w, trunc));
     }
 }
 
@@ -64,7 +71,7 @@ int grid_for(int64_t work) {
 }  // namespace
 
 cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, float* lo, int64_t ldo,
-                  cudaStream_t s) {
+                  cudaStream_t s, bool trunc) {
     if (rows <= 0 || cols <= 0) return cudaSuccess;
     const bool vec = cols % 4 == 0 && ldx % 4 == 0 && ldo % 4 == 0 &&
                      !((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(hi) |
@@ -72,9 +79,9 @@ cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, fl
     if (vec)
         split4_kernel<<<grid_for((int64_t)rows * cols / 4), 256, 0, s>>>(
             reinterpret_cast<const float4*>(x), ldx / 4, rows, cols / 4, reinterpret_cast<float4*>(hi),
-            reinterpret_cast<float4*>(lo), ldo / 4);
+            reinterpret_cast<float4*>(lo), ldo / 4, trunc);
     else
-        split_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(x, ldx, rows, cols, hi, lo, ldo);
+        split_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(x, ldx, rows, cols, hi, lo, ldo, trunc);
     return cudaGetLastError();
 }
 

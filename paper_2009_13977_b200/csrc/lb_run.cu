@@ -395,7 +395,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
     }
     // ---- forward: stage nb = split X; stage j = output of block j
     ++nl;
-    LBTRY(split(X, ldx, m, d, Sth[nb], Stl[nb], d, s));
+    LBTRY(split(X, ldx, m, d, Sth[nb], Stl[nb], d, s, true));  // stages: (x, x - trunc(x))
     for (int j = nb - 1; j >= 0; --j) {
         {
             Gemm g;  // ZfT = A WfR_j^T (m x B), Zf_j = its transpose (B x m)
@@ -424,12 +424,13 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             g.seg[0].K = B;
             g.alpha = -2.f;
             g.beta = 1.f;
-            g.c_hi = Sth[j + 1];
-            g.c_lo = Stl[j + 1];
+            g.c_hi = Sth[j + 1];  // = the activation itself (trunc split)
+            g.c_single = true;
             g.ldc = d;
             g.d_hi = Sth[j];
             g.d_lo = Stl[j];
             g.lds = d;
+            g.split_trunc = true;
             if (j == 0) {
                 g.d_f32 = Y;
                 g.ldd = ldy;
@@ -454,7 +455,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     cudaError_t e;
     // ---- backward
     ++nl;
-    LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s));
+    LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s, true));
     int cur = 0;
     for (int j = 0; j < nb; ++j) {
         {
@@ -532,11 +533,12 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.alpha = -2.f;
             g.beta = 1.f;
             g.c_hi = Gh[cur];
-            g.c_lo = Gl[cur];
+            g.c_single = true;
             g.ldc = d;
             g.d_hi = Gh[cur ^ 1];
             g.d_lo = Gl[cur ^ 1];
             g.lds = d;
+            g.split_trunc = true;
             if (j == nb - 1) {
                 g.d_f32 = dX;
                 g.ldd = lddx;
