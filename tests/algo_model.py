@@ -10,9 +10,9 @@ oracle without a GPU (the GPU suite then checks the kernels themselves).
 import numpy as np
 
 
-def blocks(n, b):
+def blocks(n, b, cap=64):
     b = min(max(b, 1), n)
-    b = min(b, 64)  # wider blocks run as 64-wide sub-blocks
+    b = min(b, cap)  # wider blocks run as 64-wide sub-blocks (chain kernels)
     return [(lo, min(lo + b, n)) for lo in range(0, n, b)]
 
 
@@ -23,11 +23,13 @@ def t_tilde(Vb):
     return np.linalg.inv(M)
 
 
-def fwd_bwd(V, X, Gout, b):
-    """V: (n, d) chain, X, Gout: (d, m).  Returns Y, dX, dV (n, d)."""
+def fwd_bwd(V, X, Gout, b, cap=64):
+    """V: (n, d) chain, X, Gout: (d, m).  Returns Y, dX, dV (n, d).
+    cap: widest block run as one (64 = the chain kernels; the large-batch path
+    of csrc/lb_*.cu runs 128/256/512-wide blocks: cap=None)."""
     n, d = V.shape
     Vt = V.T
-    bl = blocks(n, b)
+    bl = blocks(n, b, cap if cap else n)
     Ts = [t_tilde(Vt[:, lo:hi]) for lo, hi in bl]
     # forward sweep, recording activations A_i (block output) and Z'f
     A = X.copy()

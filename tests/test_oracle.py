@@ -154,3 +154,21 @@ def test_device_algorithm_model_vs_oracle(port, d, n, m, b):
     got = fwd_bwd(V, X, Gm, b)
     for a, w in zip(got, want):
         assert rel(a, w) < 1e-11
+
+
+@pytest.mark.parametrize("d,n,m", [(256, 256, 6), (300, 256, 5), (512, 384, 4)])
+def test_wide_block_algebra_vs_oracle(port, d, n, m):
+    """The large-batch path (csrc/lb_*.cu) re-blocks the chain into 128/256/512-
+    wide WY blocks whatever the caller's block width: in f64 the blocked
+    algebra with those widths equals the reference's result (its own b) to
+    1e-11 — the product and its gradients do not depend on the blocking."""
+    from tests.algo_model import fwd_bwd
+    rng = np.random.default_rng(d + n + m)
+    V, X, Gm = rng.standard_normal((n, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = port.fasth_fwd_bwd(V, X, Gm, 32)
+    for B in (128, 256, 512):
+        if n % B:
+            continue
+        got = fwd_bwd(V, X, Gm, B, cap=None)
+        for a, w in zip(got, want):
+            assert rel(a, w) < 1e-11, (B, rel(a, w))
