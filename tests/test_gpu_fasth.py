@@ -342,6 +342,37 @@ def test_host_pipelined_equals_device_bitwise(fb, d, n, m, b):
             assert np.array_equal(u.double().numpy(), w)
 
 
+def test_host_graph_replay_tracks_buffer_contents(fb):
+    """Same pinned buffers call after call: the host entry replays its cached
+    CUDA graph; new contents of V, X, G must still flow through (the graph
+    copies from the caller's buffers every replay), bitwise equal to the
+    device-resident call; FASTH_HOST_GRAPH=0 (eager) gives the same bits."""
+    import torch
+    d, n, m, b = 256, 256, 32, 32
+    Vh = torch.empty(n, d).pin_memory()
+    Xh = torch.empty(m, d).pin_memory()
+    Gh = torch.empty(m, d).pin_memory()
+    out = tuple(torch.empty(sh).pin_memory() for sh in ((m, d), (m, d), (n, d)))
+    ctx = fb.Context(0)
+    for seed in range(4):
+        g = torch.Generator().manual_seed(seed)
+        Vh.copy_(torch.randn(n, d, generator=g))
+        Xh.copy_(torch.randn(m, d, generator=g))
+        Gh.copy_(torch.randn(m, d, generator=g))
+        got = fb.forward_backward_host(Vh, Xh, Gh, b, ctx=ctx, out=out)
+        Yd, back = fb.fasth_forward_backward(Vh.cuda(), Xh.cuda().t(), Gh.cuda().t(), b, ctx=ctx)
+        want = (Yd.t().cpu(), back.grad_input.t().cpu(), back.grad_vectors.cpu())
+        for u, w in zip(got, want):
+            assert torch.equal(u, w), seed
+    os.environ["FASTH_HOST_GRAPH"] = "0"
+    try:
+        eager = [t.clone() for t in fb.forward_backward_host(Vh, Xh, Gh, b, ctx=ctx, out=out)]
+    finally:
+        del os.environ["FASTH_HOST_GRAPH"]
+    for u, w in zip(eager, want):
+        assert torch.equal(u, w)
+
+
 # ---- SVD layer -------------------------------------------------------------
 
 def svd_param(fb, U, V, s, out_dim, in_dim):
