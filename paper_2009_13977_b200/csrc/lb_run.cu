@@ -60,77 +60,84 @@ __global__ void diag_inv_kernel(const float* __restrict__ Mm, int B, float* __re
 // T_z = M_z^{-1} by blocked back-substitution over 32-row chunks:
 //   T[rc][cc] = Dinv_rc (E - sum_{k > rc} M[rc][k] T[k][cc]).
 // One CTA per pair of 32-column chunks (cc, B/32-1-cc) for balanced work.
-// The update product is register blocked: 64 threads x (4 rows x 4 columns)
-// cover the 32 x 32 block, 4 thread groups split k; the M row panel is staged
-// transposed ([k][row]) so both operands are 16-byte shared loads.  Writes T
-// and T^T, both split.  grid (B/64, nz), 256 threads.
+// The M row panel of step rc-1 streams into shared memory (cp.async, double
+// buffered) while step rc computes; the update product is register blocked:
+// 64 threads x (4 rows x 4 columns) cover the 32 x 32 block, 4 thread groups
+// take contiguous quarters of k.  Writes T and T^T, both split.
+// grid (B/64, nz), 256 threads.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
 __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ Mm, const float* __restrict__ Dinv,
                                                       int B, float* __restrict__ Th, float* __restrict__ Tl,
                                                       float* __restrict__ TTh, float* __restrict__ TTl) {
     extern __shared__ float sm[];
+    const int MP = B + 12;          // panel pitch: at most 2-way conflicts for the float4 reads
     float* Tc = sm;                 // [B][32] solution chunk
-    float* MpT = Tc + B * 32;       // [B][36] staged row panel, transposed
-    float* red = MpT + B * 36;      // [4][32][33] k-split partial sums
+    float* Mp = Tc + B * 32;        // [2][32][MP] M row panels
+    float* red = Mp + 2 * 32 * MP;  // [4][32][33] k-split partial sums
     float* R = red + 4 * 32 * 33;   // [32][33] right-hand side
-    float* Dd = R + 32 * 33;        // [32][33] diagonal-block inverse
+    float* Ddb = R + 32 * 33;       // [2][32][36] diagonal-block inverses
     const int z = blockIdx.y, nchunk = B / 32;
     const float* M = Mm + (int64_t)z * B * B;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int kq = tid >> 6, t64 = tid & 63, rg = t64 >> 3, cg = t64 & 7;
     for (int pass = 0; pass < 2; ++pass) {
         const int cc = pass == 0 ? blockIdx.x : nchunk - 1 - blockIdx.x;
-        const int c0 = cc * 32;
+        const int c0 = cc * 32, k1 = c0 + 32;
+        // step rc's operands -> buffer rc & 1: the M panel (rows rc*32..,
+        // columns [(rc+1)*32, k1)) and Dinv_rc
+        auto prefetch = [&](int rc) {
+            if (rc < 0) return;
+            const int k0 = (rc + 1) * 32, nf4 = (k1 - k0) / 4;
+            float* dst = Mp + (rc & 1) * 32 * MP;
+            for (int e = tid; e < 32 * nf4; e += 256) {
+                const int i = e / nf4, k = k0 + 4 * (e % nf4);
+                cp_async16(dst + i * MP + k, M + (int64_t)(rc * 32 + i) * B + k);
+            }
+            const float* D = Dinv + ((int64_t)z * nchunk + rc) * 1024;
+            float* dd = Ddb + (rc & 1) * 32 * 36;
+            const int i = tid >> 3, k = (tid & 7) * 4;
+            cp_async16(dd + i * 36 + k, D + i * 32 + k);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
         __syncthreads();
         for (int e = tid; e < B * 32; e += 256) Tc[e] = 0.f;
+        prefetch(cc);
         __syncthreads();
         for (int rc = cc; rc >= 0; --rc) {
-            const int r0 = rc * 32, k0 = (rc + 1) * 32, k1 = c0 + 32;
-            {  // stage M[r0 + i][k0..k1) transposed, and Dinv_rc
-                float4 buf[4][4];
+            const int r0 = rc * 32, k0 = (rc + 1) * 32;
+            const float* Dd = Ddb + (rc & 1) * 32 * 36;
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();  // panel rc landed (all threads' copies); the other buffer is free
+            prefetch(rc - 1);
+            {  // partial products over this group's quarter of [k0, k1)
+                const int q4 = (k1 - k0) / 4;
+                const int kb = k0 + kq * q4, ke = kb + q4;
+                const float* mp = Mp + (rc & 1) * 32 * MP + (4 * rg) * MP;
+                float acc[4][4] = {};
+                for (int k = kb; k < ke; k += 4) {
+                    float4 m4[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                    for (int a = 0; a < 4; ++a) m4[a] = *reinterpret_cast<const float4*>(mp + a * MP + k);
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int k = k0 + 4 * lane + 128 * v;
-                        if (k < k1)
-                            buf[u][v] = __ldg(reinterpret_cast<const float4*>(M + (int64_t)(r0 + warp + 8 * u) * B + k));
-                    }
-                const float* D = Dinv + ((int64_t)z * nchunk + rc) * 1024;
-                float dv[4];
+                    for (int kk = 0; kk < 4; ++kk) {
+                        const float4 t4 = *reinterpret_cast<const float4*>(Tc + (k + kk) * 32 + 4 * cg);
+                        const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
 #pragma unroll
-                for (int u = 0; u < 4; ++u) dv[u] = __ldg(D + (warp + 8 * u) * 32 + lane);
+                        for (int a2 = 0; a2 < 4; ++a2) {
+                            const float mv = kk == 0 ? m4[a2].x : kk == 1 ? m4[a2].y : kk == 2 ? m4[a2].z : m4[a2].w;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = warp + 8 * u;
-#pragma unroll
-                    for (int v = 0; v < 4; ++v) {
-                        const int k = k0 + 4 * lane + 128 * v;
-                        if (k < k1) {
-                            MpT[(k + 0) * 36 + i] = buf[u][v].x;
-                            MpT[(k + 1) * 36 + i] = buf[u][v].y;
-                            MpT[(k + 2) * 36 + i] = buf[u][v].z;
-                            MpT[(k + 3) * 36 + i] = buf[u][v].w;
+                            for (int bq = 0; bq < 4; ++bq) acc[a2][bq] = fmaf(mv, tv[bq], acc[a2][bq]);
                         }
                     }
-                    Dd[i * 33 + lane] = dv[u];
-                }
-            }
-            __syncthreads();
-            {  // partial products over k = k0 + kq, k0 + kq + 4, ...
-                float acc[4][4] = {};
-                for (int k = k0 + kq; k < k1; k += 4) {
-                    const float4 m4 = *reinterpret_cast<const float4*>(MpT + k * 36 + 4 * rg);
-                    const float4 t4 = *reinterpret_cast<const float4*>(Tc + k * 32 + 4 * cg);
-                    const float mv[4] = {m4.x, m4.y, m4.z, m4.w}, tv[4] = {t4.x, t4.y, t4.z, t4.w};
-#pragma unroll
-                    for (int a = 0; a < 4; ++a)
-#pragma unroll
-                        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(mv[a], tv[b], acc[a][b]);
                 }
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                for (int a2 = 0; a2 < 4; ++a2)
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) red[(kq * 32 + 4 * rg + a) * 33 + 4 * cg + b] = acc[a][b];
+                    for (int bq = 0; bq < 4; ++bq) red[(kq * 32 + 4 * rg + a2) * 33 + 4 * cg + bq] = acc[a2][bq];
             }
             __syncthreads();
             for (int e = tid; e < 1024; e += 256) {
@@ -144,11 +151,11 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
                 const int r = tid >> 3, c4 = (tid & 7) * 4;
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
                 for (int k = r; k < 32; ++k) {
-                    const float d = Dd[r * 33 + k];
-                    a0 = fmaf(d, R[k * 33 + c4 + 0], a0);
-                    a1 = fmaf(d, R[k * 33 + c4 + 1], a1);
-                    a2 = fmaf(d, R[k * 33 + c4 + 2], a2);
-                    a3 = fmaf(d, R[k * 33 + c4 + 3], a3);
+                    const float dd = Dd[r * 36 + k];
+                    a0 = fmaf(dd, R[k * 33 + c4 + 0], a0);
+                    a1 = fmaf(dd, R[k * 33 + c4 + 1], a1);
+                    a2 = fmaf(dd, R[k * 33 + c4 + 2], a2);
+                    a3 = fmaf(dd, R[k * 33 + c4 + 3], a3);
                 }
                 *reinterpret_cast<float4*>(Tc + (r0 + r) * 32 + c4) = make_float4(a0, a1, a2, a3);
             }
@@ -165,12 +172,19 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
             th[(int64_t)r * B + c0 + c] = h;
             tl[(int64_t)r * B + c0 + c] = v - h;
         }
-        for (int e = tid; e < B * 32; e += 256) {
-            const int c = e / B, r = e % B;  // coalesced along r
-            const float v = Tc[r * 32 + c];
-            const float h = rn_hi(v);
-            tth[(int64_t)(c0 + c) * B + r] = h;
-            ttl[(int64_t)(c0 + c) * B + r] = v - h;
+        for (int rb = 0; rb < B / 32; ++rb) {  // T^T through a padded 32 x 32 tile (red)
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) red[lane * 33 + warp + 8 * u] = Tc[(rb * 32 + warp + 8 * u) * 32 + lane];
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = warp + 8 * u;
+                const float v = red[c * 33 + lane];
+                const float h = rn_hi(v);
+                tth[(int64_t)(c0 + c) * B + rb * 32 + lane] = h;
+                ttl[(int64_t)(c0 + c) * B + rb * 32 + lane] = v - h;
+            }
         }
     }
 }
@@ -366,7 +380,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
     {
         ++nl;
         diag_inv_kernel<<<dim3(B / 32, nb), 32, 0, s>>>(Mm, B, Dinv);
-        const int smem = (B * 32 + B * 36 + 4 * 32 * 33 + 2 * 32 * 33) * 4;
+        const int smem = (B * 32 + 2 * 32 * (B + 12) + 4 * 32 * 33 + 32 * 33 + 2 * 32 * 36) * 4;
         static int attr = 0;
         if (attr < smem) {
             LBTRY(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
