@@ -210,7 +210,34 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
     ctx.check()
     flops = (12.0 * d * d * m + 4.0 * d * d * b) * world
     tf = flops / (ms * 1e-3) / 1e12
+    # per-kernel: CUDA events around every launch of the large-batch path
+    # (ctx timing mode), untimed steps; algorithmic flops per launch below
+    ctx.set_timing(True)
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    kt = ctx.kernel_times()
+    ctx.set_timing(False)
+    Bw, nb = 512, d // 512
+    fl = {"lb_f1_zf": 2.0 * m * Bw * d, "lb_k1_zb": 2.0 * m * Bw * d, "lb_f2_update": 2.0 * m * d * Bw,
+          "lb_k4_update": 2.0 * m * d * Bw, "lb_dv": 2.0 * Bw * d * (2 * m + Bw), "lb_q": 2.0 * Bw * Bw * m,
+          "lb_build_gram": 2.0 * Bw * Bw * d * nb, "lb_build_w": 2.0 * Bw * d * Bw * nb}
+    kern = {k: {"us_per_launch": v[0] * 1e3 / v[1], "launches_per_step": v[1] / 3,
+                "tflops": fl[k] / (v[0] * 1e-3 / v[1]) / 1e12 if k in fl else None}
+            for k, v in kt.items() if k.startswith("lb_")}
+    top = max((k for k in kern if k in fl), key=lambda k: kern[k]["us_per_launch"] * kern[k]["launches_per_step"])
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json"))).get(top)
+    except Exception:
+        pass
+    roof = {"bound": "tensor", "kernel": top, "achieved": kern[top]["tflops"], "peak": peak_3xtf32,
+            "unit": "TFLOP/s", "frac": kern[top]["tflops"] / peak_3xtf32, "traffic": traffic,
+            "flops_per_launch": fl[top],
+            "note": "3xTF32 useful flops; CUDA events per launch on the context stream; ncu tensor-pipe "
+                    "activity of these GEMMs in profiles/r01_lb_pair_gemm_full.txt"}
     return {"workload": "BASELINE configs[4]: FastH fwd+bwd d=2048, batch-sharded, dV all-reduced (NCCL)",
+            "roofline": roof, "kernels": kern,
             "d": d, "batch_per_gpu": m, "global_batch": m * world, "n_gpus": world,
             "us_per_step": ms * 1e3, "tflops": tf, "frac_3xtf32_peak": tf / (peak_3xtf32 * world),
             "steps": steps, "warmup": warmup, "gpu_launches_per_step": launches,

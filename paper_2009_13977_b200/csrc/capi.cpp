@@ -948,6 +948,25 @@ struct OutBuf {
     }
 };
 
+// Per-launch CUDA events for the large-batch kernels in timing mode 1
+// (reported through fasth_ctx_kernel_times next to the chain kernels).
+struct LbTimer final : fasthb::lb::Timer {
+    fasth_ctx c;
+    cudaEvent_t a = nullptr;
+    explicit LbTimer(fasth_ctx cx) : c(cx) {}
+    void begin(cudaStream_t s) override {
+        cudaEventCreate(&a);
+        cudaEventRecord(a, s);
+    }
+    void end(cudaStream_t s, const char* name) override {
+        cudaEvent_t b = nullptr;
+        cudaEventCreate(&b);
+        cudaEventRecord(b, s);
+        c->pending.push_back({name, a, b});
+        a = nullptr;
+    }
+};
+
 fasth_status lb_status(fasth_ctx c, cudaError_t e, const char* what) {
     return e == cudaSuccess ? FASTH_OK : fail(FASTH_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
@@ -961,11 +980,13 @@ fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, in
     fasth_status s = y.open(d, m);
     if (s == FASTH_OK) s = dx.open(d, m);
     int nl = 1;
+    LbTimer lt(c);
     if (s == FASTH_OK)
         s = c->timed(
             [&] {
                 return fasthb::lb::forward_backward(V, ldv, d, n, X, ldx, G, ldg, m, y.ptr(), y.pitch(d), dx.ptr(),
-                                                    dx.pitch(d), dV, lddv, ws, c->err_d, c->stream, c->num_sms, &nl);
+                                                    dx.pitch(d), dV, lddv, ws, c->err_d, c->stream, c->num_sms, &nl,
+                                                    c->timing == 1 ? &lt : nullptr);
             },
             "large_batch(fwd+bwd)");
     c->launches += nl - 1;

@@ -82,6 +82,14 @@ struct Gemm {
 // split count actually used (no empty K splits).
 cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms);
 
+// Optional per-launch timing (the context's timing mode): begin() before a
+// launch, end() after it with the kernel's name.
+struct Timer {
+    virtual void begin(cudaStream_t s) = 0;
+    virtual void end(cudaStream_t s, const char* name) = 0;
+    virtual ~Timer() = default;
+};
+
 // The whole large-batch step (lb_run.cu).
 int pick_block(int n);
 bool supported(int d, int n, int m);
@@ -89,12 +97,14 @@ size_t workspace_floats(int d, int n, int m, bool want_dv);
 // The two halves (fasth_forward / fasth_backward): `ws` carries the forward
 // stages from one to the other.
 cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
-                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch);
+                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
+                    Timer* tm = nullptr);
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
-                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch);
+                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm = nullptr);
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
-                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch);
+                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
+                             Timer* tm = nullptr);
 
 // Elementwise helpers (lb_path.cu).
 // split rows x cols (ld_in) into hi/lo (ld_out)

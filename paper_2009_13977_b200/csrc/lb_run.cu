@@ -347,7 +347,7 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
 // Build (V -> T~, WfR, WbR) and the forward chain; the workspace keeps every
 // forward stage for the backward half.
 cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
-                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch) {
+                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm) {
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
@@ -371,7 +371,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g.z_b_row = B;
         g.partial = Gp;
         g.ksplit = ksG;
-        LBTRY(gemm(g, s, num_sms));
+        if (tm) tm->begin(s);
+            LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_build_gram");
         ++nl;
         g_ks = g.ksplit;
     }
@@ -387,7 +389,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             attr = smem;
         }
         ++nl;
+        if (tm) tm->begin(s);
         tri_inv_kernel<<<dim3(B / 64, nb), 256, smem, s>>>(Mm, Dinv, B, Th, Tl, TTh, TTl);
+        if (tm) tm->end(s, "lb_build_tri_inv");
         LBTRY(cudaGetLastError());
     }
     for (int w = 0; w < 2; ++w) {  // WfR = T V_j, WbR = T^T V_j  (B x d per block)
@@ -404,7 +408,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g.d_hi = w == 0 ? WfH : WbH;
         g.d_lo = w == 0 ? WfL : WbL;
         g.lds = d;
-        LBTRY(gemm(g, s, num_sms));
+        if (tm) tm->begin(s);
+            LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_build_w");
         ++nl;
     }
     // ---- forward: stage nb = split X; stage j = output of block j
@@ -425,7 +431,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             g.t_hi = Zfh + (size_t)j * B * m;
             g.t_lo = Zfl + (size_t)j * B * m;
             g.ldt = m;
+            if (tm) tm->begin(s);
             LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_f1_zf");
         ++nl;
         }
         {
@@ -449,7 +457,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
                 g.d_f32 = Y;
                 g.ldd = ldy;
             }
+            if (tm) tm->begin(s);
             LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_f2_update");
         ++nl;
         }
     }
@@ -459,7 +469,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
 
 // Backward chain and dV from the forward's workspace (same d, n, m).
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
-                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch) {
+                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm) {
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
@@ -486,7 +496,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.t_hi = Zbh;
             g.t_lo = Zbl;
             g.ldt = m;
+            if (tm) tm->begin(s);
             LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_k1_zb");
         ++nl;
         }
         if (want_dv) {
@@ -500,7 +512,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.seg[0].K = m;
                 g.partial = Qp;
                 g.ksplit = ksQ;
-                LBTRY(gemm(g, s, num_sms));
+                if (tm) tm->begin(s);
+            LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_q");
         ++nl;
                 q_ks = g.ksplit;
             }
@@ -528,7 +542,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.alpha = -2.f;
                 g.partial = dVp;
                 g.ksplit = ksV;
-                LBTRY(gemm(g, s, num_sms));
+                if (tm) tm->begin(s);
+            LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_dv");
         ++nl;
                 v_ks = g.ksplit;
             }
@@ -557,7 +573,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.d_f32 = dX;
                 g.ldd = lddx;
             }
+            if (tm) tm->begin(s);
             LBTRY(gemm(g, s, num_sms));
+            if (tm) tm->end(s, "lb_k4_update");
         ++nl;
         }
         cur ^= 1;
@@ -568,10 +586,11 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
 
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
-                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch) {
+                             int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
+                             Timer* tm) {
     int n1 = 0, n2 = 0;
-    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1);
-    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2);
+    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1, tm);
+    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm);
     if (nlaunch) *nlaunch = n1 + n2;
     return e;
 }
