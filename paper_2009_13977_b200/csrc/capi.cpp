@@ -123,6 +123,21 @@ struct fasth_ctx_s {
     // step (copies, kernels, read-back) replayed with one launch while the
     // caller keeps passing the same buffers; buffers the captured sequence
     // released stay reserved for the graph until it is dropped
+    // second stream + fork/join events of the large-batch step (lb.h Streams)
+    fasthb::lb::Streams lb_st;
+    const fasthb::lb::Streams* lb_streams() {
+        if (const char* e = getenv("FASTH_LB_STREAMS"))
+            if (atoi(e) == 0) return nullptr;
+        if (!lb_st.aux) {
+            if (cudaStreamCreateWithFlags(&lb_st.aux, cudaStreamNonBlocking) != cudaSuccess) {
+                lb_st.aux = nullptr;
+                cudaGetLastError();
+                return nullptr;
+            }
+            for (auto& ev : lb_st.ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        }
+        return &lb_st;
+    }
     bool capturing = false;
     std::vector<void*> graph_held;
     cudaGraphExec_t host_exec = nullptr;
@@ -825,6 +840,11 @@ fasth_status fasth_ctx_destroy(fasth_ctx c) {
     if (c->logdet_d) cudaFree(c->logdet_d);
 
     if (c->err_h) cudaFreeHost(c->err_h);
+    if (c->lb_st.aux) {
+        cudaStreamDestroy(c->lb_st.aux);
+        for (auto ev : c->lb_st.ev)
+            if (ev) cudaEventDestroy(ev);
+    }
     delete c;
     return FASTH_OK;
 }
@@ -986,7 +1006,7 @@ fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, in
             [&] {
                 return fasthb::lb::forward_backward(V, ldv, d, n, X, ldx, G, ldg, m, y.ptr(), y.pitch(d), dx.ptr(),
                                                     dx.pitch(d), dV, lddv, ws, c->err_d, c->stream, c->num_sms, &nl,
-                                                    c->timing == 1 ? &lt : nullptr);
+                                                    c->timing == 1 ? &lt : nullptr, c->lb_streams());
             },
             "large_batch(fwd+bwd)");
     c->launches += nl - 1;
@@ -1018,7 +1038,7 @@ fasth_status lb_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, 
         s = c->timed(
             [&] {
                 return fasthb::lb::forward(V, ldv, d, n, X, ldx, m, y.ptr(), y.pitch(d), t->lb_ws, c->err_d,
-                                           c->stream, c->num_sms, &nl);
+                                           c->stream, c->num_sms, &nl, nullptr, c->lb_streams());
             },
             "large_batch(fwd)");
     c->launches += nl - 1;
@@ -1088,7 +1108,7 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
         TRY(c->timed(
             [&] {
                 return fasthb::lb::backward(d, n, m, G, ldg, dx.ptr(), dx.pitch(d), dV, lddv, t->lb_ws, c->stream,
-                                            c->num_sms, &nl);
+                                            c->num_sms, &nl, nullptr, c->lb_streams());
             },
             "large_batch(bwd)"));
         c->launches += nl - 1;

@@ -90,21 +90,32 @@ struct Timer {
     virtual ~Timer() = default;
 };
 
+// A second stream for the independent work of the step (input splits during
+// the build; the Q / dV products of block j while the gradient update of
+// block j runs), with reusable fork/join events.  nullptr: one stream.
+struct Streams {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[8] = {};
+};
+
 // The whole large-batch step (lb_run.cu).
 int pick_block(int n);
 bool supported(int d, int n, int m);
 size_t workspace_floats(int d, int n, int m, bool want_dv);
 // The two halves (fasth_forward / fasth_backward): `ws` carries the forward
 // stages from one to the other.
+// (forward: G non-null also splits the gradient for a following backward
+// called with g_split = true — the fused call)
 cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
                     int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
-                    Timer* tm = nullptr);
+                    Timer* tm = nullptr, const Streams* st = nullptr, const float* G = nullptr, int64_t ldg = 0);
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
-                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm = nullptr);
+                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm = nullptr,
+                     const Streams* st = nullptr, bool g_split = false);
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
-                             Timer* tm = nullptr);
+                             Timer* tm = nullptr, const Streams* st = nullptr);
 
 // Elementwise helpers (lb_path.cu).
 // split rows x cols (ld_in) into hi/lo (ld_out)

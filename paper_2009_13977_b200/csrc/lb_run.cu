@@ -260,9 +260,9 @@ size_t workspace_floats(int d, int n, int m, bool want_dv) {
     f += 4 * (size_t)nb * bb;       // T, T^T split
     f += 4 * nd;                    // WfR, WbR split
     f += 2 * (size_t)(nb + 1) * md;  // forward stages split
-    f += 2 * (size_t)m * B * 2;     // ZfT, ZbT split
+    f += 2 * (size_t)m * B * 3;     // ZfT, ZbT (x2) split
     f += 2 * (size_t)n * m;         // Zf (natural, all blocks) split
-    f += 2 * (size_t)B * m;         // Zb natural split
+    f += 4 * (size_t)B * m;         // Zb natural split (x2)
     f += 4 * md;                    // two gradient buffers split
     (void)want_dv;                  // the forward carves the backward's buffers too
     f += 16 * bb + 3 * bb;          // Q partials, Q, S split
@@ -287,7 +287,7 @@ struct Bufs {
     size_t nd = 0, md = 0, bb = 0;
     float *Vh, *Vl, *VTh, *VTl, *Gp, *Mm, *Dinv, *Th, *Tl, *TTh, *TTl, *WfH, *WfL, *WbH, *WbL;
     float *Sth[kMaxStages], *Stl[kMaxStages];
-    float *ZfTh, *ZfTl, *ZbTh, *ZbTl, *Zfh, *Zfl, *Zbh, *Zbl, *Gh[2], *Gl[2];
+    float *ZfTh, *ZfTl, *ZbTh2[2], *ZbTl2[2], *Zfh, *Zfl, *Zbh2[2], *Zbl2[2], *Gh[2], *Gl[2];
     float *Qp, *Qs, *Sh, *Sl, *dVp;
 };
 constexpr int ksG = 4, ksQ = 16, ksV = 4;  // split-K counts (128 CTAs each: one tile per CTA)
@@ -312,9 +312,9 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
         b.Stl[j] = c.take(md);
     }
     b.ZfTh = c.take((size_t)m * B), b.ZfTl = c.take((size_t)m * B);
-    b.ZbTh = c.take((size_t)m * B), b.ZbTl = c.take((size_t)m * B);
+    for (int i = 0; i < 2; ++i) b.ZbTh2[i] = c.take((size_t)m * B), b.ZbTl2[i] = c.take((size_t)m * B);
     b.Zfh = c.take((size_t)n * m), b.Zfl = c.take((size_t)n * m);
-    b.Zbh = c.take((size_t)B * m), b.Zbl = c.take((size_t)B * m);
+    for (int i = 0; i < 2; ++i) b.Zbh2[i] = c.take((size_t)B * m), b.Zbl2[i] = c.take((size_t)B * m);
     b.Gh[0] = c.take(md), b.Gh[1] = c.take(md), b.Gl[0] = c.take(md), b.Gl[1] = c.take(md);
     b.Qp = c.take(ksQ * bb);
     b.Qs = c.take(bb);
@@ -334,12 +334,12 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
     (void)bb;                                                                                                \
     float *Vh = b.Vh, *Vl = b.Vl, *VTh = b.VTh, *VTl = b.VTl, *Gp = b.Gp, *Mm = b.Mm, *Dinv = b.Dinv;       \
     float *Th = b.Th, *Tl = b.Tl, *TTh = b.TTh, *TTl = b.TTl, *WfH = b.WfH, *WfL = b.WfL, *WbH = b.WbH;      \
-    float *WbL = b.WbL, **Sth = b.Sth, **Stl = b.Stl, *ZfTh = b.ZfTh, *ZfTl = b.ZfTl, *ZbTh = b.ZbTh;       \
-    float *ZbTl = b.ZbTl, *Zfh = b.Zfh, *Zfl = b.Zfl, *Zbh = b.Zbh, *Zbl = b.Zbl, **Gh = b.Gh, **Gl = b.Gl; \
+    float *WbL = b.WbL, **Sth = b.Sth, **Stl = b.Stl, *ZfTh = b.ZfTh, *ZfTl = b.ZfTl;                        \
+    float *Zfh = b.Zfh, *Zfl = b.Zfl, **Gh = b.Gh, **Gl = b.Gl;                                              \
     float *Qp = b.Qp, *Qs = b.Qs, *Sh = b.Sh, *Sl = b.Sl, *dVp = b.dVp;                                    \
     (void)Vh, (void)Vl, (void)VTh, (void)VTl, (void)Gp, (void)Mm, (void)Dinv, (void)Th, (void)Tl, (void)TTh; \
     (void)TTl, (void)WfH, (void)WfL, (void)WbH, (void)WbL, (void)Sth, (void)Stl, (void)ZfTh, (void)ZfTl;     \
-    (void)ZbTh, (void)ZbTl, (void)Zfh, (void)Zfl, (void)Zbh, (void)Zbl, (void)Gh, (void)Gl, (void)Qp;       \
+    (void)Zfh, (void)Zfl, (void)Gh, (void)Gl, (void)Qp;                                                    \
     (void)Qs, (void)Sh, (void)Sl, (void)dVp
 
 }  // namespace
@@ -347,13 +347,29 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
 // Build (V -> T~, WfR, WbR) and the forward chain; the workspace keeps every
 // forward stage for the backward half.
 cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
-                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm) {
+                    int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm,
+                    const Streams* st, const float* G, int64_t ldg) {
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
     if (Y && ((ldy % 4) || (reinterpret_cast<uintptr_t>(Y) & 15))) return cudaErrorInvalidValue;
     LB_ALIASES;
     cudaError_t e;
+    // the input splits do not depend on the build: on the second stream (the
+    // triangular inverse leaves most SMs idle)
+    const bool two = st && st->aux;
+    cudaStream_t sx = two ? st->aux : s;
+    if (two) {
+        LBTRY(cudaEventRecord(st->ev[0], s));
+        LBTRY(cudaStreamWaitEvent(sx, st->ev[0], 0));
+    }
+    ++nl;
+    LBTRY(split(X, ldx, m, d, Sth[nb], Stl[nb], d, sx, true));  // stages: (x, x - trunc(x))
+    if (G) {
+        ++nl;
+        LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, sx, true));
+    }
+    if (two) LBTRY(cudaEventRecord(st->ev[1], sx));
     // ---- build: split V and V^T, Gram per block, T~, WfR = T~ V_j, WbR = T~^T V_j
     ++nl;
     LBTRY(split(V, ldv, n, d, Vh, Vl, d, s));
@@ -414,8 +430,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         ++nl;
     }
     // ---- forward: stage nb = split X; stage j = output of block j
-    ++nl;
-    LBTRY(split(X, ldx, m, d, Sth[nb], Stl[nb], d, s, true));  // stages: (x, x - trunc(x))
+    if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[1], 0));
     for (int j = nb - 1; j >= 0; --j) {
         {
             Gemm g;  // ZfT = A WfR_j^T (m x B), Zf_j = its transpose (B x m)
@@ -469,7 +484,8 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
 
 // Backward chain and dV from the forward's workspace (same d, n, m).
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
-                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm) {
+                     int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm,
+                     const Streams* st, bool g_split) {
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
@@ -477,11 +493,19 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     const bool want_dv = dV != nullptr;
     LB_ALIASES;
     cudaError_t e;
-    // ---- backward
-    ++nl;
-    LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s, true));
+    // ---- backward.  Block j: K1 (Zb) on the main stream, then Q and dV of
+    // block j on the second stream while the main stream updates G (K4); Zb
+    // is double buffered, and K4 of block j+1 (which overwrites block j's G)
+    // waits for block j's dV.
+    if (!g_split) {
+        ++nl;
+        LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s, true));
+    }
+    const bool two = st && st->aux && want_dv;
+    cudaStream_t sa = two ? st->aux : s;
     int cur = 0;
     for (int j = 0; j < nb; ++j) {
+        float *ZbTh = b.ZbTh2[j & 1], *ZbTl = b.ZbTl2[j & 1], *Zbh = b.Zbh2[j & 1], *Zbl = b.Zbl2[j & 1];
         {
             Gemm g;  // ZbT = G WbR_j^T, Zb = transpose
             g.M = m;
@@ -502,6 +526,10 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
         ++nl;
         }
         if (want_dv) {
+            if (two) {
+                LBTRY(cudaEventRecord(st->ev[2], s));
+                LBTRY(cudaStreamWaitEvent(sa, st->ev[2], 0));
+            }
             int q_ks = ksQ, v_ks = ksV;
             {
                 Gemm g;  // Q = Zf_j Zb^T (split K)
@@ -512,16 +540,16 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.seg[0].K = m;
                 g.partial = Qp;
                 g.ksplit = ksQ;
-                if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_q");
+                if (tm) tm->begin(sa);
+            LBTRY(gemm(g, sa, num_sms));
+            if (tm) tm->end(sa, "lb_q");
         ++nl;
                 q_ks = g.ksplit;
             }
             ++nl;
-    q_sum_kernel<<<(int)((bb + 255) / 256), 256, 0, s>>>(Qp, q_ks, (int64_t)bb, Qs);
+    q_sum_kernel<<<(int)((bb + 255) / 256), 256, 0, sa>>>(Qp, q_ks, (int64_t)bb, Qs);
             ++nl;
-            s_from_q_kernel<<<dim3(B / 32, B / 32), dim3(32, 8), 0, s>>>(Qs, B, Sh, Sl);
+            s_from_q_kernel<<<dim3(B / 32, B / 32), dim3(32, 8), 0, sa>>>(Qs, B, Sh, Sl);
             {
                 Gemm g;  // dV_j partials = -2 (Zb A_j + Zf_j G) + S V_j   (S = -4 K'^T pre-scaled by -1/2)
                 g.M = B;
@@ -542,17 +570,20 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.alpha = -2.f;
                 g.partial = dVp;
                 g.ksplit = ksV;
-                if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_dv");
+                if (tm) tm->begin(sa);
+            LBTRY(gemm(g, sa, num_sms));
+            if (tm) tm->end(sa, "lb_dv");
         ++nl;
                 v_ks = g.ksplit;
             }
             ++nl;
-    dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, s>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv,
+    dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv,
                                                                        lddv);
+            if (two) LBTRY(cudaEventRecord(st->ev[4 + (j & 1)], sa));
         }
         {
+            // block j-1's dV read the G buffer this update overwrites
+            if (two && j > 0) LBTRY(cudaStreamWaitEvent(s, st->ev[4 + ((j - 1) & 1)], 0));
             Gemm g;  // G <- G - 2 ZbT VT_j^T
             g.M = m;
             g.N = d;
@@ -580,6 +611,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
         }
         cur ^= 1;
     }
+    if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[4 + ((nb - 1) & 1)], 0));  // join: dV complete
     if (nlaunch) *nlaunch = nl;
     return cudaGetLastError();
 }
@@ -587,10 +619,10 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
-                             Timer* tm) {
+                             Timer* tm, const Streams* st) {
     int n1 = 0, n2 = 0;
-    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1, tm);
-    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm);
+    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1, tm, st, G, ldg);
+    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm, st, true);
     if (nlaunch) *nlaunch = n1 + n2;
     return e;
 }
