@@ -11,8 +11,8 @@
 // and one backward step, for the m x d gradient Gm and the block's output
 // activations Am (the forward tape),
 //   ZbT = Gm WbR_j^T
-//   Q   = Zf Zb^T               (B x B)   GEMM  K=m (Zf, Zb: the B x m copies)
-//   dV_j = -2 (Zb Am + Zf Gm) - 4 K'^T V_j,   K' = striu(Q - Q^T)
+//   Q   = Zf Zb^T               (B x B)   GEMM  K=m (A = ZfT, B = ZbT read MN-major)
+//   dV_j = -2 (Zb Am + Zf Gm) - 4 K'^T V_j,   K' = striu(Q - Q^T)   (A operands MN-major)
 //   Gm <- Gm - 2 ZbT VT_j^T
 // — exactly tests/algo_model.py's algebra with block width B (the product is
 // independent of the blocking; the reference's own results agree across block
@@ -55,6 +55,7 @@ struct Gemm {
     int M = 0, N = 0;
     int nseg = 1;
     Segment seg[3];
+    bool a_mn = false;    // A stored K x M (M contiguous): segment rows are k, columns m
     bool b_mn = false;    // B stored K x N (N contiguous)
     int ksplit = 1;       // > 1 (or partial != nullptr): raw partials per K split
     int nz = 1;           // batched products, coordinates advance per z:

@@ -208,7 +208,7 @@ __device__ __forceinline__ TileInfo decode(const Params& p, int t) {
     return ti;
 }
 
-template <bool B_MN, bool PAIR>
+template <bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Params p) {
     // PAIR: a 2-CTA cluster runs one 256 x 256 tile with tcgen05.mma.cta_group::2;
     // each CTA loads its 128 A rows and its half (128 rows) of the B tile
@@ -291,10 +291,21 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                     if (leader) mb_expect(fb, STG * CM);  // the pair's bytes land on the leader's barrier
                     if constexpr (PAIR) fb = (p.debug_swap & 4) ? (fb & 0xFEFFFFFFu) : mapa_u32(fb, 0);
                     const uint32_t base = su32(smem + stage * STG);
-                    const int ar = p.a_row0[sg] + ti.z * p.z_a_row + ti.m0 + (int)rank * BM;
-                    const int ac = p.a_col0[sg] + ti.z * p.z_a_col + k0;
-                    tma2d<PAIR>(base, &p.ta_hi[sg], ac, ar, fb);
-                    tma2d<PAIR>(base + A_TILE, &p.ta_lo[sg], ac, ar, fb);
+                    if constexpr (!A_MN) {
+                        const int ar = p.a_row0[sg] + ti.z * p.z_a_row + ti.m0 + (int)rank * BM;
+                        const int ac = p.a_col0[sg] + ti.z * p.z_a_col + k0;
+                        tma2d<PAIR>(base, &p.ta_hi[sg], ac, ar, fb);
+                        tma2d<PAIR>(base + A_TILE, &p.ta_lo[sg], ac, ar, fb);
+                    } else {
+                        // K x M storage (rows k, columns m): boxes of (32 m) x (32 k)
+                        const int ar = p.a_row0[sg] + ti.z * p.z_a_row + k0;
+                        const int ac = p.a_col0[sg] + ti.z * p.z_a_col + ti.m0 + (int)rank * BM;
+#pragma unroll
+                        for (int c = 0; c < BM / 32; ++c) {
+                            tma2d<PAIR>(base + c * (BK * 128), &p.ta_hi[sg], ac + 32 * c, ar, fb);
+                            tma2d<PAIR>(base + A_TILE + c * (BK * 128), &p.ta_lo[sg], ac + 32 * c, ar, fb);
+                        }
+                    }
                     if constexpr (!B_MN) {
                         const int br = p.b_row0[sg] + ti.z * p.z_b_row + ti.n0 + (int)rank * BNC;
                         const int bc = p.b_col0[sg] + ti.z * p.z_b_col + k0;
@@ -321,7 +332,8 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     } else if (warp == 1 && leader) {
         // ---------------- MMA issuer ----------------
         // instruction descriptor: D f32, A/B tf32, A K-major, B K- or MN-major, N=256, M=128
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((B_MN && !(p.debug_swap & 2) ? 1u : 0u) << 16) |
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                               ((B_MN && !(p.debug_swap & 2) ? 1u : 0u) << 16) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CM) >> 4) << 24);
         uint32_t b_lbo = 0, b_sbo = 1024;
         const uint64_t b_layout = B_MN ? 1 : 2;
@@ -355,8 +367,10 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                     const uint32_t bh = base + 2 * A_TILE, bl = bh + B_T;
 #pragma unroll
                     for (int ks = 0; ks < BK / 8; ++ks) {
-                        const uint64_t dah = sdesc(ah + ks * 32, 0, 1024);
-                        const uint64_t dal = sdesc(al + ks * 32, 0, 1024);
+                        // MN-major operands: 32-byte-atom swizzle, 32-wide chunks 4 KB apart,
+                        // 4-deep K groups 512 B apart; one MMA K step = 8 rows = 1 KB
+                        const uint64_t dah = A_MN ? sdesc(ah + ks * 1024, BK * 128, 512, 1) : sdesc(ah + ks * 32, 0, 1024);
+                        const uint64_t dal = A_MN ? sdesc(al + ks * 1024, BK * 128, 512, 1) : sdesc(al + ks * 32, 0, 1024);
                         const uint32_t boff = B_MN ? ks * 1024 : ks * 32;
                         const uint64_t dbh = sdesc(bh + boff, b_lbo, b_sbo, b_layout);
                         const uint64_t dbl = sdesc(bl + boff, b_lbo, b_sbo, b_layout);
@@ -542,8 +556,8 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.N = g.N;
     p.nseg = g.nseg;
     // CTA pairs (256-row tiles) from M = 512 on (B-row products run 64 pairs)
-    static const int pair_env = getenv("FASTH_LB_PAIR") ? atoi(getenv("FASTH_LB_PAIR")) : -1;
-    static const int pair_min = getenv("FASTH_LB_PAIR_MIN") ? atoi(getenv("FASTH_LB_PAIR_MIN")) : 512;
+    const int pair_env = getenv("FASTH_LB_PAIR") ? atoi(getenv("FASTH_LB_PAIR")) : -1;
+    const int pair_min = getenv("FASTH_LB_PAIR_MIN") ? atoi(getenv("FASTH_LB_PAIR_MIN")) : 512;
     const bool pair = pair_env >= 0 ? (pair_env != 0 && g.M > BM) : g.M >= pair_min;
     int tot_kb = 0;
     for (int sg = 0; sg < g.nseg; ++sg) {
@@ -555,8 +569,10 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
         p.a_col0[sg] = S.a_col0;
         p.b_row0[sg] = S.b_row0;
         p.b_col0[sg] = S.b_col0;
-        bool ok = make_map(&p.ta_hi[sg], S.A.hi, S.A.rows, S.A.cols, S.A.ld, BK, BM) &&
-                  make_map(&p.ta_lo[sg], S.A.lo, S.A.rows, S.A.cols, S.A.ld, BK, BM);
+        bool ok = g.a_mn ? make_map(&p.ta_hi[sg], S.A.hi, S.A.rows, S.A.cols, S.A.ld, 32, BK, true) &&
+                               make_map(&p.ta_lo[sg], S.A.lo, S.A.rows, S.A.cols, S.A.ld, 32, BK, true)
+                         : make_map(&p.ta_hi[sg], S.A.hi, S.A.rows, S.A.cols, S.A.ld, BK, BM) &&
+                               make_map(&p.ta_lo[sg], S.A.lo, S.A.rows, S.A.cols, S.A.ld, BK, BM);
         if (!g.b_mn)
             ok = ok && make_map(&p.tb_hi[sg], S.B.hi, S.B.rows, S.B.cols, S.B.ld, BK, pair ? BN / 2 : BN) &&
                  make_map(&p.tb_lo[sg], S.B.lo, S.B.rows, S.B.cols, S.B.ld, BK, pair ? BN / 2 : BN);
@@ -598,14 +614,18 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.ldt = g.ldt;
     p.partial = g.partial;
     p.debug_swap = g.debug_swap;
-    static bool attr_set[4] = {false, false, false, false};
-    const int which = (g.b_mn ? 1 : 0) + (pair ? 2 : 0);
+    static bool attr_set[8] = {};
+    const int which = (g.b_mn ? 1 : 0) + (pair ? 2 : 0) + (g.a_mn ? 4 : 0);
     void (*kern)(Params) = nullptr;
     switch (which) {
-        case 0: kern = gemm_kernel<false, false>; break;
-        case 1: kern = gemm_kernel<true, false>; break;
-        case 2: kern = gemm_kernel<false, true>; break;
-        default: kern = gemm_kernel<true, true>; break;
+        case 0: kern = gemm_kernel<false, false, false>; break;
+        case 1: kern = gemm_kernel<false, true, false>; break;
+        case 2: kern = gemm_kernel<false, false, true>; break;
+        case 3: kern = gemm_kernel<false, true, true>; break;
+        case 4: kern = gemm_kernel<true, false, false>; break;
+        case 5: kern = gemm_kernel<true, true, false>; break;
+        case 6: kern = gemm_kernel<true, false, true>; break;
+        default: kern = gemm_kernel<true, true, true>; break;
     }
     if (!attr_set[which]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);

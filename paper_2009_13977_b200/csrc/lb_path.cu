@@ -100,20 +100,22 @@ cudaError_t split_transpose(const float* v, int64_t ldv, int n, int d, float* hi
 // path on caller device buffers.  A: M x K row-major; B: N x K (b_mn = 0) or
 // K x N (b_mn = 1) row-major; optional C (M x N).  Outputs any of D (fp32),
 // D hi/lo, D^T hi/lo, or raw split-K partials [ksplit][M][N].
-extern "C" int fasthb_lb_gemm_test(const float* A, int64_t lda, const float* B, int64_t ldb, int b_mn, int M,
-                                   int N, int K, const float* C, int64_t ldc, float alpha, float beta, float* D,
-                                   int64_t ldd, float* Dhi, float* Dlo, int64_t lds, float* Thi, float* Tlo,
-                                   int64_t ldt, float* partial, int ksplit, int debug_swap) {
+// a_mn = 1: A given K x M (M contiguous).
+extern "C" int fasthb_lb_gemm_test_ex(const float* A, int64_t lda, int a_mn, const float* B, int64_t ldb, int b_mn,
+                                      int M, int N, int K, const float* C, int64_t ldc, float alpha, float beta,
+                                      float* D, int64_t ldd, float* Dhi, float* Dlo, int64_t lds, float* Thi,
+                                      float* Tlo, int64_t ldt, float* partial, int ksplit, int debug_swap) {
     using namespace fasthb::lb;
     cudaStream_t s = 0;
+    const int64_t arows = a_mn ? K : M, acols = a_mn ? M : K;
     const int64_t brows = b_mn ? K : N, bcols = b_mn ? N : K;
-    const int64_t lda_p = (K + 3) / 4 * 4, ldb_p = (bcols + 3) / 4 * 4, ldc_p = (N + 3) / 4 * 4;
+    const int64_t lda_p = (acols + 3) / 4 * 4, ldb_p = (bcols + 3) / 4 * 4, ldc_p = (N + 3) / 4 * 4;
     float *ah, *al, *bh, *bl, *ch = nullptr, *cl = nullptr;
-    cudaMalloc(&ah, M * lda_p * 4);
-    cudaMalloc(&al, M * lda_p * 4);
+    cudaMalloc(&ah, arows * lda_p * 4);
+    cudaMalloc(&al, arows * lda_p * 4);
     cudaMalloc(&bh, brows * ldb_p * 4);
     cudaMalloc(&bl, brows * ldb_p * 4);
-    split(A, lda, M, K, ah, al, lda_p, s);
+    split(A, lda, (int)arows, (int)acols, ah, al, lda_p, s);
     split(B, ldb, (int)brows, (int)bcols, bh, bl, ldb_p, s);
     if (C) {
         cudaMalloc(&ch, (int64_t)M * ldc_p * 4);
@@ -124,7 +126,8 @@ extern "C" int fasthb_lb_gemm_test(const float* A, int64_t lda, const float* B, 
     g.M = M;
     g.N = N;
     g.nseg = 1;
-    g.seg[0].A = Operand{ah, al, M, K, lda_p};
+    g.seg[0].A = Operand{ah, al, arows, acols, lda_p};
+    g.a_mn = a_mn != 0;
     g.seg[0].B = Operand{bh, bl, brows, bcols, ldb_p};
     g.seg[0].K = K;
     g.b_mn = b_mn != 0;
@@ -157,4 +160,12 @@ extern "C" int fasthb_lb_gemm_test(const float* A, int64_t lda, const float* B, 
     if (cl) cudaFree(cl);
     if (e != cudaSuccess) return (int)e;
     return (int)e2;
+}
+
+extern "C" int fasthb_lb_gemm_test(const float* A, int64_t lda, const float* B, int64_t ldb, int b_mn, int M, int N,
+                                   int K, const float* C, int64_t ldc, float alpha, float beta, float* D,
+                                   int64_t ldd, float* Dhi, float* Dlo, int64_t lds, float* Thi, float* Tlo,
+                                   int64_t ldt, float* partial, int ksplit, int debug_swap) {
+    return fasthb_lb_gemm_test_ex(A, lda, 0, B, ldb, b_mn, M, N, K, C, ldc, alpha, beta, D, ldd, Dhi, Dlo, lds, Thi,
+                                  Tlo, ldt, partial, ksplit, debug_swap);
 }

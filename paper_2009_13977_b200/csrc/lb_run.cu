@@ -204,8 +204,9 @@ __global__ void q_sum_kernel(const float* __restrict__ part, int ks, int64_t per
     Q[e] = s;
 }
 
-// S = 2 K'^T (the dV product's alpha = -2 makes it -4 K'^T), K' = striu(Q - Q^T);
-// split.  32 x 32 tiles through shared memory.  grid (B/32, B/32), 32 x 8 threads.
+// S = 2 K'^T (the dV product's alpha = -2 makes it -4 K'^T), K' = striu(Q - Q^T),
+// written transposed (the dV product reads every A operand K x M); split.
+// 32 x 32 tiles through shared memory.  grid (B/32, B/32), 32 x 8 threads.
 __global__ void s_from_q_kernel(const float* __restrict__ Q, int B, float* __restrict__ Sh, float* __restrict__ Sl) {
     __shared__ float qt[32][33], qtt[32][33];
     const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32, tx = threadIdx.x;
@@ -214,9 +215,9 @@ __global__ void s_from_q_kernel(const float* __restrict__ Q, int B, float* __res
         qtt[r][tx] = Q[(int64_t)(b0 + r) * B + a0 + tx];  // Q[b0+r][a0+tx]
     }
     __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += 8) {
+    for (int r = threadIdx.y; r < 32; r += 8) {  // S^T[a][b] = S[b][a] = 2 (Q[a][b] - Q[b][a]) for a < b
         const int a = a0 + r, b = b0 + tx;
-        const float v = b < a ? 2.f * (qtt[tx][r] - qt[r][tx]) : 0.f;  // 2 (Q[b][a] - Q[a][b])
+        const float v = a < b ? 2.f * (qt[r][tx] - qtt[tx][r]) : 0.f;
         const float h = rn_hi(v);
         Sh[(int64_t)a * B + b] = h;
         Sl[(int64_t)a * B + b] = v - h;
@@ -260,9 +261,8 @@ size_t workspace_floats(int d, int n, int m, bool want_dv) {
     f += 4 * (size_t)nb * bb;       // T, T^T split
     f += 4 * nd;                    // WfR, WbR split
     f += 2 * (size_t)(nb + 1) * md;  // forward stages split
-    f += 2 * (size_t)m * B * 3;     // ZfT, ZbT (x2) split
-    f += 2 * (size_t)n * m;         // Zf (natural, all blocks) split
-    f += 4 * (size_t)B * m;         // Zb natural split (x2)
+    f += 2 * (size_t)m * B * 2;     // ZbT (x2) split
+    f += 2 * (size_t)n * m;         // ZfT of all blocks (m x n) split
     f += 4 * md;                    // two gradient buffers split
     (void)want_dv;                  // the forward carves the backward's buffers too
     f += 16 * bb + 3 * bb;          // Q partials, Q, S split
@@ -287,7 +287,7 @@ struct Bufs {
     size_t nd = 0, md = 0, bb = 0;
     float *Vh, *Vl, *VTh, *VTl, *Gp, *Mm, *Dinv, *Th, *Tl, *TTh, *TTl, *WfH, *WfL, *WbH, *WbL;
     float *Sth[kMaxStages], *Stl[kMaxStages];
-    float *ZfTh, *ZfTl, *ZbTh2[2], *ZbTl2[2], *Zfh, *Zfl, *Zbh2[2], *Zbl2[2], *Gh[2], *Gl[2];
+    float *ZbTh2[2], *ZbTl2[2], *ZfAh, *ZfAl, *Gh[2], *Gl[2];  // ZfA: m x n, block j = columns jB..
     float *Qp, *Qs, *Sh, *Sl, *dVp;
 };
 constexpr int ksG = 4, ksQ = 16, ksV = 4;  // split-K counts (128 CTAs each: one tile per CTA)
@@ -311,10 +311,8 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
         b.Sth[j] = c.take(md);
         b.Stl[j] = c.take(md);
     }
-    b.ZfTh = c.take((size_t)m * B), b.ZfTl = c.take((size_t)m * B);
     for (int i = 0; i < 2; ++i) b.ZbTh2[i] = c.take((size_t)m * B), b.ZbTl2[i] = c.take((size_t)m * B);
-    b.Zfh = c.take((size_t)n * m), b.Zfl = c.take((size_t)n * m);
-    for (int i = 0; i < 2; ++i) b.Zbh2[i] = c.take((size_t)B * m), b.Zbl2[i] = c.take((size_t)B * m);
+    b.ZfAh = c.take((size_t)m * n), b.ZfAl = c.take((size_t)m * n);
     b.Gh[0] = c.take(md), b.Gh[1] = c.take(md), b.Gl[0] = c.take(md), b.Gl[1] = c.take(md);
     b.Qp = c.take(ksQ * bb);
     b.Qs = c.take(bb);
@@ -334,12 +332,12 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
     (void)bb;                                                                                                \
     float *Vh = b.Vh, *Vl = b.Vl, *VTh = b.VTh, *VTl = b.VTl, *Gp = b.Gp, *Mm = b.Mm, *Dinv = b.Dinv;       \
     float *Th = b.Th, *Tl = b.Tl, *TTh = b.TTh, *TTl = b.TTl, *WfH = b.WfH, *WfL = b.WfL, *WbH = b.WbH;      \
-    float *WbL = b.WbL, **Sth = b.Sth, **Stl = b.Stl, *ZfTh = b.ZfTh, *ZfTl = b.ZfTl;                        \
-    float *Zfh = b.Zfh, *Zfl = b.Zfl, **Gh = b.Gh, **Gl = b.Gl;                                              \
+    float *WbL = b.WbL, **Sth = b.Sth, **Stl = b.Stl, *ZfAh = b.ZfAh, *ZfAl = b.ZfAl;                        \
+    float **Gh = b.Gh, **Gl = b.Gl;                                                                          \
     float *Qp = b.Qp, *Qs = b.Qs, *Sh = b.Sh, *Sl = b.Sl, *dVp = b.dVp;                                    \
     (void)Vh, (void)Vl, (void)VTh, (void)VTl, (void)Gp, (void)Mm, (void)Dinv, (void)Th, (void)Tl, (void)TTh; \
-    (void)TTl, (void)WfH, (void)WfL, (void)WbH, (void)WbL, (void)Sth, (void)Stl, (void)ZfTh, (void)ZfTl;     \
-    (void)Zfh, (void)Zfl, (void)Gh, (void)Gl, (void)Qp;                                                    \
+    (void)TTl, (void)WfH, (void)WfL, (void)WbH, (void)WbL, (void)Sth, (void)Stl, (void)ZfAh, (void)ZfAl;     \
+    (void)Gh, (void)Gl, (void)Qp;                                                                          \
     (void)Qs, (void)Sh, (void)Sl, (void)dVp
 
 }  // namespace
@@ -440,12 +438,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             g.seg[0].B = Operand{WfH, WfL, n, d, d};
             g.seg[0].b_row0 = j * B;
             g.seg[0].K = d;
-            g.d_hi = ZfTh;
-            g.d_lo = ZfTl;
-            g.lds = B;
-            g.t_hi = Zfh + (size_t)j * B * m;
-            g.t_lo = Zfl + (size_t)j * B * m;
-            g.ldt = m;
+            g.d_hi = ZfAh + (size_t)j * B;  // columns jB.. of the m x n ZfT of all blocks
+            g.d_lo = ZfAl + (size_t)j * B;
+            g.lds = n;
             if (tm) tm->begin(s);
             LBTRY(gemm(g, s, num_sms));
             if (tm) tm->end(s, "lb_f1_zf");
@@ -455,7 +450,8 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             Gemm g;  // A_j = A_{j+1} - 2 ZfT VT_j^T
             g.M = m;
             g.N = d;
-            g.seg[0].A = Operand{ZfTh, ZfTl, m, B, B};
+            g.seg[0].A = Operand{ZfAh, ZfAl, m, n, n};
+            g.seg[0].a_col0 = j * B;
             g.seg[0].B = Operand{VTh, VTl, d, n, n};
             g.seg[0].b_col0 = j * B;
             g.seg[0].K = B;
@@ -505,7 +501,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     cudaStream_t sa = two ? st->aux : s;
     int cur = 0;
     for (int j = 0; j < nb; ++j) {
-        float *ZbTh = b.ZbTh2[j & 1], *ZbTl = b.ZbTl2[j & 1], *Zbh = b.Zbh2[j & 1], *Zbl = b.Zbl2[j & 1];
+        float *ZbTh = b.ZbTh2[j & 1], *ZbTl = b.ZbTl2[j & 1];
         {
             Gemm g;  // ZbT = G WbR_j^T, Zb = transpose
             g.M = m;
@@ -517,9 +513,6 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.d_hi = ZbTh;
             g.d_lo = ZbTl;
             g.lds = B;
-            g.t_hi = Zbh;
-            g.t_lo = Zbl;
-            g.ldt = m;
             if (tm) tm->begin(s);
             LBTRY(gemm(g, s, num_sms));
             if (tm) tm->end(s, "lb_k1_zb");
@@ -532,11 +525,13 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             }
             int q_ks = ksQ, v_ks = ksV;
             {
-                Gemm g;  // Q = Zf_j Zb^T (split K)
+                Gemm g;  // Q = Zf_j Zb^T (split K): A = ZfT columns jB.., B = ZbT, both MN-major
                 g.M = g.N = B;
-                g.seg[0].A = Operand{Zfh, Zfl, n, m, m};
-                g.seg[0].a_row0 = j * B;
-                g.seg[0].B = Operand{Zbh, Zbl, B, m, m};
+                g.a_mn = true;
+                g.b_mn = true;
+                g.seg[0].A = Operand{ZfAh, ZfAl, m, n, n};
+                g.seg[0].a_col0 = j * B;
+                g.seg[0].B = Operand{ZbTh, ZbTl, m, B, B};
                 g.seg[0].K = m;
                 g.partial = Qp;
                 g.ksplit = ksQ;
@@ -555,15 +550,16 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.M = B;
                 g.N = d;
                 g.nseg = 3;
+                g.a_mn = true;  // every A here is stored K x M: ZbT, ZfT, S^T
                 g.b_mn = true;
-                g.seg[0].A = Operand{Zbh, Zbl, B, m, m};
+                g.seg[0].A = Operand{ZbTh, ZbTl, m, B, B};
                 g.seg[0].B = Operand{Sth[j], Stl[j], m, d, d};
                 g.seg[0].K = m;
-                g.seg[1].A = Operand{Zfh, Zfl, n, m, m};
-                g.seg[1].a_row0 = j * B;
+                g.seg[1].A = Operand{ZfAh, ZfAl, m, n, n};
+                g.seg[1].a_col0 = j * B;
                 g.seg[1].B = Operand{Gh[cur], Gl[cur], m, d, d};
                 g.seg[1].K = m;
-                g.seg[2].A = Operand{Sh, Sl, B, B, B};
+                g.seg[2].A = Operand{Sh, Sl, B, B, B};  // S^T
                 g.seg[2].B = Operand{Vh, Vl, n, d, d};  // V_j rows: K x N, N contiguous
                 g.seg[2].b_row0 = j * B;
                 g.seg[2].K = B;

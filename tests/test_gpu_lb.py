@@ -164,3 +164,27 @@ def test_large_batch_unaligned_outputs(monkeypatch):
     fb.fasth_forward_backward(V, X, G, 32, out=(Y, dX, dV))
     torch.cuda.synchronize()
     assert torch.equal(Y, Y0) and torch.equal(dX, b0.grad_input) and torch.equal(dV, b0.grad_vectors)
+
+
+@pytest.mark.parametrize("M,N,K,b_mn,pair", [(256, 512, 256, 0, 0), (256, 512, 256, 1, 0), (1024, 512, 256, 1, 1),
+                                             (512, 768, 96, 0, 1), (300, 200, 64, 1, 0)])
+def test_gemm_hook_mn_major_a(M, N, K, b_mn, pair, monkeypatch):
+    """A operand stored K x M (MN-major, 32-byte-atom swizzle), 1-CTA and CTA-pair tiles."""
+    from paper_2009_13977_b200 import _lib
+    if pair:
+        monkeypatch.setenv("FASTH_LB_PAIR", "1")
+    lib = _lib.load()
+    f = lib.fasthb_lb_gemm_test_ex
+    P, I64, I, F = C.c_void_p, C.c_int64, C.c_int, C.c_float
+    f.argtypes = [P, I64, I, P, I64, I, I, I, I, P, I64, F, F, P, I64, P, P, I64, P, P, I64, P, I, I]
+    f.restype = I
+    p = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    At = torch.randn(K, M, device="cuda", generator=g)  # A^T stored
+    B = torch.randn(K, N, device="cuda", generator=g) if b_mn else torch.randn(N, K, device="cuda", generator=g)
+    ref = At.double().t() @ (B.double() if b_mn else B.double().t())
+    D = torch.zeros(M, N, device="cuda")
+    assert f(p(At), M, 1, p(B), N if b_mn else K, b_mn, M, N, K, None, N, 1.0, 0.0, p(D), N, None, None, N, None,
+             None, M, None, 1, 0) == 0
+    torch.cuda.synchronize()
+    assert rel(D, ref) < 1e-5
