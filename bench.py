@@ -211,13 +211,20 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
     flops = (12.0 * d * d * m + 4.0 * d * d * b) * world
     tf = flops / (ms * 1e-3) / 1e12
     # per-kernel: CUDA events around every launch of the large-batch path
-    # (ctx timing mode), untimed steps; algorithmic flops per launch below
+    # (ctx timing mode), untimed steps, one stream (concurrent kernels would
+    # stretch each other's event windows); algorithmic flops per launch below
+    saved = os.environ.get("FASTH_LB_STREAMS")
+    os.environ["FASTH_LB_STREAMS"] = "0"
     ctx.set_timing(True)
     for _ in range(3):
         step()
     torch.cuda.synchronize()
     kt = ctx.kernel_times()
     ctx.set_timing(False)
+    if saved is None:
+        del os.environ["FASTH_LB_STREAMS"]
+    else:
+        os.environ["FASTH_LB_STREAMS"] = saved
     Bw, nb = 512, d // 512
     fl = {"lb_f1_zf": 2.0 * m * Bw * d, "lb_k1_zb": 2.0 * m * Bw * d, "lb_f2_update": 2.0 * m * d * Bw,
           "lb_k4_update": 2.0 * m * d * Bw, "lb_dv": 2.0 * Bw * d * (2 * m + Bw), "lb_q": 2.0 * Bw * Bw * m,
@@ -234,8 +241,8 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
     roof = {"bound": "tensor", "kernel": top, "achieved": kern[top]["tflops"], "peak": peak_3xtf32,
             "unit": "TFLOP/s", "frac": kern[top]["tflops"] / peak_3xtf32, "traffic": traffic,
             "flops_per_launch": fl[top],
-            "note": "3xTF32 useful flops; CUDA events per launch on the context stream; ncu tensor-pipe "
-                    "activity of these GEMMs in profiles/r01_lb_pair_gemm_full.txt"}
+            "note": "3xTF32 useful flops; CUDA events per launch on the context stream (kernels serialised "
+                    "for this pass); ncu tensor-pipe activity of these GEMMs in profiles/r01_lb_*_full.txt"}
     return {"workload": "BASELINE configs[4]: FastH fwd+bwd d=2048, batch-sharded, dV all-reduced (NCCL)",
             "roofline": roof, "kernels": kern,
             "d": d, "batch_per_gpu": m, "global_batch": m * world, "n_gpus": world,
