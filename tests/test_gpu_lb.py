@@ -58,7 +58,8 @@ def inputs(n, d, m, seed=0):
     return V, X, G
 
 
-@pytest.mark.parametrize("n,d,m", [(512, 512, 1024), (1024, 1024, 2048), (384, 256, 640), (2048, 2048, 4096)])
+@pytest.mark.parametrize("n,d,m", [(512, 512, 1024), (1024, 1024, 2048), (384, 256, 640), (2048, 2048, 4096),
+                                   (640, 500, 1100), (1536, 1540, 1300), (256, 772, 228), (128, 1024, 4100)])
 def test_large_batch_matches_f64(n, d, m, monkeypatch):
     from paper_2009_13977_b200 import fasth as fb
     monkeypatch.setenv("FASTH_LB", "1")
