@@ -326,6 +326,14 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
     do {                                        \
         if ((e = (x)) != cudaSuccess) return e; \
     } while (0)
+// one GEMM launch, timed in the context's timing mode, counted
+#define LB_GEMM(g, st, name)          \
+    do {                              \
+        if (tm) tm->begin(st);        \
+        LBTRY(gemm(g, st, num_sms));  \
+        if (tm) tm->end(st, name);    \
+        ++nl;                         \
+    } while (0)
 #define LB_ALIASES                                                                                           \
     const int B = b.B, nb = b.nb;                                                                            \
     const size_t bb = b.bb;                                                                                  \
@@ -385,10 +393,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g.z_b_row = B;
         g.partial = Gp;
         g.ksplit = ksG;
-        if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_build_gram");
-        ++nl;
+        LB_GEMM(g, s, "lb_build_gram");
         g_ks = g.ksplit;
     }
     ++nl;
@@ -422,10 +427,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g.d_hi = w == 0 ? WfH : WbH;
         g.d_lo = w == 0 ? WfL : WbL;
         g.lds = d;
-        if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_build_w");
-        ++nl;
+        LB_GEMM(g, s, "lb_build_w");
     }
     // ---- forward: stage nb = split X; stage j = output of block j
     if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[1], 0));
@@ -441,10 +443,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             g.d_hi = ZfAh + (size_t)j * B;  // columns jB.. of the m x n ZfT of all blocks
             g.d_lo = ZfAl + (size_t)j * B;
             g.lds = n;
-            if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_f1_zf");
-        ++nl;
+            LB_GEMM(g, s, "lb_f1_zf");
         }
         {
             Gemm g;  // A_j = A_{j+1} - 2 ZfT VT_j^T
@@ -468,10 +467,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
                 g.d_f32 = Y;
                 g.ldd = ldy;
             }
-            if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_f2_update");
-        ++nl;
+            LB_GEMM(g, s, "lb_f2_update");
         }
     }
     if (nlaunch) *nlaunch = nl;
@@ -513,10 +509,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.d_hi = ZbTh;
             g.d_lo = ZbTl;
             g.lds = B;
-            if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_k1_zb");
-        ++nl;
+            LB_GEMM(g, s, "lb_k1_zb");
         }
         if (want_dv) {
             if (two) {
@@ -535,14 +528,11 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.seg[0].K = m;
                 g.partial = Qp;
                 g.ksplit = ksQ;
-                if (tm) tm->begin(sa);
-            LBTRY(gemm(g, sa, num_sms));
-            if (tm) tm->end(sa, "lb_q");
-        ++nl;
+                LB_GEMM(g, sa, "lb_q");
                 q_ks = g.ksplit;
             }
             ++nl;
-    q_sum_kernel<<<(int)((bb + 255) / 256), 256, 0, sa>>>(Qp, q_ks, (int64_t)bb, Qs);
+            q_sum_kernel<<<(int)((bb + 255) / 256), 256, 0, sa>>>(Qp, q_ks, (int64_t)bb, Qs);
             ++nl;
             s_from_q_kernel<<<dim3(B / 32, B / 32), dim3(32, 8), 0, sa>>>(Qs, B, Sh, Sl);
             {
@@ -566,15 +556,11 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.alpha = -2.f;
                 g.partial = dVp;
                 g.ksplit = ksV;
-                if (tm) tm->begin(sa);
-            LBTRY(gemm(g, sa, num_sms));
-            if (tm) tm->end(sa, "lb_dv");
-        ++nl;
+                LB_GEMM(g, sa, "lb_dv");
                 v_ks = g.ksplit;
             }
             ++nl;
-    dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv,
-                                                                       lddv);
+            dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv, lddv);
             if (two) LBTRY(cudaEventRecord(st->ev[4 + (j & 1)], sa));
         }
         {
@@ -600,10 +586,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 g.d_f32 = dX;
                 g.ldd = lddx;
             }
-            if (tm) tm->begin(s);
-            LBTRY(gemm(g, s, num_sms));
-            if (tm) tm->end(s, "lb_k4_update");
-        ++nl;
+            LB_GEMM(g, s, "lb_k4_update");
         }
         cur ^= 1;
     }
@@ -623,6 +606,7 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
     return e;
 }
 #undef LBTRY
+#undef LB_GEMM
 #undef LB_ALIASES
 
 }  // namespace lb
