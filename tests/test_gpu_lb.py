@@ -189,3 +189,25 @@ def test_gemm_hook_mn_major_a(M, N, K, b_mn, pair, monkeypatch):
              None, M, None, 1, 0) == 0
     torch.cuda.synchronize()
     assert rel(D, ref) < 1e-5
+
+
+def test_large_batch_host_entry_graph(monkeypatch):
+    """fasth_forward_backward_host at a large-batch shape: the cached CUDA
+    graph captures the two-stream large-batch step (fork/join events) and
+    replays it bitwise equal to the device-resident call, call after call."""
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.delenv("FASTH_LB", raising=False)
+    n = d = 512
+    m = 1024
+    V, X, G = inputs(n, d, m, seed=21)
+    Vh = V.cpu().pin_memory()
+    Xh = X.t().contiguous().cpu().pin_memory()
+    Gh = G.t().contiguous().cpu().pin_memory()
+    out = tuple(torch.empty(sh).pin_memory() for sh in ((m, d), (m, d), (n, d)))
+    ctx = fb.Context(0)
+    Yd, back = fb.fasth_forward_backward(V, X, G, 32, ctx=ctx)
+    want = (Yd.t().cpu(), back.grad_input.t().cpu(), back.grad_vectors.cpu())
+    for _ in range(3):
+        got = fb.forward_backward_host(Vh, Xh, Gh, 32, ctx=ctx, out=out)
+        for u, w in zip(got, want):
+            assert torch.equal(u, w)
