@@ -138,6 +138,16 @@ def cpu_reference(d, m, b, reps, warm=1):
     return mean * 1e6, std * 1e6, R.hardware_threads(), "reference"
 
 
+def cpu_sequential(d, m, b, reps=8):
+    """The reference's sequential-Householder path (run_bench algo=sequential:
+    single-threaded by construction, reference.hpp), timed beside FastH as
+    the north_star asks: (mean µs, std µs)."""
+    from oracle.oracle import Ref
+    R = Ref()
+    mean, std, _ = R.run_bench("mul", "sequential", d, m, b, reps, SEED, 0)
+    return mean * 1e6, std * 1e6
+
+
 def run_reference_impl(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -476,6 +486,10 @@ def main():
             cpu = {"value": us_c, "unit": "us/step", "cores": cores, "kind": kind,
                    "sample": f"reference bench::run_bench op=mul d={D} m={M} k={B} algo=fasth, "
                              f"{args.cpu_reps} reps (std {std_c:.0f} us), all host threads"}
+            us_s, std_s = cpu_sequential(D, M, B)
+            cpu["sequential"] = {"value": us_s, "unit": "us/step", "cores": 1,
+                                 "sample": f"run_bench op=mul d={D} m={M} algo=sequential (the reference's "
+                                           f"reflection-by-reflection path), 8 reps (std {std_s:.0f} us)"}
         except Exception as e:
             cpu = {"value": None, "unit": "us/step", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
