@@ -412,15 +412,7 @@ template <int BS, int TPW>
 cudaError_t launch_t(const SweepArgs& a, cudaStream_t s) {
     const SweepSmem L = sweep_layout(a.C, BS, a.d_pad, a.nstg);
     auto kern = sweep_kernel<BS, TPW>;
-    static int configured_smem = 0;
-    if ((int)L.total > configured_smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)L.total);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured_smem = (int)L.total;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total, true); e != cudaSuccess) return e;
     const int ngroups = (a.m + WC - 1) / WC;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.C * ngroups, 1, 1);

@@ -310,12 +310,7 @@ template <int RTW>
 cudaError_t launch_panel_t(const SweepV2Args& a, cudaStream_t s) {
     const PanelSmem L = panel_layout();
     auto kern = panel_kernel<RTW>;
-    static bool configured = false;
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-        if (e != cudaSuccess) return e;
-        configured = true;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total); e != cudaSuccess) return e;
     const int npanels = (a.m + PCOLS - 1) / PCOLS;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(npanels * a.ndir, 1, 1);

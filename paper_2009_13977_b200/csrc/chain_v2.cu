@@ -414,14 +414,7 @@ template <int BS, int TPW>
 cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
     const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg);
     auto kern = sweep2_kernel<BS, TPW>;
-    static size_t configured = 0;
-    if (L.total > configured) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured = L.total;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total, true); e != cudaSuccess) return e;
     const int RT = a.d_pad / a.C / 16;
     const int NR = RT < MAXNR ? RT : MAXNR;
     cudaLaunchConfig_t cfg = {};

@@ -216,13 +216,10 @@ size_t dv_smem() {
 
 template <int BS>
 cudaError_t launch_dv_t(const DvArgs& a, cudaStream_t s) {
-    static bool configured = false;
     const size_t smem = dv_smem<BS>();
-    if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(dv_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+    {
+        cudaError_t e = ensure_smem(reinterpret_cast<const void*>(dv_kernel<BS>), smem);
         if (e != cudaSuccess) return e;
-        configured = true;
     }
     const dim3 grid((a.d + RT - 1) / RT, a.q);
     dv_kernel<BS><<<grid, kThreads, smem, s>>>(a);

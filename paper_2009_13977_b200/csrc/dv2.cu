@@ -262,12 +262,8 @@ template <int BS>
 cudaError_t launch_dv2_t(const DvArgs& a, cudaStream_t s) {
     const dim3 grid((a.d_pad + DV_ROWS - 1) / DV_ROWS, a.q);
     constexpr size_t smem = dv2_smem<BS>();
-    static bool configured = false;
-    if (!configured && smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(dv2_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    configured = true;
+    if (smem > 48 * 1024)
+        if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(dv2_kernel<BS>), smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(DV_WARPS * 32, 1, 1);

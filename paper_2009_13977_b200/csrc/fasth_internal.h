@@ -26,6 +26,11 @@
 
 namespace fasthb {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize [, NonPortableClusterSizeAllowed])
+// once per (device, kernel) and size: function attributes are per device, so
+// a process driving several GPUs must configure each one (attr.cpp).
+cudaError_t ensure_smem(const void* kernel, size_t bytes, bool nonportable_cluster = false);
+
 constexpr int kThreads = 256;
 constexpr int kMaxBS = 64;
 

@@ -614,7 +614,6 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
     p.ldt = g.ldt;
     p.partial = g.partial;
     p.debug_swap = g.debug_swap;
-    static bool attr_set[8] = {};
     const int which = (g.b_mn ? 1 : 0) + (pair ? 2 : 0) + (g.a_mn ? 4 : 0);
     void (*kern)(Params) = nullptr;
     switch (which) {
@@ -627,11 +626,7 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
         case 6: kern = gemm_kernel<true, false, true>; break;
         default: kern = gemm_kernel<true, true, true>; break;
     }
-    if (!attr_set[which]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-        if (e != cudaSuccess) return e;
-        attr_set[which] = true;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), SMEM_BYTES); e != cudaSuccess) return e;
     const int units = pair ? std::max(num_sms / 2, 1) : std::max(num_sms, 1);
     const int grid = std::min(p.total, units) * (pair ? 2 : 1);
     cudaLaunchConfig_t cfg = {};

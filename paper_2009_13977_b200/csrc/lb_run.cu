@@ -402,11 +402,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         ++nl;
         diag_inv_kernel<<<dim3(B / 32, nb), 32, 0, s>>>(Mm, B, Dinv);
         const int smem = (B * 32 + 2 * 32 * (B + 12) + 4 * 32 * 33 + 32 * 33 + 2 * 32 * 36) * 4;
-        static int attr = 0;
-        if (attr < smem) {
-            LBTRY(cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr = smem;
-        }
+        LBTRY(ensure_smem(reinterpret_cast<const void*>(tri_inv_kernel), smem));
         ++nl;
         if (tm) tm->begin(s);
         tri_inv_kernel<<<dim3(B / 64, nb), 256, smem, s>>>(Mm, Dinv, B, Th, Tl, TTh, TTl);

@@ -375,15 +375,8 @@ template <int BS>
 cudaError_t launch_build_t(const Plan& p, const float* V, int64_t ldv, ErrWord* err,
                            cudaStream_t st) {
     const BuildSmem<BS> L(p.d_pad / p.CB);
-    static size_t configured = 0;
-    if (L.total > configured) {
-        cudaError_t e = cudaFuncSetAttribute(build_kernel<BS>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(build_kernel<BS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured = L.total;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(build_kernel<BS>), L.total, true); e != cudaSuccess)
+        return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.q * p.CB, 1, 1);
     cfg.blockDim = dim3(kThreads, 1, 1);

@@ -372,14 +372,8 @@ __global__ void __launch_bounds__(NTH, 2) build2_kernel(Plan p, const float* __r
 template <int BS>
 cudaError_t launch_build2_t(const Plan& p, const float* V, int64_t ldv, ErrWord* err, cudaStream_t st) {
     const B2Smem<BS> L(p.d_pad / p.CB);
-    static size_t configured = 0;
-    if (L.total > configured) {
-        cudaError_t e = cudaFuncSetAttribute(build2_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(build2_kernel<BS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        configured = L.total;
-    }
+    if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(build2_kernel<BS>), L.total, true); e != cudaSuccess)
+        return e;
     cudaLaunchConfig_t cfg = {};
     const int nrange = (p.blk_hi < 0 ? p.q : p.blk_hi) - p.blk_lo;
     const int nclu = p.nbuild > 0 ? (p.nbuild < p.q ? p.nbuild : p.q) : nrange;
