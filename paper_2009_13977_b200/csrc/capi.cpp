@@ -1178,12 +1178,38 @@ bool is_pinned(const void* p) {
     return at.type == cudaMemoryTypeHost;
 }
 
+// Device view of a pinned (UVA-mapped) host buffer, nullptr if it has none.
+const float* mapped(const float* p) {
+    cudaPointerAttributes at;
+    if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return static_cast<const float*>(at.devicePointer);
+}
+
 // The host-buffer step, enqueued on c->stream: H2D of V, X, G, the one-call
-// step on device copies, D2H of Y, dX, dV.  bufs: v, x, g, y, dx, dv.
+// step on device copies, D2H of Y, dX, dV.  bufs: v, x, g, y, dx, dv.  Small
+// activations (the chain path's batches) are not copied when the caller's
+// buffers are pinned: the sweeps read X, G and write Y, dX through PCIe
+// directly (one pass each), which saves four copies per call.
 fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, int d, int n, const float* X,
                                const float* G, int m, int block_width, float* Y, float* dX, float* dV) {
     float *v = bufs[0], *x = bufs[1], *g = bufs[2], *y = bufs[3], *dx = bufs[4], *dv = bufs[5];
     const size_t nv = (size_t)d * n, nx = (size_t)d * m;
+    const char* zc = getenv("FASTH_HOST_ZEROCOPY");
+    if ((!zc || atoi(zc) != 0) && nx * 4 <= (1u << 20) && !use_large_batch(d, n, m)) {
+        const float *xm = mapped(X), *gm = mapped(G), *ym = mapped(Y), *dxm = mapped(dX);
+        if (xm && gm && ym && dxm) {
+            x = const_cast<float*>(xm), g = const_cast<float*>(gm);
+            y = const_cast<float*>(ym), dx = const_cast<float*>(dxm);
+            if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
+            TRY(fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d, n ? dv : nullptr,
+                                       d));
+            if (nv) CU(cudaMemcpyAsync(dV, dv, nv * 4, cudaMemcpyDeviceToHost, c->stream));
+            return FASTH_OK;
+        }
+    }
     if (nx) CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
     if (nx) CU(cudaMemcpyAsync(g, G, nx * 4, cudaMemcpyHostToDevice, c->stream));
     // (Overlapping V's upload with the builds and the sweep was tried: a
