@@ -933,13 +933,15 @@ fasth_status fasth_ctx_trim(fasth_ctx c) {
 }
 
 // Large-batch path (lb.h): the chain re-blocked into 512-wide WY blocks, every
-// step a tcgen05 GEMM.  Chosen when the batch is wide enough for the GEMMs to
-// fill the GPU (m >= 1024 and d >= 512 here; FASTH_LB=0/1 forces the choice)
-// and the shapes meet its alignment (n a multiple of 128, d and m of 4).
+// step a tcgen05 GEMM (split K when the batch is small).  Chosen where it
+// measured faster than the chain kernels (scripts/small_batch_probe.py, one
+// B200): m >= 1024 at d >= 512, m >= 128 at d >= 1024 (2.3-5x over the panel
+// sweep at d >= 2048), m >= 64 at d >= 4096; FASTH_LB=0/1 forces the choice.
+// Shapes must meet its alignment (n a multiple of 128, d and m of 4).
 bool use_large_batch(int d, int n, int m) {
     if (!fasthb::lb::supported(d, n, m)) return false;
     if (const char* e = getenv("FASTH_LB")) return atoi(e) != 0;
-    return m >= 1024 && d >= 512;
+    return (m >= 1024 && d >= 512) || (m >= 128 && d >= 1024) || (m >= 64 && d >= 4096);
 }
 
 bool vec_ok(const float* p, int64_t ld) { return !p || ((ld % 4) == 0 && !(reinterpret_cast<uintptr_t>(p) & 15)); }

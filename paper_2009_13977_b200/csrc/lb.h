@@ -76,6 +76,11 @@ struct Gemm {
     float *t_hi = nullptr, *t_lo = nullptr;  // transposed split copy D^T (N x M)
     int64_t ldt = 0;
     float* partial = nullptr;                // [nz][ksplit][M][N]
+    // optional: products with few tiles (small batch) split K into this
+    // scratch ([nz][ks][M][N]) and finish in a reduction epilogue kernel
+    float* split_scratch = nullptr;
+    int64_t split_scratch_floats = 0;
+    int launched = 0;                        // out: kernels gemm() launched (1, or 2 with the reduction)
     int debug_swap = 0;                      // test hook: MN-major LBO/SBO swap
 };
 

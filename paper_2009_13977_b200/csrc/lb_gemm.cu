@@ -548,17 +548,97 @@ bool make_map(CUtensorMap* m, const float* ptr, int64_t rows, int64_t cols, int6
 
 }  // namespace
 
+namespace {
+bool use_pair(int M) {
+    // CTA pairs (256-row tiles) from M = 512 on (B-row products run 64 pairs)
+    const int pair_env = getenv("FASTH_LB_PAIR") ? atoi(getenv("FASTH_LB_PAIR")) : -1;
+    const int pair_min = getenv("FASTH_LB_PAIR_MIN") ? atoi(getenv("FASTH_LB_PAIR_MIN")) : 512;
+    return pair_env >= 0 ? (pair_env != 0 && M > BM) : M >= pair_min;
+}
+
+// Split-K reduction with the full epilogue: D = sum_s P[z][s] (+ beta C), written
+// fp32 and/or split (one float4 per thread).
+__global__ void reduce_epilogue_kernel(const float4* __restrict__ part, int ks, int nz, int M, int N, int64_t z_out,
+                                       float beta, const float* __restrict__ c_hi, const float* __restrict__ c_lo,
+                                       int c_single, int64_t ldc, float* __restrict__ d_f32, int64_t ldd,
+                                       float* __restrict__ d_hi, float* __restrict__ d_lo, int64_t lds,
+                                       int split_trunc) {
+    const int n4 = N / 4;
+    const int64_t per = (int64_t)M * n4, total = per * nz;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = e / per, w = e % per;
+        const int r = (int)(w / n4), c = (int)(w % n4) * 4;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < ks; ++k) {
+            const float4 v = __ldcs(part + (z * ks + k) * per + w);
+            a.x += v.x, a.y += v.y, a.z += v.z, a.w += v.w;
+        }
+        const int64_t gr = z * z_out + r;
+        if (c_hi) {
+            float4 cv = *reinterpret_cast<const float4*>(c_hi + gr * ldc + c);
+            if (!c_single) {
+                const float4 cl = *reinterpret_cast<const float4*>(c_lo + gr * ldc + c);
+                cv.x += cl.x, cv.y += cl.y, cv.z += cl.z, cv.w += cl.w;
+            }
+            a.x += beta * cv.x, a.y += beta * cv.y, a.z += beta * cv.z, a.w += beta * cv.w;
+        }
+        if (d_f32) *reinterpret_cast<float4*>(d_f32 + gr * ldd + c) = a;
+        if (d_hi) {
+            const float4 h = split_trunc ? make_float4(tr_hi(a.x), tr_hi(a.y), tr_hi(a.z), tr_hi(a.w))
+                                         : make_float4(rn_hi(a.x), rn_hi(a.y), rn_hi(a.z), rn_hi(a.w));
+            *reinterpret_cast<float4*>(d_hi + gr * lds + c) = split_trunc ? a : h;
+            *reinterpret_cast<float4*>(d_lo + gr * lds + c) = make_float4(a.x - h.x, a.y - h.y, a.z - h.z, a.w - h.w);
+        }
+    }
+}
+}  // namespace
+
+cudaError_t gemm_launch(Gemm& g, cudaStream_t s, int num_sms);
+
+// Front end: a product with too few output tiles to fill the GPU (small batch)
+// runs split K into g.split_scratch and reduces with the full epilogue.
 cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
+    if (g.split_scratch && !g.partial && !g.t_hi) {
+        const bool pair = use_pair(g.M);
+        const int tile_m = pair ? 2 * BM : BM;
+        const int nz = std::max(1, g.nz);
+        const int tiles = nz * ((g.M + tile_m - 1) / tile_m) * ((g.N + BN - 1) / BN);
+        const int units = pair ? std::max(num_sms / 2, 1) : std::max(num_sms, 1);
+        int tot_kb = 0;
+        for (int sg = 0; sg < g.nseg; ++sg) tot_kb += (g.seg[sg].K + BK - 1) / BK;
+        if (tiles * 2 <= units && tot_kb >= 4) {
+            const int ks = std::max(2, std::min({units / tiles, tot_kb / 2, 16}));
+            if ((int64_t)ks * nz * g.M * g.N <= g.split_scratch_floats) {
+                Gemm q = g;
+                q.partial = g.split_scratch;
+                q.ksplit = ks;
+                q.c_hi = q.c_lo = nullptr;
+                q.d_f32 = q.d_hi = q.d_lo = nullptr;
+                cudaError_t e = gemm_launch(q, s, num_sms);
+                if (e != cudaSuccess) return e;
+                const int64_t work = (int64_t)nz * g.M * (g.N / 4);
+                const int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms * 8);
+                g.launched = 2;
+                reduce_epilogue_kernel<<<grid, 256, 0, s>>>(reinterpret_cast<const float4*>(g.split_scratch), q.ksplit,
+                                                            nz, g.M, g.N, g.z_out, g.beta, g.c_hi, g.c_lo,
+                                                            g.c_single, g.ldc, g.d_f32, g.ldd, g.d_hi, g.d_lo,
+                                                            g.lds, g.split_trunc);
+                return cudaGetLastError();
+            }
+        }
+    }
+    g.launched = 1;
+    return gemm_launch(g, s, num_sms);
+}
+
+cudaError_t gemm_launch(Gemm& g, cudaStream_t s, int num_sms) {
     if (g.M <= 0 || g.N <= 0 || g.nseg < 1 || g.nseg > 3 || g.N % 4) return cudaErrorInvalidValue;
     if (g.t_hi && g.c_hi) return cudaErrorInvalidValue;  // the transposed copy carries no C term
     Params p{};
     p.M = g.M;
     p.N = g.N;
     p.nseg = g.nseg;
-    // CTA pairs (256-row tiles) from M = 512 on (B-row products run 64 pairs)
-    const int pair_env = getenv("FASTH_LB_PAIR") ? atoi(getenv("FASTH_LB_PAIR")) : -1;
-    const int pair_min = getenv("FASTH_LB_PAIR_MIN") ? atoi(getenv("FASTH_LB_PAIR_MIN")) : 512;
-    const bool pair = pair_env >= 0 ? (pair_env != 0 && g.M > BM) : g.M >= pair_min;
+    const bool pair = use_pair(g.M);
     int tot_kb = 0;
     for (int sg = 0; sg < g.nseg; ++sg) {
         const Segment& S = g.seg[sg];

@@ -247,7 +247,13 @@ int pick_block(int n) {
 }
 
 bool supported(int d, int n, int m) {
-    return d >= 128 && d % 4 == 0 && n >= 128 && pick_block(n) > 0 && m >= 128 && m % 4 == 0;
+    return d >= 128 && d % 4 == 0 && n >= 128 && pick_block(n) > 0 && m >= 16 && m % 4 == 0;
+}
+
+// split-K scratch for the chain products when the batch is too small for
+// their output tiles to fill the GPU: 16 partial m x max(d, n) slabs
+int64_t small_batch_scratch(int d, int n, int m) {
+    return m < 1024 ? (int64_t)16 * m * std::max(d, n) : 0;
 }
 
 size_t workspace_floats(int d, int n, int m, bool want_dv) {
@@ -267,6 +273,7 @@ size_t workspace_floats(int d, int n, int m, bool want_dv) {
     (void)want_dv;                  // the forward carves the backward's buffers too
     f += 16 * bb + 3 * bb;          // Q partials, Q, S split
     f += 8 * (size_t)B * d;         // dV partials
+    f += (size_t)small_batch_scratch(d, n, m);
     return f + 256 * 32;            // alignment slack
 }
 
@@ -289,6 +296,8 @@ struct Bufs {
     float *Sth[kMaxStages], *Stl[kMaxStages];
     float *ZbTh2[2], *ZbTl2[2], *ZfAh, *ZfAl, *Gh[2], *Gl[2];  // ZfA: m x n, block j = columns jB..
     float *Qp, *Qs, *Sh, *Sl, *dVp;
+    float* ksc;  // split-K scratch of the small-batch chain products (m < 1024)
+    int64_t ksc_n;
 };
 constexpr int ksG = 4, ksQ = 16, ksV = 4;  // split-K counts (128 CTAs each: one tile per CTA)
 
@@ -319,6 +328,8 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
     b.Sh = c.take(bb);
     b.Sl = c.take(bb);
     b.dVp = c.take((size_t)(ksV + 1) * B * d);
+    b.ksc_n = small_batch_scratch(d, n, m);
+    b.ksc = b.ksc_n ? c.take((size_t)b.ksc_n) : nullptr;
     return true;
 }
 
@@ -332,7 +343,7 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
         if (tm) tm->begin(st);        \
         LBTRY(gemm(g, st, num_sms));  \
         if (tm) tm->end(st, name);    \
-        ++nl;                         \
+        nl += g.launched;             \
     } while (0)
 #define LB_ALIASES                                                                                           \
     const int B = b.B, nb = b.nb;                                                                            \
@@ -430,6 +441,8 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
     for (int j = nb - 1; j >= 0; --j) {
         {
             Gemm g;  // ZfT = A WfR_j^T (m x B), Zf_j = its transpose (B x m)
+            g.split_scratch = b.ksc;
+            g.split_scratch_floats = b.ksc_n;
             g.M = m;
             g.N = B;
             g.seg[0].A = Operand{Sth[j + 1], Stl[j + 1], m, d, d};
@@ -443,6 +456,8 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         }
         {
             Gemm g;  // A_j = A_{j+1} - 2 ZfT VT_j^T
+            g.split_scratch = b.ksc;
+            g.split_scratch_floats = b.ksc_n;
             g.M = m;
             g.N = d;
             g.seg[0].A = Operand{ZfAh, ZfAl, m, n, n};
@@ -496,6 +511,8 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
         float *ZbTh = b.ZbTh2[j & 1], *ZbTl = b.ZbTl2[j & 1];
         {
             Gemm g;  // ZbT = G WbR_j^T, Zb = transpose
+            g.split_scratch = b.ksc;
+            g.split_scratch_floats = b.ksc_n;
             g.M = m;
             g.N = B;
             g.seg[0].A = Operand{Gh[cur], Gl[cur], m, d, d};
@@ -563,6 +580,8 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             // block j-1's dV read the G buffer this update overwrites
             if (two && j > 0) LBTRY(cudaStreamWaitEvent(s, st->ev[4 + ((j - 1) & 1)], 0));
             Gemm g;  // G <- G - 2 ZbT VT_j^T
+            g.split_scratch = b.ksc;
+            g.split_scratch_floats = b.ksc_n;
             g.M = m;
             g.N = d;
             g.seg[0].A = Operand{ZbTh, ZbTl, m, B, B};
