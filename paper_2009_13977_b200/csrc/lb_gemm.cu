@@ -607,8 +607,9 @@ cudaError_t gemm(Gemm& g, cudaStream_t s, int num_sms) {
         int tot_kb = 0;
         for (int sg = 0; sg < g.nseg; ++sg) tot_kb += (g.seg[sg].K + BK - 1) / BK;
         if (tiles * 2 <= units && tot_kb >= 4) {
-            const int ks = std::max(2, std::min({units / tiles, tot_kb / 2, 16}));
-            if ((int64_t)ks * nz * g.M * g.N <= g.split_scratch_floats) {
+            const int64_t fit = g.split_scratch_floats / ((int64_t)nz * g.M * g.N);
+            const int ks = (int)std::min<int64_t>({(int64_t)units / tiles, (int64_t)tot_kb / 2, 64, fit});
+            if (ks >= 2) {
                 Gemm q = g;
                 q.partial = g.split_scratch;
                 q.ksplit = ks;

@@ -251,9 +251,10 @@ bool supported(int d, int n, int m) {
 }
 
 // split-K scratch for the chain products when the batch is too small for
-// their output tiles to fill the GPU: 16 partial m x max(d, n) slabs
+// their output tiles to fill the GPU: up to 64 partial m x max(d, n) slabs,
+// capped at 128 MB
 int64_t small_batch_scratch(int d, int n, int m) {
-    return m < 1024 ? (int64_t)16 * m * std::max(d, n) : 0;
+    return m < 1024 ? std::min<int64_t>((int64_t)64 * m * std::max(d, n), (int64_t)32 << 20) : 0;
 }
 
 size_t workspace_floats(int d, int n, int m, bool want_dv) {
