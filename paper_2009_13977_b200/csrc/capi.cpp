@@ -138,6 +138,16 @@ struct fasth_ctx_s {
         }
         return &lb_st;
     }
+    // the SVD layer's independent leg work (U-leg build during the V leg, the
+    // U-leg gradient kernel during the V-leg backward) on the same side stream
+    const fasthb::lb::Streams* svd_streams() {
+        if (const char* e = getenv("FASTH_SVD_STREAMS"))
+            if (atoi(e) == 0) return nullptr;
+        return lb_streams();
+    }
+    // set around a launch that follows a cross-stream event wait: it must not
+    // use programmatic dependent launch (see run_forward)
+    bool after_stream_wait = false;
     bool capturing = false;
     std::vector<void*> graph_held;
     cudaGraphExec_t host_exec = nullptr;
@@ -569,7 +579,11 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     if (t->v2nstg) {
         SweepV2Args a = v2_args(t);
         a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, record);
-        a.pdl = !getenv("FASTH_NO_PDL");  // the builder was the previous launch; X predates it
+        // the builder was the previous launch; X predates it.  Not after a
+        // cross-stream event wait: a programmatic launch does not reliably
+        // honour a cudaStreamWaitEvent placed before it (measured)
+        a.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;
+        c->after_stream_wait = false;
         return launch_traced_sweep2(c, a, "sweep(forward)");
     }
     SweepArgs a{};
@@ -600,7 +614,7 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
 fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, int g_valid,
                           const float* g_scale, float* dX, int64_t lddx, float* dV,
-                          int64_t lddv) {
+                          int64_t lddv, const fasthb::lb::Streams* dv_side = nullptr) {
     const Plan& p = t->plan;
     if (!t->tapeA || !t->zf)
         return fail(FASTH_ERR_INVALID, "fasth_backward: tape was recorded without activations");
@@ -645,7 +659,18 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
-    return run_dv(c, t, dV, lddv);
+    if (!dv_side) return run_dv(c, t, dV, lddv);
+    // gradient kernel on the side stream (off the dX critical path); the
+    // caller joins on dv_side->ev[11]
+    CU(cudaEventRecord(dv_side->ev[10], c->stream));
+    CU(cudaStreamWaitEvent(dv_side->aux, dv_side->ev[10], 0));
+    cudaStream_t main_stream = c->stream;
+    c->stream = dv_side->aux;
+    c->after_stream_wait = true;  // consumed by the gradient kernel's launch
+    s = run_dv(c, t, dV, lddv);
+    c->stream = main_stream;
+    CU(cudaEventRecord(dv_side->ev[11], dv_side->aux));
+    return s;
 }
 
 fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe) {
@@ -657,7 +682,8 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
         v.dvcnt = c->counters + 2 * kMaxPipeQ;
         v.done_target = (unsigned)(2 * t->ngroups * t->C);
     }
-    v.pdl = !getenv("FASTH_NO_PDL");  // the sweep was the previous launch
+    v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
+    c->after_stream_wait = false;
     v.Vbl = p.Vbl;
     v.d = p.d;
     v.d_pad = p.d_pad;
@@ -706,7 +732,8 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
     a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, want_dv);
     a.dir[1] = v2_backward_dir(t, G, ldg, p.d, nullptr, dx, lddx, want_dv);
     const bool pipe = t->pipelined && want_dv;
-    a.pdl = !getenv("FASTH_NO_PDL");  // the builder was the previous launch
+    a.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the builder was the previous launch
+    c->after_stream_wait = false;
     if (pipe) {
         a.ready = c->counters;
         a.done = c->counters + kMaxPipeQ;
@@ -1012,6 +1039,7 @@ fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, in
             },
             "large_batch(fwd+bwd)");
     c->launches += nl - 1;
+    c->after_stream_wait = true;  // the step joined its side streams
     if (s == FASTH_OK) s = y.close(d, m);
     if (s == FASTH_OK) s = dx.close(d, m);
     c->release(ws);  // pool reuse is stream ordered
@@ -1044,6 +1072,7 @@ fasth_status lb_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, 
             },
             "large_batch(fwd)");
     c->launches += nl - 1;
+    c->after_stream_wait = true;  // the step joined its side streams
     if (s == FASTH_OK) s = y.close(d, m);
     if (s == FASTH_OK) s = c->finish();
     if (s == FASTH_OK && tape)
@@ -1114,6 +1143,7 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
             },
             "large_batch(bwd)"));
         c->launches += nl - 1;
+        c->after_stream_wait = true;  // the step joined its side streams
         TRY(dx.close(d, m));
         return c->finish();
     }
@@ -1318,6 +1348,19 @@ fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const floa
     do {
         s = c->alloc_n((size_t)p->in_dim * std::max(m, 1), &st->T1);
         if (s) break;
+        // The U leg's WY build does not depend on the V leg: it runs on the side
+        // stream (fork after everything enqueued so far, join before the U sweep)
+        const fasthb::lb::Streams* side = (p->nu > 0 && p->nv > 0 && m > 0) ? c->svd_streams() : nullptr;
+        if (side) {
+            CU(cudaEventRecord(side->ev[8], c->stream));
+            CU(cudaStreamWaitEvent(side->aux, side->ev[8], 0));
+            cudaStream_t main_stream = c->stream;
+            c->stream = side->aux;
+            s = new_tape(c, p->U, p->ldu, p->out_dim, p->nu, m, block_width, 0, 0, &st->u);
+            c->stream = main_stream;
+            if (s) break;
+            CU(cudaEventRecord(side->ev[9], side->aux));
+        }
         // V^T leg: the reversed V chain (svd_layer.hpp:113)
         if (p->nv > 0 && m > 0) {
             s = new_tape(c, p->V, p->ldv, p->in_dim, p->nv, m, block_width, 1, 1, &st->v);
@@ -1329,7 +1372,12 @@ fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const floa
         if (s) break;
         // U leg on T2 = Sigma T1 (svd_layer.hpp:114-115), Sigma fused into the load
         if (p->nu > 0 && m > 0) {
-            s = new_tape(c, p->U, p->ldu, p->out_dim, p->nu, m, block_width, 0, 0, &st->u);
+            if (side) {
+                CU(cudaStreamWaitEvent(c->stream, side->ev[9], 0));
+                c->after_stream_wait = true;
+            } else {
+                s = new_tape(c, p->U, p->ldu, p->out_dim, p->nu, m, block_width, 0, 0, &st->u);
+            }
             if (s) break;
             st->u->scale = p->sigma;
             st->u->n_valid = st->k;
@@ -1364,6 +1412,7 @@ fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd
     float* dT2 = nullptr;
     TRY(c->alloc_n((size_t)p->out_dim * std::max(m, 1), &dT2));
     fasth_status s = FASTH_OK;
+    const fasthb::lb::Streams* side = nullptr;
     do {
         if (m == 0) {
             if (dU && p->nu)
@@ -1373,9 +1422,11 @@ fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd
             if (dsigma && k) CU(cudaMemsetAsync(dsigma, 0, k * 4, c->stream));
             break;
         }
-        // U leg (svd_layer.hpp:124)
+        // U leg (svd_layer.hpp:124); its gradient kernel (dU) runs on the side
+        // stream while dSigma and the V leg continue (joined below)
         if (st->u) {
-            s = run_backward(c, st->u, G, ldg, p->out_dim, nullptr, dT2, p->out_dim, dU, lddu);
+            side = (dU && st->v) ? c->svd_streams() : nullptr;
+            s = run_backward(c, st->u, G, ldg, p->out_dim, nullptr, dT2, p->out_dim, dU, lddu, side);
         } else {
             s = copy_cols(c, G, ldg, dT2, p->out_dim, p->out_dim, m);
         }
@@ -1389,6 +1440,10 @@ fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd
         // V^T leg on dT1 = Sigma dT2 (svd_layer.hpp:139-147), Sigma fused into the load
         if (st->v) {
             s = run_backward(c, st->v, dT2, p->out_dim, k, p->sigma, dX, lddx, dV, lddv);
+            if (side && s == FASTH_OK) {
+                CU(cudaStreamWaitEvent(c->stream, side->ev[11], 0));  // dU done
+                c->after_stream_wait = true;
+            }
         } else if (dX) {
             s = c->timed([&] { return launch_scale_rows(dT2, p->out_dim, k, p->sigma, p->in_dim, m, dX, lddx,
                                               0, c->stream); }, "scale_rows");

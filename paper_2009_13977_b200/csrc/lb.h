@@ -101,7 +101,7 @@ struct Timer {
 // block j runs), with reusable fork/join events.  nullptr: one stream.
 struct Streams {
     cudaStream_t aux = nullptr;
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[12] = {};  // 0-7: large-batch step, 8-11: SVD layer legs (capi.cpp)
 };
 
 // The whole large-batch step (lb_run.cu).
