@@ -173,6 +173,51 @@ def run_reference_impl(args):
     print(json.dumps(line))
 
 
+def layer_line(local, steps=50, warmup=5):
+    """BASELINE configs[1] read as the layer: the SVD-reparameterised layer
+    W = U Sigma V^T at d = 784, b = 32, batch 32 (svd_layer.hpp:106-154):
+    svd_forward + svd_backward per step (two FastH chains each way, Sigma,
+    dSigma), device time with CUDA events, inputs resident.  Synthetic:
+    normalised N(0,1) vectors, sigma ~ U(0.5, 2) (bench.hpp:129-131)."""
+    import torch
+
+    from paper_2009_13977_b200 import fasth as fb
+    d, b, m = D, B, M
+    g = torch.Generator(device="cuda").manual_seed(SEED)
+    U = torch.randn(d, d, device="cuda", generator=g)
+    V = torch.randn(d, d, device="cuda", generator=g)
+    U /= U.norm(dim=1, keepdim=True)
+    V /= V.norm(dim=1, keepdim=True)
+    s = torch.rand(d, device="cuda", generator=g) * 1.5 + 0.5
+    X = torch.randn(m, d, device="cuda", generator=g).t()
+    G = torch.randn(m, d, device="cuda", generator=g).t()
+    p = fb.SvdParam(d, d, U, V, s)
+    ctx = fb.Context(local, deferred=True)
+
+    def step():
+        _, tape = fb.svd_forward(p, X, b, ctx=ctx)
+        return fb.svd_backward(p, tape, G)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    n0 = ctx.launch_count
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ctx.check()
+    us = e0.elapsed_time(e1) * 1e3 / steps
+    return {"workload": "BASELINE configs[1] as the layer: svd_forward + svd_backward, W = U Sigma V^T",
+            "d": d, "block_width": b, "batch": m, "us_per_step": us,
+            "tflops": 2 * flops_alg(d, d, m, b) / (us * 1e-6) / 1e12,
+            "gpu_launches_per_step": (ctx.launch_count - n0) / steps, "steps": steps, "warmup": warmup,
+            "timing": "eager, CUDA events on the context stream, inputs resident",
+            "data": "synthetic: normalised N(0,1) vectors, sigma ~ U(0.5, 2)"}
+
+
 def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
     """BASELINE.json configs[4]: d = 2048 FastH fwd+bwd at 8192 columns per GPU
     (weak: a 8192*world batch sharded by columns), dV all-reduced over NCCL
@@ -525,6 +570,18 @@ def main():
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
+    if world == 1:
+        try:
+            line["config2_layer"] = layer_line(local)
+            if cpu is not None and cpu.get("value"):
+                from oracle.oracle import Ref
+                mean, std, _ = Ref().run_bench("layer", "fasth", D, M, B, 20, SEED, 0)
+                line["config2_layer"]["cpu_reference_us"] = mean * 1e6
+                line["config2_layer"]["cpu_reference_sample"] = (
+                    f"run_bench op=layer d={D} m={M} k={B} algo=fasth, 20 reps (std {std * 1e6:.0f} us), "
+                    "all host threads")
+        except Exception as e:  # noqa: BLE001
+            line["config2_layer"] = {"unavailable": str(e)[:200]}
     if not args.no_config5:
         try:
             line["config5"] = large_batch_line(world, rank, local, peak_3xtf32)
