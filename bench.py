@@ -194,9 +194,8 @@ def layer_line(local, steps=50, warmup=5):
     p = fb.SvdParam(d, d, U, V, s)
     ctx = fb.Context(local, deferred=True)
 
-    def step():
-        _, tape = fb.svd_forward(p, X, b, ctx=ctx)
-        return fb.svd_backward(p, tape, G)
+    def step():  # G drawn up front, as the reference's layer benchmark (bench.hpp:166-209)
+        return fb.svd_forward_backward(p, X, G, b, ctx=ctx)
 
     for _ in range(warmup):
         step()
@@ -210,7 +209,8 @@ def layer_line(local, steps=50, warmup=5):
     torch.cuda.synchronize()
     ctx.check()
     us = e0.elapsed_time(e1) * 1e3 / steps
-    return {"workload": "BASELINE configs[1] as the layer: svd_forward + svd_backward, W = U Sigma V^T",
+    return {"workload": "BASELINE configs[1] as the layer: svd_forward + svd_backward as "
+                        "fasth_svd_forward_backward (paired sweeps), W = U Sigma V^T",
             "d": d, "block_width": b, "batch": m, "us_per_step": us,
             "tflops": 2 * flops_alg(d, d, m, b) / (us * 1e-6) / 1e12,
             "gpu_launches_per_step": (ctx.launch_count - n0) / steps, "steps": steps, "warmup": warmup,

@@ -155,6 +155,14 @@ fasth_status fasth_svd_backward(fasth_ctx ctx, const fasth_svd_param* p, fasth_s
                                 const float* G, int64_t ldg, float* dX, int64_t lddx, float* dU,
                                 int64_t lddu, float* dV, int64_t lddv, float* dsigma);
 fasth_status fasth_svd_tape_destroy(fasth_svd_tape tape);
+/* svd_forward + svd_backward in one call for a caller holding grad_output up
+ * front (the reference benchmark's layer step, bench.hpp:166-209): the four
+ * chain sweeps run as two paired launches.  Same outputs as the two calls;
+ * square layers (out_dim == in_dim, nu == nv) take the paired path. */
+fasth_status fasth_svd_forward_backward(fasth_ctx ctx, const fasth_svd_param* p, const float* X,
+                                        int64_t ldx, const float* G, int64_t ldg, int m, int block_width,
+                                        float* Y, int64_t ldy, float* dX, int64_t lddx, float* dU,
+                                        int64_t lddu, float* dV, int64_t lddv, float* dsigma);
 
 /* svd_step (svd_layer.hpp:158) fused with clamp_sigma (svd_layer.hpp:196)
  * when clamp_eps >= 0: v <- v - eta dv, sigma <- sigma - eta dsigma.

@@ -1455,6 +1455,136 @@ fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd
     return s;
 }
 
+// svd_forward + svd_backward as one call when grad_output is known up front
+// (the reference benchmark's layer step, bench.hpp:166-209).  The U leg's
+// backward sweep needs only G and the V leg's forward sweep only X, so the
+// four sweeps pair up into two launches on disjoint clusters:
+//   launch 1: V-leg forward (X -> T1)           | U-leg backward (G -> dT2)
+//   launch 2: U-leg forward (Sigma T1 -> Y)     | V-leg backward (Sigma dT2 -> dX)
+// then dSigma and both gradient kernels.  Square layers whose legs share a
+// sweep geometry; anything else runs the two calls.
+fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx,
+                                        const float* G, int64_t ldg, int m, int block_width, float* Y,
+                                        int64_t ldy, float* dX, int64_t lddx, float* dU, int64_t lddu,
+                                        float* dV, int64_t lddv, float* dsigma) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    TRY(check_param("svd_forward_backward", p));
+    TRY(check_mat("svd_forward: X", X, ldx, p->in_dim, m));
+    TRY(check_mat("svd_forward: Y", Y, ldy, p->out_dim, m));
+    TRY(check_mat("svd_backward: G", G, ldg, p->out_dim, m));
+    if (dX) TRY(check_mat("svd_backward: dX", dX, lddx, p->in_dim, m));
+    if (dU) TRY(check_mat("svd_backward: dU", dU, lddu, p->out_dim, p->nu));
+    if (dV) TRY(check_mat("svd_backward: dV", dV, lddv, p->in_dim, p->nv));
+    const bool square = p->out_dim == p->in_dim && p->nu == p->nv && p->nu > 0 && m > 0;
+    auto two_calls = [&]() -> fasth_status {
+        fasth_svd_tape st = nullptr;
+        TRY(fasth_svd_forward(c, p, X, ldx, m, block_width, Y, ldy, &st));
+        fasth_status s = fasth_svd_backward(c, p, st, G, ldg, dX, lddx, dU, lddu, dV, lddv, dsigma);
+        fasth_svd_tape_destroy(st);
+        return s;
+    };
+    if (!square || getenv("FASTH_SVD_FUSED") && atoi(getenv("FASTH_SVD_FUSED")) == 0) return two_calls();
+    const int d = p->in_dim, k = std::min(p->out_dim, p->in_dim);
+    fasth_tape tv = nullptr, tu = nullptr;
+    float *T1 = nullptr, *dT2 = nullptr;
+    fasth_status s = FASTH_OK;
+    const fasthb::lb::Streams* side = c->svd_streams();
+    do {
+        // builds: U on the side stream, V on the main stream
+        if (side) {
+            CU(cudaEventRecord(side->ev[8], c->stream));
+            CU(cudaStreamWaitEvent(side->aux, side->ev[8], 0));
+            cudaStream_t main_stream = c->stream;
+            c->stream = side->aux;
+            s = new_tape(c, p->U, p->ldu, d, p->nu, m, block_width, 0, 0, &tu);
+            c->stream = main_stream;
+            if (s) break;
+            CU(cudaEventRecord(side->ev[9], side->aux));
+        } else {
+            s = new_tape(c, p->U, p->ldu, d, p->nu, m, block_width, 0, 0, &tu);
+            if (s) break;
+        }
+        s = new_tape(c, p->V, p->ldv, d, p->nv, m, block_width, 1, 1, &tv);
+        if (s) break;
+        if (side) {
+            CU(cudaStreamWaitEvent(c->stream, side->ev[9], 0));
+            c->after_stream_wait = true;
+        }
+        const bool same = tv->v2nstg && tu->v2nstg && tv->v2nstg == tu->v2nstg && tv->C == tu->C &&
+                          tv->ngroups == tu->ngroups && tv->WC == tu->WC && tv->plan.d_pad == tu->plan.d_pad &&
+                          tv->plan.q == tu->plan.q && tv->plan.BS == tu->plan.BS;
+        if (!same) {
+            free_tape(tu);
+            free_tape(tv);
+            tu = tv = nullptr;
+            return two_calls();
+        }
+        tu->scale = p->sigma;
+        tu->n_valid = k;
+        s = c->alloc_n((size_t)d * m, &T1);
+        if (s) break;
+        s = c->alloc_n((size_t)d * m, &dT2);
+        if (s) break;
+        const bool want_dv = dV != nullptr, want_du = dU != nullptr;
+        for (fasth_tape t : {tv, tu}) {
+            const bool g = t == tv ? want_dv : want_du;
+            const Plan& pl = t->plan;
+            if (!t->tapeA) s = c->alloc_n((size_t)pl.q * t->ngroups * pl.d_pad * t->WC, &t->tapeA);
+            if (!s && !t->zf) s = c->alloc_n((size_t)pl.q * pl.BS * t->m, &t->zf);
+            if (!s && g && !t->tapeG) s = c->alloc_n((size_t)pl.q * t->ngroups * pl.d_pad * t->WC, &t->tapeG);
+            if (!s && g && !t->zb) s = c->alloc_n((size_t)pl.q * pl.BS * t->m, &t->zb);
+            if (s) break;
+        }
+        if (s) break;
+        {  // launch 1: V forward | U backward
+            SweepV2Args a = v2_args(tv);
+            a.ndir = 2;
+            a.dir[0] = v2_forward_dir(tv, X, ldx, T1, d, want_dv);
+            a.dir[1] = v2_backward_dir(tu, G, ldg, d, nullptr, dT2, d, want_du);
+            a.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;
+            c->after_stream_wait = false;
+            s = launch_traced_sweep2(c, a, "sweep(svd 1)");
+            if (s) break;
+        }
+        {  // launch 2: U forward (Sigma T1) | V backward (Sigma dT2); reads launch 1's
+           // outputs from its first instruction: no programmatic early start
+            SweepV2Args a = v2_args(tu);
+            a.ndir = 2;
+            a.dir[0] = v2_forward_dir(tu, T1, d, Y, ldy, want_du);
+            float* dx = dX;
+            if (!dx) {
+                s = c->alloc_n((size_t)d * m, &dx);
+                if (s) break;
+            }
+            a.dir[1] = v2_backward_dir(tv, dT2, d, k, p->sigma, dx, dX ? lddx : d, want_dv);
+            a.pdl = 0;
+            s = launch_traced_sweep2(c, a, "sweep(svd 2)");
+            if (dx != dX) c->release(dx);
+            if (s) break;
+        }
+        if (dsigma) {
+            s = c->timed([&] { return launch_dsigma(dT2, d, T1, d, k, m, dsigma, c->stream); }, "dsigma");
+            if (s) break;
+        }
+        c->after_stream_wait = true;  // the gradient kernels read both launches' tapes
+        if (want_du) {
+            s = run_dv(c, tu, dU, lddu);
+            if (s) break;
+        }
+        if (want_dv) {
+            c->after_stream_wait = true;
+            s = run_dv(c, tv, dV, lddv);
+            if (s) break;
+        }
+    } while (0);
+    free_tape(tu);
+    free_tape(tv);
+    c->release(T1);
+    c->release(dT2);
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
 fasth_status fasth_svd_tape_destroy(fasth_svd_tape st) {
     if (!st) return FASTH_OK;
     free_tape(st->u);

@@ -405,6 +405,30 @@ def svd_backward(p: SvdParam, tape: SvdTape, G: torch.Tensor) -> SvdGradients:
     return SvdGradients(dU, dV, ds, dX)
 
 
+def svd_forward_backward(p: SvdParam, X: torch.Tensor, G: torch.Tensor, block_width: int, *,
+                         ctx: Context | None = None):
+    """svd_forward + svd_backward in one call (``fasth_svd_forward_backward``)
+    for a caller holding grad_output up front (bench.hpp:166-209's layer
+    step).  Returns (Y, SvdGradients)."""
+    X, ldx = _colmajor(X, "svd_forward: X")
+    G, ldg = _colmajor(G, "svd_backward: grad_output")
+    if X.shape[0] != p.in_dim or tuple(G.shape) != (p.out_dim, X.shape[1]):
+        raise DimensionError("svd_forward_backward: X / grad_output shape mismatch")
+    pc = p._c()
+    c = _ctx(ctx, X)
+    m = X.shape[1]
+    dev = X.device
+    Y = _new_out(p.out_dim, m, X)
+    dX = _new_out(p.in_dim, m, X)
+    dU = torch.empty((p.U.shape[0], p.out_dim), dtype=torch.float32, device=dev)
+    dV = torch.empty((p.V.shape[0], p.in_dim), dtype=torch.float32, device=dev)
+    ds = torch.empty(p.min_dim(), dtype=torch.float32, device=dev)
+    _check(c.lib.fasth_svd_forward_backward(c.h, C.byref(pc), _ptr(X), ldx, _ptr(G), ldg, m, int(block_width),
+                                            _ptr(Y), max(p.out_dim, 1), _ptr(dX), max(p.in_dim, 1), _ptr(dU),
+                                            max(p.out_dim, 1), _ptr(dV), max(p.in_dim, 1), _ptr(ds)))
+    return Y, SvdGradients(dU, dV, ds, dX)
+
+
 def svd_step(p: SvdParam, g: SvdGradients, eta: float, *, clamp_epsilon: float | None = None,
              inplace: bool = False, ctx: Context | None = None) -> SvdParam:
     """svd_layer.hpp:158 (optionally fused with clamp_sigma, :196)."""

@@ -380,6 +380,47 @@ def svd_param(fb, U, V, s, out_dim, in_dim):
 
 
 @pytest.mark.parametrize("case", ["svd8", "svd6x4", "svd4x6", "svd64"])
+def test_svd_forward_backward_fused_matches_two_calls(fb, golden, case):
+    """fasth_svd_forward_backward (paired sweeps) == svd_forward + svd_backward
+    bitwise, and within tolerance of the reference's golden outputs."""
+    import json
+    g = {k.split("/", 1)[1]: golden[k] for k in golden.files if k.startswith(case + "/")}
+    meta = json.load(open(os.path.join(HERE, "golden", "fasth_golden.json")))[case]
+    p = svd_param(fb, g["U"], g["V"], g["sigma"], meta["out"], meta["in"])
+    Y0, tape = fb.svd_forward(p, dev(g["X"]), meta["b"])
+    g0 = fb.svd_backward(p, tape, dev(g["G"]))
+    Y1, g1 = fb.svd_forward_backward(p, dev(g["X"]), dev(g["G"]), meta["b"])
+    import torch
+    torch.cuda.synchronize()
+    for a, b in ((Y1, Y0), (g1.grad_input, g0.grad_input), (g1.grad_U_vectors, g0.grad_U_vectors),
+                 (g1.grad_V_vectors, g0.grad_V_vectors), (g1.grad_sigma, g0.grad_sigma)):
+        assert torch.equal(a, b)
+    assert rel(Y1, g["Y"]) <= TOL and rel(g1.grad_input, g["dX"]) <= TOL and rel(g1.grad_U_vectors, g["dU"]) <= TOL
+
+
+def test_svd_forward_backward_fused_d784(fb):
+    """Config 2 as the layer (d = 784, b = 32, m = 32): paired path == two calls, bitwise."""
+    import torch
+    d, m = 784, 32
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    U = torch.randn(d, d, device="cuda", generator=gen)
+    V = torch.randn(d, d, device="cuda", generator=gen)
+    U /= U.norm(dim=1, keepdim=True)
+    V /= V.norm(dim=1, keepdim=True)
+    s = torch.rand(d, device="cuda", generator=gen) * 1.5 + 0.5
+    X = torch.randn(m, d, device="cuda", generator=gen).t()
+    G = torch.randn(m, d, device="cuda", generator=gen).t()
+    p = fb.SvdParam(d, d, U, V, s)
+    Y0, tape = fb.svd_forward(p, X, 32)
+    g0 = fb.svd_backward(p, tape, G)
+    Y1, g1 = fb.svd_forward_backward(p, X, G, 32)
+    torch.cuda.synchronize()
+    for a, b in ((Y1, Y0), (g1.grad_input, g0.grad_input), (g1.grad_U_vectors, g0.grad_U_vectors),
+                 (g1.grad_V_vectors, g0.grad_V_vectors), (g1.grad_sigma, g0.grad_sigma)):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("case", ["svd8", "svd6x4", "svd4x6", "svd64"])
 def test_svd_layer_matches_reference_golden(fb, golden, case):
     import json
     g = {k.split("/", 1)[1]: golden[k] for k in golden.files if k.startswith(case + "/")}
