@@ -109,8 +109,8 @@ def time_fasth(op: str, w, b: int, reps: int):
         def step():
             if op == "det":  # bench.hpp:162: log|det| of the parameter, then the layer
                 fb.log_abs_det(p, ctx=ctx)
-            y, tape = fb.svd_forward(p, X, b, ctx=ctx)
-            fb.svd_backward(p, tape, G)
+            # G drawn up front (bench.hpp:166-209): the paired-sweep layer call
+            y, _ = fb.svd_forward_backward(p, X, G, b, ctx=ctx)
             return y
     y = step()
     torch.cuda.synchronize()
