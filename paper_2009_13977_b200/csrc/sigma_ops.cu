@@ -35,8 +35,21 @@ __global__ void dsigma_kernel(const float* __restrict__ dT2, int64_t ld2,
                               float* dsigma) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
+    // 8 columns' loads in flight per round trip (the loop was latency bound);
+    // the batch sum stays in f64, in the same column order
     double acc = 0.0;
-    for (int l = 0; l < m; ++l) acc += (double)dT2[(int64_t)l * ld2 + i] * T1[(int64_t)l * ld1 + i];
+    int l = 0;
+    for (; l + 8 <= m; l += 8) {
+        float a[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a[u] = __ldg(dT2 + (int64_t)(l + u) * ld2 + i);
+            b[u] = __ldg(T1 + (int64_t)(l + u) * ld1 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += (double)a[u] * b[u];
+    }
+    for (; l < m; ++l) acc += (double)dT2[(int64_t)l * ld2 + i] * T1[(int64_t)l * ld1 + i];
     dsigma[i] = (float)acc;
 }
 
