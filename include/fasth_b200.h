@@ -53,6 +53,7 @@ typedef enum fasth_status {
 typedef struct fasth_ctx_s* fasth_ctx;
 typedef struct fasth_tape_s* fasth_tape;         /* TapeForward  (fasth.hpp:22-29)     */
 typedef struct fasth_svd_tape_s* fasth_svd_tape; /* SvdTape      (svd_layer.hpp:83-86) */
+typedef struct fasth_svd_plan_s* fasth_svd_plan; /* both legs' WY blocks, built ahead of a forward */
 
 enum { FASTH_CHECK_SYNC = 0, FASTH_CHECK_DEFERRED = 1 };
 
@@ -155,6 +156,18 @@ fasth_status fasth_svd_backward(fasth_ctx ctx, const fasth_svd_param* p, fasth_s
                                 const float* G, int64_t ldg, float* dX, int64_t lddx, float* dU,
                                 int64_t lddu, float* dV, int64_t lddv, float* dsigma);
 fasth_status fasth_svd_tape_destroy(fasth_svd_tape tape);
+/* Build a layer's WY blocks ahead of its forward (the blocks depend only on
+ * U and V): with on_side_stream != 0 the builds run on the context's side
+ * stream, so a training loop can prepare layer k+1 while layer k sweeps.  A
+ * plan is single use: fasth_svd_forward_planned consumes it (same m and
+ * block width); U and V must not change in between.  Destroy unused plans. */
+fasth_status fasth_svd_plan_create(fasth_ctx ctx, const fasth_svd_param* p, int m, int block_width,
+                                   int on_side_stream, fasth_svd_plan* out);
+fasth_status fasth_svd_plan_destroy(fasth_svd_plan plan);
+/* svd_forward (svd_layer.hpp:106) on a prepared plan (consumed). */
+fasth_status fasth_svd_forward_planned(fasth_ctx ctx, const fasth_svd_param* p, fasth_svd_plan plan,
+                                       const float* X, int64_t ldx, int m, int block_width, float* Y,
+                                       int64_t ldy, fasth_svd_tape* tape);
 /* svd_forward + svd_backward in one call for a caller holding grad_output up
  * front (the reference benchmark's layer step, bench.hpp:166-209): the four
  * chain sweeps run as two paired launches.  Same outputs as the two calls;

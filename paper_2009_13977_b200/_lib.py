@@ -57,6 +57,10 @@ SIGNATURES = {
                                      I64, VP]),
     "fasth_svd_forward_backward": (C.c_int, [VP, C.POINTER(SvdParamC), VP, I64, VP, I64, C.c_int, C.c_int, VP,
                                              I64, VP, I64, VP, I64, VP, I64, VP]),
+    "fasth_svd_plan_create": (C.c_int, [VP, C.POINTER(SvdParamC), C.c_int, C.c_int, C.c_int, C.POINTER(VP)]),
+    "fasth_svd_plan_destroy": (C.c_int, [VP]),
+    "fasth_svd_forward_planned": (C.c_int, [VP, C.POINTER(SvdParamC), VP, VP, I64, C.c_int, C.c_int, VP, I64,
+                                            C.POINTER(VP)]),
     "fasth_svd_tape_destroy": (C.c_int, [VP]),
     "fasth_svd_step": (C.c_int, [VP, C.POINTER(SvdParamC), VP, I64, VP, I64, VP, C.c_float,
                                  C.c_float, VP, I64, VP, I64, VP]),

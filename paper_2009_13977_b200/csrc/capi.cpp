@@ -293,6 +293,14 @@ struct fasth_tape_s {
     float* lb_ws = nullptr;  // large-batch path (lb.h): workspace holding the forward stages
 };
 
+struct fasth_svd_plan_s {
+    fasth_ctx ctx = nullptr;
+    int out_dim = 0, in_dim = 0, m = 0, b = 0;
+    fasth_tape u = nullptr, v = nullptr;  // built tapes (no activations yet)
+    cudaEvent_t ready = nullptr;           // recorded on the side stream (nullptr: same stream)
+    bool used = false;                     // single use: the forward takes the tapes
+};
+
 struct fasth_svd_tape_s {
     fasth_ctx ctx = nullptr;
     int out_dim = 0, in_dim = 0, m = 0, k = 0;
@@ -1330,9 +1338,71 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
 }
 
 // ---- SVD layer -------------------------------------------------------------
+fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan, const float* X,
+                              int64_t ldx, int m, int block_width, float* Y, int64_t ldy, fasth_svd_tape* tape);
+
 fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx,
                                int m, int block_width, float* Y, int64_t ldy,
                                fasth_svd_tape* tape) {
+    return svd_forward_impl(c, p, nullptr, X, ldx, m, block_width, Y, ldy, tape);
+}
+
+fasth_status fasth_svd_plan_create(fasth_ctx c, const fasth_svd_param* p, int m, int block_width,
+                                   int on_side_stream, fasth_svd_plan* out) {
+    if (!c || !out) return fail(FASTH_ERR_INVALID, "svd_plan_create: null argument");
+    *out = nullptr;
+    TRY(check_param("svd_plan_create", p));
+    if (m < 0) return fail(FASTH_ERR_DIMENSION, "svd_plan_create: negative batch");
+    fasth_svd_plan pl = new fasth_svd_plan_s;
+    pl->ctx = c;
+    pl->out_dim = p->out_dim;
+    pl->in_dim = p->in_dim;
+    pl->m = m;
+    pl->b = block_width;
+    const fasthb::lb::Streams* side = on_side_stream ? c->svd_streams() : nullptr;
+    cudaStream_t main_stream = c->stream;
+    fasth_status s = FASTH_OK;
+    if (side) {
+        cudaEventRecord(side->ev[8], c->stream);  // after everything that produced U, V
+        cudaStreamWaitEvent(side->aux, side->ev[8], 0);
+        c->stream = side->aux;
+    }
+    if (p->nv > 0 && m > 0) s = new_tape(c, p->V, p->ldv, p->in_dim, p->nv, m, block_width, 1, 1, &pl->v);
+    if (s == FASTH_OK && p->nu > 0 && m > 0) s = new_tape(c, p->U, p->ldu, p->out_dim, p->nu, m, block_width, 0, 0, &pl->u);
+    if (side) {
+        c->stream = main_stream;
+        if (s == FASTH_OK && cudaEventCreateWithFlags(&pl->ready, cudaEventDisableTiming) == cudaSuccess)
+            cudaEventRecord(pl->ready, side->aux);
+    }
+    if (s != FASTH_OK) {
+        fasth_svd_plan_destroy(pl);
+        return s;
+    }
+    *out = pl;
+    return FASTH_OK;
+}
+
+fasth_status fasth_svd_plan_destroy(fasth_svd_plan pl) {
+    if (!pl) return FASTH_OK;
+    free_tape(pl->u);
+    free_tape(pl->v);
+    if (pl->ready) cudaEventDestroy(pl->ready);
+    delete pl;
+    return FASTH_OK;
+}
+
+fasth_status fasth_svd_forward_planned(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan,
+                                       const float* X, int64_t ldx, int m, int block_width, float* Y,
+                                       int64_t ldy, fasth_svd_tape* tape) {
+    if (!plan) return fail(FASTH_ERR_INVALID, "svd_forward_planned: null plan");
+    if (plan->used) return fail(FASTH_ERR_INVALID, "svd_forward_planned: plan already consumed");
+    if (plan->out_dim != p->out_dim || plan->in_dim != p->in_dim || plan->m != m || plan->b != block_width)
+        return fail(FASTH_ERR_DIMENSION, "svd_forward_planned: plan built for another shape / block width");
+    return svd_forward_impl(c, p, plan, X, ldx, m, block_width, Y, ldy, tape);
+}
+
+fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan, const float* X,
+                              int64_t ldx, int m, int block_width, float* Y, int64_t ldy, fasth_svd_tape* tape) {
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     TRY(check_param("svd_forward", p));
     TRY(check_mat("svd_forward: X", X, ldx, p->in_dim, m));
@@ -1348,9 +1418,20 @@ fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const floa
     do {
         s = c->alloc_n((size_t)p->in_dim * std::max(m, 1), &st->T1);
         if (s) break;
+        if (plan) {  // prepared blocks: take the plan's tapes, join its side-stream builds
+            st->v = plan->v;
+            st->u = plan->u;
+            plan->v = plan->u = nullptr;
+            plan->used = true;
+            if (plan->ready) {
+                CU(cudaStreamWaitEvent(c->stream, plan->ready, 0));
+                c->after_stream_wait = true;
+            }
+        }
         // The U leg's WY build does not depend on the V leg: it runs on the side
         // stream (fork after everything enqueued so far, join before the U sweep)
-        const fasthb::lb::Streams* side = (p->nu > 0 && p->nv > 0 && m > 0) ? c->svd_streams() : nullptr;
+        const fasthb::lb::Streams* side =
+            (!plan && p->nu > 0 && p->nv > 0 && m > 0) ? c->svd_streams() : nullptr;
         if (side) {
             CU(cudaEventRecord(side->ev[8], c->stream));
             CU(cudaStreamWaitEvent(side->aux, side->ev[8], 0));
@@ -1363,8 +1444,11 @@ fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const floa
         }
         // V^T leg: the reversed V chain (svd_layer.hpp:113)
         if (p->nv > 0 && m > 0) {
-            s = new_tape(c, p->V, p->ldv, p->in_dim, p->nv, m, block_width, 1, 1, &st->v);
+            if (!st->v) s = new_tape(c, p->V, p->ldv, p->in_dim, p->nv, m, block_width, 1, 1, &st->v);
             if (s) break;
+            // the sweep reads its input before griddepcontrol.wait (its predecessor is
+            // meant to be the builder): prepared blocks => no programmatic launch
+            if (plan) c->after_stream_wait = true;
             s = run_forward(c, st->v, X, ldx, st->T1, p->in_dim, tape != nullptr);
         } else {
             s = copy_cols(c, X, ldx, st->T1, p->in_dim, p->in_dim, m);
@@ -1375,12 +1459,13 @@ fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const floa
             if (side) {
                 CU(cudaStreamWaitEvent(c->stream, side->ev[9], 0));
                 c->after_stream_wait = true;
-            } else {
+            } else if (!st->u) {
                 s = new_tape(c, p->U, p->ldu, p->out_dim, p->nu, m, block_width, 0, 0, &st->u);
             }
             if (s) break;
             st->u->scale = p->sigma;
             st->u->n_valid = st->k;
+            if (plan || side) c->after_stream_wait = true;  // T1 comes from the preceding V sweep
             s = run_forward(c, st->u, st->T1, p->in_dim, Y, ldy, tape != nullptr);
         } else {
             s = c->timed([&] { return launch_scale_rows(st->T1, p->in_dim, st->k, p->sigma, p->out_dim, m, Y,

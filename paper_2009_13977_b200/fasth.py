@@ -371,8 +371,37 @@ class SvdTape:
             pass
 
 
-def svd_forward(p: SvdParam, X: torch.Tensor, block_width: int, *, ctx: Context | None = None):
-    """svd_layer.hpp:106 — returns (Y, tape), Y = U (Sigma (V^T X))."""
+class SvdPlan:
+    """Both legs' WY blocks built ahead of a forward (``fasth_svd_plan_create``);
+    single use: ``svd_forward(..., plan=)`` consumes it."""
+
+    def __init__(self, ctx, handle, m, block_width):
+        self.ctx, self.h, self.m, self.block_width = ctx, handle, m, block_width
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                self.ctx.lib.fasth_svd_plan_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def svd_plan(p: SvdParam, m: int, block_width: int, *, side_stream: bool = True,
+             ctx: Context | None = None) -> SvdPlan:
+    """Build layer p's WY blocks now (on the context's side stream by default),
+    for a later ``svd_forward(p, X, block_width, plan=...)`` with X of m columns."""
+    pc = p._c()
+    c = _ctx(ctx, p.sigma)
+    h = C.c_void_p()
+    _check(c.lib.fasth_svd_plan_create(c.h, C.byref(pc), int(m), int(block_width), int(side_stream), C.byref(h)))
+    return SvdPlan(c, h, m, block_width)
+
+
+def svd_forward(p: SvdParam, X: torch.Tensor, block_width: int, *, ctx: Context | None = None,
+                plan: SvdPlan | None = None):
+    """svd_layer.hpp:106 — returns (Y, tape), Y = U (Sigma (V^T X)).  With
+    ``plan`` (from ``svd_plan``) the prepared WY blocks are used (and consumed)."""
     X, ldx = _colmajor(X, "svd_forward: X")
     if X.shape[0] != p.in_dim:
         raise DimensionError(f"svd_forward: X has {X.shape[0]} rows, in_dim {p.in_dim}")
@@ -381,8 +410,14 @@ def svd_forward(p: SvdParam, X: torch.Tensor, block_width: int, *, ctx: Context 
     m = X.shape[1]
     Y = _new_out(p.out_dim, m, X)
     h = C.c_void_p()
-    _check(c.lib.fasth_svd_forward(c.h, C.byref(pc), _ptr(X), ldx, m, int(block_width), _ptr(Y),
-                                   max(p.out_dim, 1), C.byref(h)))
+    if plan is not None:
+        if not plan.h:
+            raise Error("svd_forward: plan already consumed")
+        _check(c.lib.fasth_svd_forward_planned(c.h, C.byref(pc), plan.h, _ptr(X), ldx, m, int(block_width),
+                                               _ptr(Y), max(p.out_dim, 1), C.byref(h)))
+    else:
+        _check(c.lib.fasth_svd_forward(c.h, C.byref(pc), _ptr(X), ldx, m, int(block_width), _ptr(Y),
+                                       max(p.out_dim, 1), C.byref(h)))
     return Y, SvdTape(c, h, m)
 
 

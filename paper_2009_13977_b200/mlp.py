@@ -33,6 +33,7 @@ class MLPConfig:
     lam: float = 1e-3        # log|det| regulariser weight
     eta: float = 1e-3        # SGD step (svd_layer.hpp:158)
     clamp_eps: float = 0.5   # clamp_sigma epsilon (svd_layer.hpp:196)
+    prebuild: bool = True    # build layer k+1's WY blocks while layer k sweeps (svd_plan)
 
 
 def random_layers(cfg: MLPConfig, seed: int = 0, device="cuda"):
@@ -55,8 +56,15 @@ def train_step(layers, x, target, cfg: MLPConfig, ctx=None):
     the loss as a 0-d device tensor (no host sync)."""
     hs, pre, tapes = [x], [], []
     h = x
+    m = x.shape[1]
+    # layer k+1's WY blocks are built on the side stream while layer k sweeps
+    # (they depend only on that layer's U and V)
+    plan = fb.svd_plan(layers[0], m, cfg.block_width, ctx=ctx) if cfg.prebuild else None
     for k, p in enumerate(layers):
-        y, tape = fb.svd_forward(p, h, cfg.block_width, ctx=ctx)
+        nxt = (fb.svd_plan(layers[k + 1], m, cfg.block_width, ctx=ctx)
+               if cfg.prebuild and k + 1 < len(layers) else None)
+        y, tape = fb.svd_forward(p, h, cfg.block_width, ctx=ctx, plan=plan)
+        plan = nxt
         tapes.append(tape)
         pre.append(y)
         h = torch.nn.functional.leaky_relu(y, cfg.slope) if k < cfg.depth - 1 else y

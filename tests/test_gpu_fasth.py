@@ -398,6 +398,32 @@ def test_svd_forward_backward_fused_matches_two_calls(fb, golden, case):
     assert rel(Y1, g["Y"]) <= TOL and rel(g1.grad_input, g["dX"]) <= TOL and rel(g1.grad_U_vectors, g["dU"]) <= TOL
 
 
+def test_svd_plan_forward_equals_plain(fb):
+    """svd_plan (WY blocks built ahead, on the side stream) + svd_forward(plan=)
+    == svd_forward bitwise; a plan is single use and shape checked."""
+    import torch
+    d, m = 256, 32
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    U = torch.randn(d, d, device="cuda", generator=gen)
+    V = torch.randn(d, d, device="cuda", generator=gen)
+    s = torch.rand(d, device="cuda", generator=gen) + 0.5
+    X = torch.randn(m, d, device="cuda", generator=gen).t()
+    G = torch.randn(m, d, device="cuda", generator=gen).t()
+    p = fb.SvdParam(d, d, U, V, s)
+    Y0, t0 = fb.svd_forward(p, X, 32)
+    g0 = fb.svd_backward(p, t0, G)
+    plan = fb.svd_plan(p, m, 32)
+    Y1, t1 = fb.svd_forward(p, X, 32, plan=plan)
+    g1 = fb.svd_backward(p, t1, G)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1) and torch.equal(g0.grad_input, g1.grad_input)
+    assert torch.equal(g0.grad_U_vectors, g1.grad_U_vectors) and torch.equal(g0.grad_V_vectors, g1.grad_V_vectors)
+    with pytest.raises(fb.Error):
+        fb.svd_forward(p, X, 32, plan=plan)  # consumed
+    with pytest.raises(fb.DimensionError):
+        fb.svd_forward(p, X, 16, plan=fb.svd_plan(p, m, 32))  # other block width
+
+
 def test_svd_forward_backward_fused_d784(fb):
     """Config 2 as the layer (d = 784, b = 32, m = 32): paired path == two calls, bitwise."""
     import torch
