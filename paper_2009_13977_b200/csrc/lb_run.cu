@@ -58,106 +58,111 @@ __global__ void diag_inv_kernel(const float* __restrict__ Mm, int B, float* __re
 }
 
 // T_z = M_z^{-1} by blocked back-substitution over 32-row chunks:
-//   T[rc][cc] = Dinv_rc (E - sum_{k > rc} M[rc][k] T[k][cc]).
-// One CTA per pair of 32-column chunks (cc, B/32-1-cc) for balanced work.
+//   T[rc][cc] = Dinv_rc (E - sum_{k > rc} M[rc][k] T[k][cc]),
+// one CTA per pair of CW-column chunks (cc, B/CW-1-cc) for balanced work (CW =
+// 16: twice the CTAs of 32-wide chunks, half the work per dependent step).
 // The M row panel of step rc-1 streams into shared memory (cp.async, double
 // buffered) while step rc computes; the update product is register blocked:
-// 64 threads x (4 rows x 4 columns) cover the 32 x 32 block, 4 thread groups
-// take contiguous quarters of k.  Writes T and T^T, both split.
-// grid (B/64, nz), 256 threads.
+// 64 threads x (4 rows x CW/8 columns) cover the 32 x CW block, 4 thread
+// groups take contiguous quarters of k.  Writes T and T^T, both split.
+// grid (B/(2 CW), nz), 256 threads.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                  "l"(src)
                  : "memory");
 }
+template <int CW>
 __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ Mm, const float* __restrict__ Dinv,
                                                       int B, float* __restrict__ Th, float* __restrict__ Tl,
                                                       float* __restrict__ TTh, float* __restrict__ TTl) {
+    constexpr int CPT = CW / 8;     // columns per thread in the update
+    constexpr int RP = CW + 1;      // red / R pitch
     extern __shared__ float sm[];
     const int MP = B + 12;          // panel pitch: at most 2-way conflicts for the float4 reads
-    float* Tc = sm;                 // [B][32] solution chunk
-    float* Mp = Tc + B * 32;        // [2][32][MP] M row panels
-    float* red = Mp + 2 * 32 * MP;  // [4][32][33] k-split partial sums
-    float* R = red + 4 * 32 * 33;   // [32][33] right-hand side
-    float* Ddb = R + 32 * 33;       // [2][32][36] diagonal-block inverses
-    const int z = blockIdx.y, nchunk = B / 32;
+    float* Tc = sm;                 // [B][CW] solution chunk
+    float* Mp = Tc + B * CW;        // [2][32][MP] M row panels
+    float* red = Mp + 2 * 32 * MP;  // [4][32][RP] k-split partial sums (also the T^T tile)
+    float* R = red + 4 * 32 * RP;   // [32][RP] right-hand side
+    float* Ddb = R + 32 * RP;       // [2][32][36] diagonal-block inverses
+    const int z = blockIdx.y, nchunk = B / CW;
     const float* M = Mm + (int64_t)z * B * B;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int kq = tid >> 6, t64 = tid & 63, rg = t64 >> 3, cg = t64 & 7;
     for (int pass = 0; pass < 2; ++pass) {
         const int cc = pass == 0 ? blockIdx.x : nchunk - 1 - blockIdx.x;
-        const int c0 = cc * 32, k1 = c0 + 32;
+        const int c0 = cc * CW, k1 = c0 + CW;
         // step rc's operands -> buffer rc & 1: the M panel (rows rc*32..,
         // columns [(rc+1)*32, k1)) and Dinv_rc
         auto prefetch = [&](int rc) {
             if (rc < 0) return;
-            const int k0 = (rc + 1) * 32, nf4 = (k1 - k0) / 4;
+            const int k0 = (rc + 1) * 32, nf4 = k1 > k0 ? (k1 - k0) / 4 : 0;
             float* dst = Mp + (rc & 1) * 32 * MP;
             for (int e = tid; e < 32 * nf4; e += 256) {
                 const int i = e / nf4, k = k0 + 4 * (e % nf4);
                 cp_async16(dst + i * MP + k, M + (int64_t)(rc * 32 + i) * B + k);
             }
-            const float* D = Dinv + ((int64_t)z * nchunk + rc) * 1024;
+            const float* D = Dinv + ((int64_t)z * (B / 32) + rc) * 1024;
             float* dd = Ddb + (rc & 1) * 32 * 36;
             const int i = tid >> 3, k = (tid & 7) * 4;
             cp_async16(dd + i * 36 + k, D + i * 32 + k);
             asm volatile("cp.async.commit_group;" ::: "memory");
         };
         __syncthreads();
-        for (int e = tid; e < B * 32; e += 256) Tc[e] = 0.f;
-        prefetch(cc);
+        for (int e = tid; e < B * CW; e += 256) Tc[e] = 0.f;
+        const int rtop = c0 / 32;  // row chunk holding the chunk's diagonal
+        prefetch(rtop);
         __syncthreads();
-        for (int rc = cc; rc >= 0; --rc) {
+        for (int rc = rtop; rc >= 0; --rc) {
             const int r0 = rc * 32, k0 = (rc + 1) * 32;
             const float* Dd = Ddb + (rc & 1) * 32 * 36;
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();  // panel rc landed (all threads' copies); the other buffer is free
             prefetch(rc - 1);
             {  // partial products over this group's quarter of [k0, k1)
-                const int q4 = (k1 - k0) / 4;
+                const int q4 = k1 > k0 ? (k1 - k0) / 4 : 0;
                 const int kb = k0 + kq * q4, ke = kb + q4;
                 const float* mp = Mp + (rc & 1) * 32 * MP + (4 * rg) * MP;
-                float acc[4][4] = {};
+                float acc[4][CPT] = {};
                 for (int k = kb; k < ke; k += 4) {
                     float4 m4[4];
 #pragma unroll
                     for (int a = 0; a < 4; ++a) m4[a] = *reinterpret_cast<const float4*>(mp + a * MP + k);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        const float4 t4 = *reinterpret_cast<const float4*>(Tc + (k + kk) * 32 + 4 * cg);
-                        const float tv[4] = {t4.x, t4.y, t4.z, t4.w};
+                        float tv[CPT];
+#pragma unroll
+                        for (int bq = 0; bq < CPT; ++bq) tv[bq] = Tc[(k + kk) * CW + CPT * cg + bq];
 #pragma unroll
                         for (int a2 = 0; a2 < 4; ++a2) {
                             const float mv = kk == 0 ? m4[a2].x : kk == 1 ? m4[a2].y : kk == 2 ? m4[a2].z : m4[a2].w;
 #pragma unroll
-                            for (int bq = 0; bq < 4; ++bq) acc[a2][bq] = fmaf(mv, tv[bq], acc[a2][bq]);
+                            for (int bq = 0; bq < CPT; ++bq) acc[a2][bq] = fmaf(mv, tv[bq], acc[a2][bq]);
                         }
                     }
                 }
 #pragma unroll
                 for (int a2 = 0; a2 < 4; ++a2)
 #pragma unroll
-                    for (int bq = 0; bq < 4; ++bq) red[(kq * 32 + 4 * rg + a2) * 33 + 4 * cg + bq] = acc[a2][bq];
+                    for (int bq = 0; bq < CPT; ++bq) red[(kq * 32 + 4 * rg + a2) * RP + CPT * cg + bq] = acc[a2][bq];
             }
             __syncthreads();
-            for (int e = tid; e < 1024; e += 256) {
-                const int r = e >> 5, c = e & 31;
-                const float sum = red[(0 * 32 + r) * 33 + c] + red[(1 * 32 + r) * 33 + c] +
-                                  red[(2 * 32 + r) * 33 + c] + red[(3 * 32 + r) * 33 + c];
-                R[r * 33 + c] = (r0 + r == c0 + c ? 1.f : 0.f) - sum;
+            for (int e = tid; e < 32 * CW; e += 256) {
+                const int r = e / CW, c = e % CW;
+                const float sum = red[(0 * 32 + r) * RP + c] + red[(1 * 32 + r) * RP + c] +
+                                  red[(2 * 32 + r) * RP + c] + red[(3 * 32 + r) * RP + c];
+                R[r * RP + c] = (r0 + r == c0 + c ? 1.f : 0.f) - sum;
             }
             __syncthreads();
             {  // T[rc] = Dinv_rc R  (Dinv upper triangular)
-                const int r = tid >> 3, c4 = (tid & 7) * 4;
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                const int r = tid >> 3, cb = (tid & 7) * CPT;
+                float acc[CPT] = {};
                 for (int k = r; k < 32; ++k) {
                     const float dd = Dd[r * 36 + k];
-                    a0 = fmaf(dd, R[k * 33 + c4 + 0], a0);
-                    a1 = fmaf(dd, R[k * 33 + c4 + 1], a1);
-                    a2 = fmaf(dd, R[k * 33 + c4 + 2], a2);
-                    a3 = fmaf(dd, R[k * 33 + c4 + 3], a3);
+#pragma unroll
+                    for (int bq = 0; bq < CPT; ++bq) acc[bq] = fmaf(dd, R[k * RP + cb + bq], acc[bq]);
                 }
-                *reinterpret_cast<float4*>(Tc + (r0 + r) * 32 + c4) = make_float4(a0, a1, a2, a3);
+#pragma unroll
+                for (int bq = 0; bq < CPT; ++bq) Tc[(r0 + r) * CW + cb + bq] = acc[bq];
             }
             __syncthreads();
         }
@@ -165,20 +170,20 @@ __global__ void __launch_bounds__(256) tri_inv_kernel(const float* __restrict__ 
         float* tl = Tl + (int64_t)z * B * B;
         float* tth = TTh + (int64_t)z * B * B;
         float* ttl = TTl + (int64_t)z * B * B;
-        for (int e = tid; e < B * 32; e += 256) {
-            const int r = e >> 5, c = e & 31;
+        for (int e = tid; e < B * CW; e += 256) {
+            const int r = e / CW, c = e % CW;
             const float v = Tc[e];
             const float h = rn_hi(v);
             th[(int64_t)r * B + c0 + c] = h;
             tl[(int64_t)r * B + c0 + c] = v - h;
         }
-        for (int rb = 0; rb < B / 32; ++rb) {  // T^T through a padded 32 x 32 tile (red)
+        for (int rb = 0; rb < B / 32; ++rb) {  // T^T through a padded 32 x CW tile (red)
             __syncthreads();
 #pragma unroll
-            for (int u = 0; u < 4; ++u) red[lane * 33 + warp + 8 * u] = Tc[(rb * 32 + warp + 8 * u) * 32 + lane];
+            for (int u = 0; u < CPT; ++u) red[(warp + 8 * u) * 33 + lane] = Tc[(rb * 32 + lane) * CW + warp + 8 * u];
             __syncthreads();
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < CPT; ++u) {
                 const int c = warp + 8 * u;
                 const float v = red[c * 33 + lane];
                 const float h = rn_hi(v);
@@ -413,11 +418,12 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
     {
         ++nl;
         diag_inv_kernel<<<dim3(B / 32, nb), 32, 0, s>>>(Mm, B, Dinv);
-        const int smem = (B * 32 + 2 * 32 * (B + 12) + 4 * 32 * 33 + 32 * 33 + 2 * 32 * 36) * 4;
-        LBTRY(ensure_smem(reinterpret_cast<const void*>(tri_inv_kernel), smem));
+        constexpr int CW = 16;
+        const int smem = (B * CW + 2 * 32 * (B + 12) + 5 * 32 * (CW + 1) + 2 * 32 * 36) * 4;
+        LBTRY(ensure_smem(reinterpret_cast<const void*>(tri_inv_kernel<CW>), smem));
         ++nl;
         if (tm) tm->begin(s);
-        tri_inv_kernel<<<dim3(B / 64, nb), 256, smem, s>>>(Mm, Dinv, B, Th, Tl, TTh, TTl);
+        tri_inv_kernel<CW><<<dim3(B / (2 * CW), nb), 256, smem, s>>>(Mm, Dinv, B, Th, Tl, TTh, TTl);
         if (tm) tm->end(s, "lb_build_tri_inv");
         LBTRY(cudaGetLastError());
     }
