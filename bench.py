@@ -238,11 +238,17 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
     ctx = fb.Context(local, deferred=True)
     outs = (torch.empty(m, d, device="cuda").t(), torch.empty(m, d, device="cuda").t(),
             torch.empty(d, d, device="cuda"))
+    comm = None
+    if world > 1:  # dV all-reduced per 512-row bucket as the backward finishes it
+        from paper_2009_13977_b200.sharding import allreduce_dv_buckets
+        ctx.set_dv_buckets(4)
+        comm = torch.cuda.Stream()
 
     def step():
         _, back = fb.fasth_forward_backward(V, X, G, b, ctx=ctx, out=outs)
         if world > 1:
-            dist.all_reduce(back.grad_vectors)
+            allreduce_dv_buckets(back.grad_vectors, ctx.dv_buckets(), comm)
+            torch.cuda.current_stream().wait_stream(comm)
 
     for _ in range(warmup):
         step()
@@ -298,7 +304,8 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
             "flops_per_launch": fl[top],
             "note": "3xTF32 useful flops; CUDA events per launch on the context stream (kernels serialised "
                     "for this pass); ncu tensor-pipe activity of these GEMMs in profiles/r01_lb_*_full.txt"}
-    return {"workload": "BASELINE configs[4]: FastH fwd+bwd d=2048, batch-sharded, dV all-reduced (NCCL)",
+    return {"workload": "BASELINE configs[4]: FastH fwd+bwd d=2048, batch-sharded, dV all-reduced (NCCL, "
+                        "4 row buckets overlapped with the backward)",
             "roofline": roof, "kernels": kern,
             "d": d, "batch_per_gpu": m, "global_batch": m * world, "n_gpus": world,
             "us_per_step": ms * 1e3, "tflops": tf, "frac_3xtf32_peak": tf / (peak_3xtf32 * world),

@@ -83,6 +83,19 @@ fasth_status fasth_ctx_set_timing(fasth_ctx ctx, int mode);
 int fasth_ctx_kernel_times(fasth_ctx ctx, char* buf, int buflen);
 /* Release cached device memory held by the context's pool. */
 fasth_status fasth_ctx_trim(fasth_ctx ctx);
+/* dV row buckets for batch-sharded data parallelism (no reference
+ * counterpart: the reference is single-process).  `events` are
+ * caller-owned cudaEvent_t handles (count 0 turns the feature off).  Every
+ * later fasth_backward / fasth_forward_backward that writes dV records
+ * events[k] once dV rows [row_end[k-1], row_end[k]) are final, on the stream
+ * that wrote them: the large-batch path after each group of its WY blocks
+ * (so an all-reduce of those rows overlaps the rest of the backward), the
+ * chain paths once after the whole dV.  fasth_ctx_dv_buckets copies up to
+ * `max` row_end values of the last call and returns the bucket count (0: no
+ * events recorded; -1: bad arguments).  Bucket bounds are known when the
+ * call returns (before the device work completes). */
+fasth_status fasth_ctx_set_dv_events(fasth_ctx ctx, void* const* events, int count);
+int fasth_ctx_dv_buckets(fasth_ctx ctx, int64_t* row_end, int max);
 
 /* Device buffers from the context's pool and stream-ordered copies, so host
  * code (the C++ mirror, language bindings) needs no CUDA headers.

@@ -36,6 +36,8 @@ SIGNATURES = {
     "fasth_ctx_check": (C.c_int, [VP]),
     "fasth_ctx_launch_count": (I64, [VP]),
     "fasth_ctx_trim": (C.c_int, [VP]),
+    "fasth_ctx_set_dv_events": (C.c_int, [VP, C.POINTER(VP), C.c_int]),
+    "fasth_ctx_dv_buckets": (C.c_int, [VP, C.POINTER(I64), C.c_int]),
     "fasth_device_alloc": (C.c_int, [VP, I64, C.POINTER(VP)]),
     "fasth_device_free": (C.c_int, [VP, VP]),
     "fasth_copy": (C.c_int, [VP, VP, VP, I64, C.c_int]),

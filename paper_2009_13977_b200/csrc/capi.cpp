@@ -148,6 +148,28 @@ struct fasth_ctx_s {
     // set around a launch that follows a cross-stream event wait: it must not
     // use programmatic dependent launch (see run_forward)
     bool after_stream_wait = false;
+    // dV bucket events (fasth_ctx_set_dv_events): caller-owned cudaEvent_t
+    std::vector<cudaEvent_t> dv_events;
+    std::vector<int64_t> dv_row_end;
+    int dv_used = 0;
+    fasthb::lb::DvNotify* dv_notify(fasthb::lb::DvNotify& nt) {
+        if (dv_events.empty()) return nullptr;
+        nt.ev = dv_events.data();
+        nt.count = (int)dv_events.size();
+        nt.row_end = dv_row_end.data();
+        nt.used = 0;
+        return &nt;
+    }
+    // paths that finish dV in one piece: one bucket, recorded after the last
+    // dV launch on the context stream
+    fasth_status dv_notify_whole(int n) {
+        if (dv_events.empty()) return FASTH_OK;
+        cudaError_t e = cudaEventRecord(dv_events[0], stream);
+        if (e != cudaSuccess) return fail(FASTH_ERR_CUDA, "dV event record: %s", cudaGetErrorString(e));
+        dv_row_end[0] = n;
+        dv_used = 1;
+        return FASTH_OK;
+    }
     bool capturing = false;
     std::vector<void*> graph_held;
     cudaGraphExec_t host_exec = nullptr;
@@ -932,6 +954,21 @@ fasth_status fasth_ctx_synchronize(fasth_ctx c) {
     return FASTH_OK;
 }
 
+fasth_status fasth_ctx_set_dv_events(fasth_ctx c, void* const* events, int count) {
+    if (!c || count < 0 || (count > 0 && !events)) return fail(FASTH_ERR_INVALID, "fasth_ctx_set_dv_events: bad argument");
+    c->dv_events.assign(reinterpret_cast<const cudaEvent_t*>(events), reinterpret_cast<const cudaEvent_t*>(events) + count);
+    c->dv_row_end.assign(count, 0);
+    c->dv_used = 0;
+    return FASTH_OK;
+}
+
+int fasth_ctx_dv_buckets(fasth_ctx c, int64_t* row_end, int max) {
+    if (!c || max < 0 || (max > 0 && !row_end)) return -1;
+    const int k = std::min(max, c->dv_used);
+    for (int i = 0; i < k; ++i) row_end[i] = c->dv_row_end[i];
+    return c->dv_used;
+}
+
 fasth_status fasth_ctx_set_timing(fasth_ctx c, int mode) {
     if (!c || mode < 0 || mode > 2) return fail(FASTH_ERR_INVALID, "fasth_ctx_set_timing: bad argument");
     if (c->timing == 2)
@@ -1038,14 +1075,17 @@ fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, in
     if (s == FASTH_OK) s = dx.open(d, m);
     int nl = 1;
     LbTimer lt(c);
+    fasthb::lb::DvNotify nt;
+    fasthb::lb::DvNotify* ntp = dV ? c->dv_notify(nt) : nullptr;
     if (s == FASTH_OK)
         s = c->timed(
             [&] {
                 return fasthb::lb::forward_backward(V, ldv, d, n, X, ldx, G, ldg, m, y.ptr(), y.pitch(d), dx.ptr(),
                                                     dx.pitch(d), dV, lddv, ws, c->err_d, c->stream, c->num_sms, &nl,
-                                                    c->timing == 1 ? &lt : nullptr, c->lb_streams());
+                                                    c->timing == 1 ? &lt : nullptr, c->lb_streams(), ntp);
             },
             "large_batch(fwd+bwd)");
+    if (ntp) c->dv_used = nt.used;
     c->launches += nl - 1;
     c->after_stream_wait = true;  // the step joined its side streams
     if (s == FASTH_OK) s = y.close(d, m);
@@ -1129,6 +1169,7 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
                             int64_t lddx, float* dV, int64_t lddv) {
     if (!c || !t) return fail(FASTH_ERR_INVALID, "fasth_backward: null ctx or tape");
     const int d = t->plan.d, n = t->plan.n, m = t->m;
+    c->dv_used = 0;
     TRY(check_mat("fasth_backward: G", G, ldg, d, m));
     if (dX) TRY(check_mat("fasth_backward: dX", dX, lddx, d, m));
     if (dV) TRY(check_mat("fasth_backward: dV", dV, lddv, d, n));
@@ -1138,24 +1179,29 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
     }
     if (m == 0) {
         if (dV) CU(cudaMemset2DAsync(dV, lddv * sizeof(float), 0, d * sizeof(float), n, c->stream));
+        if (dV) TRY(c->dv_notify_whole(n));
         return c->finish();
     }
     if (t->lb_ws) {
         OutBuf dx{c, dX, lddx};
         TRY(dx.open(d, m));
         int nl = 1;
+        fasthb::lb::DvNotify nt;
+        fasthb::lb::DvNotify* ntp = dV ? c->dv_notify(nt) : nullptr;
         TRY(c->timed(
             [&] {
                 return fasthb::lb::backward(d, n, m, G, ldg, dx.ptr(), dx.pitch(d), dV, lddv, t->lb_ws, c->stream,
-                                            c->num_sms, &nl, nullptr, c->lb_streams());
+                                            c->num_sms, &nl, nullptr, c->lb_streams(), false, ntp);
             },
             "large_batch(bwd)"));
+        if (ntp) c->dv_used = nt.used;
         c->launches += nl - 1;
         c->after_stream_wait = true;  // the step joined its side streams
         TRY(dx.close(d, m));
         return c->finish();
     }
     TRY(run_backward(c, t, G, ldg, d, nullptr, dX, lddx, dV, lddv));
+    if (dV) TRY(c->dv_notify_whole(n));
     return c->finish();
 }
 
@@ -1187,6 +1233,7 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
     TRY(check_mat("fasth_backward: G", G, ldg, d, m));
     if (dX) TRY(check_mat("fasth_backward: dX", dX, lddx, d, m));
     if (dV) TRY(check_mat("fasth_backward: dV", dV, lddv, d, n));
+    c->dv_used = 0;
     if (n == 0 || m == 0) {  // the two-call path handles the degenerate shapes
         fasth_tape t = nullptr;
         TRY(fasth_forward(c, V, ldv, d, n, X, ldx, m, block_width, Y, ldy, &t));
@@ -1199,6 +1246,7 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
     fasth_tape t = nullptr;
     TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr));
     fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);
+    if (s == FASTH_OK && dV) s = c->dv_notify_whole(n);
     free_tape(t);  // pool reuse is stream ordered
     if (s == FASTH_OK) s = c->finish();
     return s;

@@ -104,6 +104,19 @@ struct Streams {
     cudaEvent_t ev[12] = {};  // 0-7: large-batch step, 8-11: SVD layer legs (capi.cpp)
 };
 
+// dV completion per row bucket (batch-sharded data parallelism, SURVEY
+// §8(e)): the backward records ev[k] on the stream that wrote the last dV
+// rows of bucket k as soon as they are final, so a caller can all-reduce
+// those rows while the remaining blocks run.  Blocks are grouped into
+// min(count, blocks) buckets in backward order (rows 0.. first); row_end[k]
+// is the exclusive end row of bucket k, `used` the bucket count.
+struct DvNotify {
+    const cudaEvent_t* ev = nullptr;
+    int count = 0;
+    int64_t* row_end = nullptr;
+    int used = 0;
+};
+
 // The whole large-batch step (lb_run.cu).
 int pick_block(int n);
 bool supported(int d, int n, int m);
@@ -117,11 +130,11 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
                     Timer* tm = nullptr, const Streams* st = nullptr, const float* G = nullptr, int64_t ldg = 0);
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
                      int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm = nullptr,
-                     const Streams* st = nullptr, bool g_split = false);
+                     const Streams* st = nullptr, bool g_split = false, DvNotify* nt = nullptr);
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
-                             Timer* tm = nullptr, const Streams* st = nullptr);
+                             Timer* tm = nullptr, const Streams* st = nullptr, DvNotify* nt = nullptr);
 
 // Elementwise helpers (lb_path.cu).
 // split rows x cols (ld_in) into hi/lo (ld_out)

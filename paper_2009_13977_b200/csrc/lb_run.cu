@@ -495,7 +495,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
 // Backward chain and dV from the forward's workspace (same d, n, m).
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
                      int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm,
-                     const Streams* st, bool g_split) {
+                     const Streams* st, bool g_split, DvNotify* nt) {
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
@@ -582,6 +582,15 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             ++nl;
             dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv, lddv);
             if (two) LBTRY(cudaEventRecord(st->ev[4 + (j & 1)], sa));
+            if (nt && nt->count > 0) {  // last block of its bucket: rows up to here are final
+                const int nbk = std::min(nt->count, nb);
+                const int bk = (int)((int64_t)j * nbk / nb);
+                if (j + 1 == nb || (int)((int64_t)(j + 1) * nbk / nb) != bk) {
+                    LBTRY(cudaEventRecord(nt->ev[bk], sa));
+                    nt->row_end[bk] = std::min<int64_t>(n, (int64_t)(j + 1) * B);
+                    nt->used = bk + 1;
+                }
+            }
         }
         {
             // block j-1's dV read the G buffer this update overwrites
@@ -620,10 +629,10 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
-                             Timer* tm, const Streams* st) {
+                             Timer* tm, const Streams* st, DvNotify* nt) {
     int n1 = 0, n2 = 0;
     cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1, tm, st, G, ldg);
-    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm, st, true);
+    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm, st, true, nt);
     if (nlaunch) *nlaunch = n1 + n2;
     return e;
 }

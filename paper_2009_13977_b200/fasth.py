@@ -113,6 +113,31 @@ class Context:
             out[name] = (float(ms), int(cnt))
         return out
 
+    def set_dv_buckets(self, count: int):
+        """Ask later fasth_backward / fasth_forward_backward calls to signal
+        dV row buckets as they complete (fasth_ctx_set_dv_events): ``count``
+        torch CUDA events, read back with :meth:`dv_buckets`.  0 turns it off."""
+        evs = [torch.cuda.Event() for _ in range(count)]
+        with torch.cuda.device(self.device):
+            for e in evs:  # torch creates the CUDA event on first record
+                e.record()
+        arr = (C.c_void_p * max(count, 1))(*[C.c_void_p(e.cuda_event) for e in evs])
+        _check(self.lib.fasth_ctx_set_dv_events(self.h, arr, count))
+        self._dv_events = evs
+
+    def dv_buckets(self) -> list:
+        """[(row_begin, row_end, event)] of the last call's dV buckets, in
+        completion order; all-reduce dV[row_begin:row_end] on a stream that
+        waits on `event`."""
+        evs = getattr(self, "_dv_events", [])
+        ends = (C.c_int64 * max(len(evs), 1))()
+        k = self.lib.fasth_ctx_dv_buckets(self.h, ends, len(evs))
+        out, lo = [], 0
+        for i in range(max(k, 0)):
+            out.append((lo, int(ends[i]), evs[i]))
+            lo = int(ends[i])
+        return out
+
     @property
     def launch_count(self) -> int:
         return int(self.lib.fasth_ctx_launch_count(self.h))

@@ -228,3 +228,73 @@ def test_default_selection_mid_batch(monkeypatch):
         names = set(ctx.kernel_times())
         ctx.set_timing(False)
         assert ("large_batch(fwd+bwd)" in names) == lb, names
+
+
+@pytest.mark.parametrize("count,lb", [(4, True), (2, True), (3, True), (4, False), (0, True)])
+def test_dv_bucket_events(count, lb, monkeypatch):
+    """fasth_ctx_set_dv_events: each bucket's event fires only once its dV
+    rows are final (a side stream copies each slice right after waiting on
+    its event; the copies must equal the finished dV), buckets tile [0, n)
+    in order, and the chain path reports one whole-dV bucket."""
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.setenv("FASTH_LB", "1" if lb else "0")
+    n = d = 2048 if lb else 256
+    m = 1024 if lb else 32
+    V, X, G = inputs(n, d, m, seed=11)
+    ctx = fb.Context(0)
+    ctx.set_dv_buckets(count)
+    side = torch.cuda.Stream()
+    for rep in range(2):
+        dV = torch.full((n, d), float("nan"), device="cuda")
+        snap = torch.full((n, d), float("nan"), device="cuda")
+        outs = (torch.empty(m, d, device="cuda").t(), torch.empty(m, d, device="cuda").t(), dV)
+        fb.fasth_forward_backward(V, X, G, 32, ctx=ctx, out=outs)
+        bk = ctx.dv_buckets()
+        for lo, hi, ev in bk:
+            side.wait_event(ev)
+            with torch.cuda.stream(side):
+                snap[lo:hi].copy_(dV[lo:hi])
+        torch.cuda.synchronize()
+        if count == 0:
+            assert bk == []
+            continue
+        want = min(count, n // 512) if lb else 1
+        assert len(bk) == want, bk
+        assert bk[0][0] == 0 and bk[-1][1] == n and all(a[1] == b[0] for a, b in zip(bk, bk[1:]))
+        assert torch.equal(snap, dV), f"rep {rep}: a bucket event fired before its rows were final"
+        assert torch.isfinite(dV).all()
+
+
+def test_dv_buckets_nccl_allreduce_single_rank(monkeypatch):
+    """The bench's world > 1 step (sharding.allreduce_dv_buckets on a comm
+    stream gated by the bucket events) through a 1-rank NCCL group: runs,
+    and the sum over one rank leaves dV unchanged."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2009_13977_b200 import fasth as fb
+    from paper_2009_13977_b200.sharding import allreduce_dv_buckets
+    monkeypatch.setenv("FASTH_LB", "1")
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        n = d = 2048
+        m = 1024
+        V, X, G = inputs(n, d, m, seed=12)
+        ctx = fb.Context(0)
+        ctx.set_dv_buckets(4)
+        comm = torch.cuda.Stream()
+        _, ref = fb.fasth_forward_backward(V, X, G, 32, ctx=ctx)
+        ref = ref.grad_vectors.clone()
+        for _ in range(3):
+            _, back = fb.fasth_forward_backward(V, X, G, 32, ctx=ctx)
+            allreduce_dv_buckets(back.grad_vectors, ctx.dv_buckets(), comm)
+            torch.cuda.current_stream().wait_stream(comm)
+        torch.cuda.synchronize()
+        assert torch.equal(back.grad_vectors, ref)
+    finally:
+        dist.destroy_process_group()

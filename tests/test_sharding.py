@@ -20,31 +20,34 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, d, m, b, out_q):
+def _worker(rank, world, port, d, m, b, out_q, bucketed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Port
-    from paper_2009_13977_b200.sharding import allreduce_grads
+    from paper_2009_13977_b200.sharding import allreduce_dv_buckets, allreduce_grads
     rng = np.random.default_rng(7)
     V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
     lo, hi = shard_range(m, world, rank)
     Y, dX, dV = Port().fasth_fwd_bwd(V, X[:, lo:hi], G[:, lo:hi], b)
     dVt = torch.tensor(dV)
-    allreduce_grads([dVt])
+    if bucketed:  # row buckets as Context.dv_buckets() reports them (events: GPU only)
+        allreduce_dv_buckets(dVt, [(0, 3, None), (3, 3, None), (3, 10, None), (10, d, None)])
+    else:
+        allreduce_grads([dVt])
     out_q.put((rank, lo, hi, Y, dX, dVt.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m", [8, 7])
-def test_batch_sharded_dV_allreduce_gloo(m):
+@pytest.mark.parametrize("m,bucketed", [(8, False), (7, False), (7, True)])
+def test_batch_sharded_dV_allreduce_gloo(m, bucketed):
     from oracle.oracle import Port, relative_error
     d, b, world = 24, 5, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, d, m, b, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, d, m, b, q, bucketed)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
