@@ -1389,6 +1389,76 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
 fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan, const float* X,
                               int64_t ldx, int m, int block_width, float* Y, int64_t ldy, fasth_svd_tape* tape);
 
+// Both legs on the large-batch path (same thresholds as fasth_forward).
+bool svd_large_batch(const fasth_svd_param* p, int m) {
+    return m > 0 && p->nu > 0 && p->nv > 0 && use_large_batch(p->in_dim, p->nv, m) &&
+           use_large_batch(p->out_dim, p->nu, m);
+}
+
+// Large-batch SVD layer forward (svd_layer.hpp:106-116): the V^T leg is the V
+// chain in reverse order (svd_layer.hpp:113), run as the large-batch step on
+// a vector-reversed copy of V; Sigma between the legs is materialised
+// (T2 = Sigma T1, zero rows past k) instead of fused into the sweep's loads.
+fasth_status lb_svd_forward(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx, int m, int b,
+                            float* Y, int64_t ldy, fasth_svd_tape st) {
+    float *vrev = nullptr, *T2 = nullptr;
+    TRY(c->alloc_n((size_t)p->in_dim * p->nv, &vrev));
+    fasth_status s = FASTH_OK;
+    do {
+        s = c->timed([&] { return fasthb::lb::reverse_vectors(p->V, p->ldv, p->in_dim, p->nv, vrev, p->in_dim,
+                                                              c->stream); }, "lb_reverse");
+        if (s) break;
+        s = lb_forward(c, vrev, p->in_dim, p->in_dim, p->nv, X, ldx, m, b, st->T1, p->in_dim, &st->v);
+        if (s) break;
+        s = c->alloc_n((size_t)p->out_dim * m, &T2);
+        if (s) break;
+        s = c->timed([&] { return launch_scale_rows(st->T1, p->in_dim, st->k, p->sigma, p->out_dim, m, T2,
+                                                    p->out_dim, 0, c->stream); }, "scale_rows");
+        if (s) break;
+        s = lb_forward(c, p->U, p->ldu, p->out_dim, p->nu, T2, p->out_dim, m, b, Y, ldy, &st->u);
+    } while (0);
+    c->release(vrev);  // pool reuse is stream ordered
+    if (T2) c->release(T2);
+    return s;
+}
+
+// Large-batch SVD layer backward (svd_layer.hpp:122-147) on the tapes above.
+fasth_status lb_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd_tape st, const float* G,
+                             int64_t ldg, float* dX, int64_t lddx, float* dU, int64_t lddu, float* dV,
+                             int64_t lddv, float* dsigma) {
+    const int m = st->m, k = st->k;
+    float *dT2 = nullptr, *dT1 = nullptr, *dvrev = nullptr;
+    fasth_status s = c->alloc_n((size_t)p->out_dim * m, &dT2);
+    do {
+        if (s) break;
+        s = fasth_backward(c, st->u, G, ldg, dT2, p->out_dim, dU, lddu);
+        if (s) break;
+        if (dsigma) {
+            s = c->timed([&] { return launch_dsigma(dT2, p->out_dim, st->T1, p->in_dim, k, m, dsigma,
+                                                    c->stream); }, "dsigma");
+            if (s) break;
+        }
+        s = c->alloc_n((size_t)p->in_dim * m, &dT1);
+        if (s) break;
+        s = c->timed([&] { return launch_scale_rows(dT2, p->out_dim, k, p->sigma, p->in_dim, m, dT1, p->in_dim, 0,
+                                                    c->stream); }, "scale_rows");
+        if (s) break;
+        if (dV) {
+            s = c->alloc_n((size_t)p->in_dim * p->nv, &dvrev);
+            if (s) break;
+        }
+        s = fasth_backward(c, st->v, dT1, p->in_dim, dX, lddx, dvrev, p->in_dim);
+        if (s) break;
+        if (dV)
+            s = c->timed([&] { return fasthb::lb::reverse_vectors(dvrev, p->in_dim, p->in_dim, p->nv, dV, lddv,
+                                                                  c->stream); }, "lb_reverse");
+    } while (0);
+    if (dT2) c->release(dT2);
+    if (dT1) c->release(dT1);
+    if (dvrev) c->release(dvrev);
+    return s;
+}
+
 fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx,
                                int m, int block_width, float* Y, int64_t ldy,
                                fasth_svd_tape* tape) {
@@ -1407,6 +1477,10 @@ fasth_status fasth_svd_plan_create(fasth_ctx c, const fasth_svd_param* p, int m,
     pl->in_dim = p->in_dim;
     pl->m = m;
     pl->b = block_width;
+    if (svd_large_batch(p, m)) {  // the large-batch step builds its WY blocks inside the forward
+        *out = pl;
+        return FASTH_OK;
+    }
     const fasthb::lb::Streams* side = on_side_stream ? c->svd_streams() : nullptr;
     cudaStream_t main_stream = c->stream;
     fasth_status s = FASTH_OK;
@@ -1466,6 +1540,12 @@ fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_p
     do {
         s = c->alloc_n((size_t)p->in_dim * std::max(m, 1), &st->T1);
         if (s) break;
+        if (svd_large_batch(p, m)) {
+            if (plan) plan->used = true;  // large-batch plans carry no blocks
+            s = lb_svd_forward(c, p, X, ldx, m, block_width, Y, ldy, st);
+            if (s == FASTH_OK) s = c->finish();
+            break;
+        }
         if (plan) {  // prepared blocks: take the plan's tapes, join its side-stream builds
             st->v = plan->v;
             st->u = plan->u;
@@ -1542,6 +1622,10 @@ fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd
     if (dX) TRY(check_mat("svd_backward: dX", dX, lddx, p->in_dim, m));
     if (dU) TRY(check_mat("svd_backward: dU", dU, lddu, p->out_dim, p->nu));
     if (dV) TRY(check_mat("svd_backward: dV", dV, lddv, p->in_dim, p->nv));
+    if (m > 0 && st->u && st->u->lb_ws && st->v && st->v->lb_ws) {
+        TRY(lb_svd_backward(c, p, st, G, ldg, dX, lddx, dU, lddu, dV, lddv, dsigma));
+        return c->finish();
+    }
     float* dT2 = nullptr;
     TRY(c->alloc_n((size_t)p->out_dim * std::max(m, 1), &dT2));
     fasth_status s = FASTH_OK;
@@ -1616,7 +1700,8 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
         fasth_svd_tape_destroy(st);
         return s;
     };
-    if (!square || getenv("FASTH_SVD_FUSED") && atoi(getenv("FASTH_SVD_FUSED")) == 0) return two_calls();
+    if (!square || svd_large_batch(p, m) || (getenv("FASTH_SVD_FUSED") && atoi(getenv("FASTH_SVD_FUSED")) == 0))
+        return two_calls();
     const int d = p->in_dim, k = std::min(p->out_dim, p->in_dim);
     fasth_tape tv = nullptr, tu = nullptr;
     float *T1 = nullptr, *dT2 = nullptr;

@@ -137,6 +137,9 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
                              Timer* tm = nullptr, const Streams* st = nullptr, DvNotify* nt = nullptr);
 
 // Elementwise helpers (lb_path.cu).
+// dst vector i = src vector n-1-i (d-float vectors, leading dims lds / ldd):
+// the SVD layer's V^T leg is the V chain in reverse order
+cudaError_t reverse_vectors(const float* src, int64_t lds, int d, int n, float* dst, int64_t ldd, cudaStream_t s);
 // split rows x cols (ld_in) into hi/lo (ld_out)
 // (trunc: the (x, x - trunc_tf32(x)) form, see Gemm::split_trunc)
 cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, float* lo,

@@ -64,6 +64,15 @@ __global__ void split_t_kernel(const float* __restrict__ v, int64_t ldv, int n, 
     }
 }
 
+// dst vector i = src vector n-1-i (vectors are the d-float columns)
+__global__ void reverse_vectors_kernel(const float* __restrict__ src, int64_t lds, int d, int n,
+                                       float* __restrict__ dst, int64_t ldd) {
+    const int i = blockIdx.y;
+    const float* a = src + (int64_t)(n - 1 - i) * lds;
+    float* b = dst + (int64_t)i * ldd;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < d; k += gridDim.x * blockDim.x) b[k] = a[k];
+}
+
 int grid_for(int64_t work) {
     return (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
 }
@@ -82,6 +91,12 @@ cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, fl
             reinterpret_cast<float4*>(lo), ldo / 4, trunc);
     else
         split_kernel<<<grid_for((int64_t)rows * cols), 256, 0, s>>>(x, ldx, rows, cols, hi, lo, ldo, trunc);
+    return cudaGetLastError();
+}
+
+cudaError_t reverse_vectors(const float* src, int64_t lds, int d, int n, float* dst, int64_t ldd, cudaStream_t s) {
+    if (n <= 0 || d <= 0) return cudaSuccess;
+    reverse_vectors_kernel<<<dim3((d + 255) / 256, n), 256, 0, s>>>(src, lds, d, n, dst, ldd);
     return cudaGetLastError();
 }
 

@@ -298,3 +298,68 @@ def test_dv_buckets_nccl_allreduce_single_rank(monkeypatch):
         assert torch.equal(back.grad_vectors, ref)
     finally:
         dist.destroy_process_group()
+
+
+def svd_model64(U, V, s, X, G, B=64):
+    """The SVD layer (svd_layer.hpp:106-147) in float64 torch on model64:
+    T1 = rev(V) chain X, T2 = Sigma T1, Y = U chain T2; backward in reverse."""
+    out_dim, in_dim = U.shape[1], V.shape[1]
+    k = min(out_dim, in_dim)
+    m = X.shape[1]
+    Vr = V.flip(0)
+    T1, _, _ = model64(Vr, X, torch.zeros_like(X), B)
+    T2 = torch.zeros(out_dim, m, dtype=torch.float64, device=X.device)
+    T2[:k] = s[:k, None].double() * T1[:k]
+    Y, dT2, dU = model64(U, T2, G, B)
+    ds = (dT2[:k] * T1[:k]).sum(1)
+    dT1 = torch.zeros(in_dim, m, dtype=torch.float64, device=X.device)
+    dT1[:k] = s[:k, None].double() * dT2[:k]
+    _, dX, dVr = model64(Vr, X, dT1, B)
+    return Y, dX, dU, dVr.flip(0), ds
+
+
+@pytest.mark.parametrize("out_dim,in_dim,m", [(1024, 1024, 1024), (768, 512, 1100), (512, 1024, 1024)])
+def test_large_batch_svd_layer(out_dim, in_dim, m, monkeypatch):
+    """SVD layer with both legs on the large-batch path (V^T leg on a
+    vector-reversed copy of V, Sigma materialised between the legs): the
+    two-call, one-call and planned entry points against the float64 model
+    and against the chain-kernel layer."""
+    from paper_2009_13977_b200 import fasth as fb
+    g = torch.Generator(device="cuda").manual_seed(out_dim + in_dim + m)
+    U = torch.randn(out_dim, out_dim, device="cuda", generator=g)
+    V = torch.randn(in_dim, in_dim, device="cuda", generator=g)
+    k = min(out_dim, in_dim)
+    s = torch.rand(k, device="cuda", generator=g) * 1.5 + 0.5
+    X = torch.randn(m, in_dim, device="cuda", generator=g).t()
+    G = torch.randn(m, out_dim, device="cuda", generator=g).t()
+    p = fb.SvdParam(out_dim, in_dim, U, V, s)
+    want = svd_model64(U, V, s, X, G)
+
+    def grads(gr):
+        return (gr.grad_input, gr.grad_U_vectors, gr.grad_V_vectors, gr.grad_sigma)
+
+    monkeypatch.setenv("FASTH_LB", "1")
+    ctx = fb.Context(0)
+    n0 = ctx.launch_count
+    Y1, t1 = fb.svd_forward(p, X, 32, ctx=ctx)
+    g1 = fb.svd_backward(p, t1, G)
+    launches = ctx.launch_count - n0
+    Y2, g2 = fb.svd_forward_backward(p, X, G, 32, ctx=ctx)
+    Y3, t3 = fb.svd_forward(p, X, 32, ctx=ctx, plan=fb.svd_plan(p, m, 32, ctx=ctx))
+    g3 = fb.svd_backward(p, t3, G)
+    monkeypatch.setenv("FASTH_LB", "0")
+    Y0, t0 = fb.svd_forward(p, X, 32)
+    g0 = fb.svd_backward(p, t0, G)
+    torch.cuda.synchronize()
+    assert launches > 40, launches  # both legs ran the multi-kernel large-batch step
+    got = (Y1,) + grads(g1)
+    errs = [rel(a, w) for a, w in zip(got, want)]
+    print(f"svd {out_dim}x{in_dim} m={m}: rel err Y/dX/dU/dV/ds " + " ".join(f"{e:.2e}" for e in errs)
+          + f", {launches} launches")
+    assert max(errs) <= TOL, errs
+    for a, b in zip(got, (Y2,) + grads(g2)):
+        assert torch.equal(a, b)
+    for a, b in zip(got, (Y3,) + grads(g3)):
+        assert torch.equal(a, b)
+    for a, b in zip(got, (Y0,) + grads(g0)):
+        assert rel(a, b.double()) <= TOL
