@@ -1112,11 +1112,13 @@ fasth_status lb_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, 
     OutBuf y{c, Y, ldy};
     if (s == FASTH_OK) s = y.open(d, m);
     int nl = 1;
+    LbTimer lt(c);
     if (s == FASTH_OK)
         s = c->timed(
             [&] {
                 return fasthb::lb::forward(V, ldv, d, n, X, ldx, m, y.ptr(), y.pitch(d), t->lb_ws, c->err_d,
-                                           c->stream, c->num_sms, &nl, nullptr, c->lb_streams());
+                                           c->stream, c->num_sms, &nl, c->timing == 1 ? &lt : nullptr,
+                                           c->lb_streams());
             },
             "large_batch(fwd)");
     c->launches += nl - 1;
@@ -1186,12 +1188,14 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
         OutBuf dx{c, dX, lddx};
         TRY(dx.open(d, m));
         int nl = 1;
+        LbTimer lt(c);
         fasthb::lb::DvNotify nt;
         fasthb::lb::DvNotify* ntp = dV ? c->dv_notify(nt) : nullptr;
         TRY(c->timed(
             [&] {
                 return fasthb::lb::backward(d, n, m, G, ldg, dx.ptr(), dx.pitch(d), dV, lddv, t->lb_ws, c->stream,
-                                            c->num_sms, &nl, nullptr, c->lb_streams(), false, ntp);
+                                            c->num_sms, &nl, c->timing == 1 ? &lt : nullptr, c->lb_streams(),
+                                            false, ntp);
             },
             "large_batch(bwd)"));
         if (ntp) c->dv_used = nt.used;

@@ -53,6 +53,42 @@ __global__ void dsigma_kernel(const float* __restrict__ dT2, int64_t ld2,
     dsigma[i] = (float)acc;
 }
 
+// Large batches: 32 rows per CTA, the batch split into DSW contiguous column
+// ranges (one warp each, coalesced 128 B row segments per column), f64
+// partials combined in warp order (deterministic).
+constexpr int DSW = 32;
+__global__ void __launch_bounds__(32 * DSW) dsigma_wide_kernel(const float* __restrict__ dT2, int64_t ld2,
+                                                              const float* __restrict__ T1, int64_t ld1, int k,
+                                                              int m, float* dsigma) {
+    __shared__ double part[DSW][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int i = blockIdx.x * 32 + lane;
+    const int per = (m + DSW - 1) / DSW;
+    const int l0 = min(m, w * per), l1 = min(m, l0 + per);
+    double acc = 0.0;
+    if (i < k) {
+        int l = l0;
+        for (; l + 4 <= l1; l += 4) {
+            float a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                a[u] = __ldg(dT2 + (int64_t)(l + u) * ld2 + i);
+                b[u] = __ldg(T1 + (int64_t)(l + u) * ld1 + i);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc += (double)a[u] * b[u];
+        }
+        for (; l < l1; ++l) acc += (double)dT2[(int64_t)l * ld2 + i] * T1[(int64_t)l * ld1 + i];
+    }
+    part[w][lane] = acc;
+    __syncthreads();
+    if (w == 0 && i < k) {
+        double t = 0.0;
+        for (int u = 0; u < DSW; ++u) t += part[u][lane];
+        dsigma[i] = (float)t;
+    }
+}
+
 __global__ void step_kernel(const float* __restrict__ P, int64_t ldp, const float* __restrict__ dP,
                             int64_t lddp, int dim, float eta, float* out, int64_t ldo,
                             ErrWord* err, int tag) {
@@ -148,7 +184,10 @@ cudaError_t launch_scale_rows(const float* x, int64_t ldx, int n_valid, const fl
 cudaError_t launch_dsigma(const float* dT2, int64_t ld2, const float* T1, int64_t ld1, int k,
                           int m, float* dsigma, cudaStream_t s) {
     if (k == 0) return cudaSuccess;
-    dsigma_kernel<<<(k + 127) / 128, 128, 0, s>>>(dT2, ld2, T1, ld1, k, m, dsigma);
+    if (m >= 512)  // one thread per row would leave most SMs idle for a long sequential sum
+        dsigma_wide_kernel<<<(k + 31) / 32, 32 * DSW, 0, s>>>(dT2, ld2, T1, ld1, k, m, dsigma);
+    else
+        dsigma_kernel<<<(k + 127) / 128, 128, 0, s>>>(dT2, ld2, T1, ld1, k, m, dsigma);
     return cudaGetLastError();
 }
 
