@@ -331,6 +331,12 @@ struct fasth_svd_tape_s {
     float* T1 = nullptr;     // V^T X, in_dim x m
 };
 
+// defined in the extern "C" block below (large-batch path selection)
+extern "C" bool use_large_batch(int d, int n, int m);
+extern "C" fasth_status lb_apply_chain(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int reversed,
+                                      const float* X, int64_t ldx, int n_valid, const float* scale, int m,
+                                      float* Y, int64_t ldy);
+
 namespace {
 
 void free_plan(fasth_ctx c, Plan& p) {
@@ -823,6 +829,7 @@ fasth_status apply_chain(fasth_ctx c, const float* V, int64_t ldv, int d, int n,
             return c->timed([&] { return launch_scale_rows(X, ldx, n_valid, scale, d, m, Y, ldy, 0, c->stream); }, "scale_rows");
         return copy_cols(c, X, ldx, Y, ldy, d, m);
     }
+    if (use_large_batch(d, n, m)) return lb_apply_chain(c, V, ldv, d, n, reversed, X, ldx, n_valid, scale, m, Y, ldy);
     fasth_tape t = nullptr;
     TRY(new_tape(c, V, ldv, d, n, m, b, reversed, tag, &t));
     t->scale = scale;
@@ -1092,6 +1099,55 @@ fasth_status run_large_batch(fasth_ctx c, const float* V, int64_t ldv, int d, in
     if (s == FASTH_OK) s = dx.close(d, m);
     c->release(ws);  // pool reuse is stream ordered
     if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
+// apply_chain on the large-batch path (the Sigma-ops at large batch): a
+// reversed chain runs on a vector-reversed copy of V, Sigma-scaled input rows
+// are materialised first; forward only.
+fasth_status lb_apply_chain(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int reversed, const float* X,
+                            int64_t ldx, int n_valid, const float* scale, int m, float* Y, int64_t ldy) {
+    float *vr = nullptr, *xs = nullptr, *ws = nullptr;
+    fasth_status s = FASTH_OK;
+    OutBuf y{c, Y, ldy};
+    do {
+        if (reversed) {
+            s = c->alloc_n((size_t)d * n, &vr);
+            if (s) break;
+            s = c->timed([&] { return fasthb::lb::reverse_vectors(V, ldv, d, n, vr, d, c->stream); }, "lb_reverse");
+            if (s) break;
+            V = vr;
+            ldv = d;
+        }
+        if (scale || n_valid < d) {
+            s = c->alloc_n((size_t)d * m, &xs);
+            if (s) break;
+            s = c->timed([&] { return launch_scale_rows(X, ldx, n_valid, scale, d, m, xs, d, 0, c->stream); },
+                         "scale_rows");
+            if (s) break;
+            X = xs;
+            ldx = d;
+        }
+        s = c->alloc_n(fasthb::lb::workspace_floats(d, n, m, false), &ws);
+        if (s) break;
+        s = y.open(d, m);
+        if (s) break;
+        int nl = 1;
+        LbTimer lt(c);
+        s = c->timed(
+            [&] {
+                return fasthb::lb::forward(V, ldv, d, n, X, ldx, m, y.ptr(), y.pitch(d), ws, c->err_d, c->stream,
+                                           c->num_sms, &nl, c->timing == 1 ? &lt : nullptr, c->lb_streams());
+            },
+            "large_batch(fwd)");
+        c->launches += nl - 1;
+        c->after_stream_wait = true;
+        if (s) break;
+        s = y.close(d, m);
+    } while (0);
+    if (vr) c->release(vr);  // pool reuse is stream ordered
+    if (xs) c->release(xs);
+    if (ws) c->release(ws);
     return s;
 }
 

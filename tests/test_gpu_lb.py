@@ -363,3 +363,39 @@ def test_large_batch_svd_layer(out_dim, in_dim, m, monkeypatch):
         assert torch.equal(a, b)
     for a, b in zip(got, (Y0,) + grads(g0)):
         assert rel(a, b.double()) <= TOL
+
+
+@pytest.mark.parametrize("op", ["inverse", "exponential", "cayley"])
+def test_large_batch_sigma_ops(op, monkeypatch):
+    """Sigma-ops (matops.hpp:43-117) at large batch: both chain applications
+    on the large-batch forward (reversed U^T leg on a reversed copy, f(Sigma)
+    rows materialised) against the float64 model and the chain kernels."""
+    from paper_2009_13977_b200 import fasth as fb
+    d, m = 1024, 2048
+    g = torch.Generator(device="cuda").manual_seed(21)
+    U = torch.randn(d, d, device="cuda", generator=g)
+    s = torch.rand(d, device="cuda", generator=g) * 0.5 + 0.5
+    X = torch.randn(m, d, device="cuda", generator=g).t()
+    if op == "inverse":
+        V = torch.randn(d, d, device="cuda", generator=g)
+        fs = 1.0 / s.double()
+    else:
+        V = torch.empty(0, d, device="cuda")
+        fs = torch.exp(s.double()) if op == "exponential" else (1 - s.double()) / (1 + s.double())
+    p = fb.SvdParam(d, d, U, V, s)
+    fn = getattr(fb, "apply_" + op)
+    Z = torch.zeros(d, m, dtype=torch.float64, device="cuda")
+    T = model64(U.flip(0), X, Z, 64)[0]
+    want = model64(V if op == "inverse" else U, fs[:, None] * T, Z, 64)[0]
+    monkeypatch.setenv("FASTH_LB", "1")
+    ctx = fb.Context(0)
+    n0 = ctx.launch_count
+    Y1 = fn(p, X, 32, ctx=ctx)
+    launches = ctx.launch_count - n0
+    monkeypatch.setenv("FASTH_LB", "0")
+    Y0 = fn(p, X, 32, ctx=ctx)
+    torch.cuda.synchronize()
+    err = rel(Y1, want)
+    print(f"{op}: rel err {err:.2e}, {launches} launches")
+    assert launches > 20, launches
+    assert err <= TOL and rel(Y0, want) <= TOL
