@@ -54,3 +54,28 @@ def test_mlp_train_step_matches_oracle():
         assert relative_error(p.U.double().cpu().numpy(), U) <= 1e-4
         assert relative_error(p.V.double().cpu().numpy(), V) <= 1e-4
         assert relative_error(p.sigma.double().cpu().numpy(), s) <= 1e-4
+
+
+def test_mlp_train_step_large_batch_matches_chain_path(monkeypatch):
+    """The same training step at a batch that selects the large-batch path
+    for every layer leg (plans carry no blocks there) against the chain
+    kernels (FASTH_LB=0): loss and updated parameters within tolerance."""
+    import torch
+
+    from paper_2009_13977_b200 import mlp
+
+    cfg = mlp.MLPConfig(d=512, depth=2, block_width=32, eta=1e-3, lam=1e-3)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(cfg.d, 1024, device="cuda", generator=g)
+    target = torch.randn(cfg.d, 1024, device="cuda", generator=g)
+    out = {}
+    for lb in ("1", "0"):
+        monkeypatch.setenv("FASTH_LB", lb)
+        layers = mlp.random_layers(cfg, seed=5)
+        loss = float(mlp.train_step(layers, x, target, cfg))
+        out[lb] = (loss, layers)
+    (l1, a), (l0, b) = out["1"], out["0"]
+    assert abs(l1 - l0) <= 1e-4 * abs(l0)
+    rel = lambda u, v: float((u.double() - v.double()).norm() / v.double().norm())
+    for p, q in zip(a, b):
+        assert rel(p.U, q.U) <= 1e-4 and rel(p.V, q.V) <= 1e-4 and rel(p.sigma, q.sigma) <= 1e-4
