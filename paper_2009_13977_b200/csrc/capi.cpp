@@ -176,9 +176,12 @@ struct fasth_ctx_s {
     HostGraphKey host_key;
     std::vector<void*> host_bufs;
     int64_t host_launches = 0;
+    cudaStream_t host_stream = nullptr;  // host-buffer entry on the legacy stream (fasth_forward_backward_host)
+    cudaEvent_t host_ev = nullptr;
     void drop_host_graph() {
         if (!host_exec && graph_held.empty() && host_bufs.empty()) return;
         cudaStreamSynchronize(stream);
+        if (host_stream) cudaStreamSynchronize(host_stream);
         if (host_exec) cudaGraphExecDestroy(host_exec);
         host_exec = nullptr;
         std::vector<void*> held;
@@ -897,6 +900,11 @@ fasth_status fasth_ctx_destroy(fasth_ctx c) {
     if (!c) return FASTH_OK;
     c->drop_host_graph();
     cudaStreamSynchronize(c->stream);
+    if (c->host_stream) {
+        cudaStreamSynchronize(c->host_stream);
+        cudaStreamDestroy(c->host_stream);
+        cudaEventDestroy(c->host_ev);
+    }
     for (auto& kv : c->free_list)
         for (void* p : kv.second) cudaFree(p);
     for (auto& kv : c->live) cudaFree(kv.first);
@@ -1373,10 +1381,8 @@ fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, 
 
 }  // namespace
 
-fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int n,
-                                         const float* X, const float* G, int m, int block_width,
-                                         float* Y, float* dX, float* dV) {
-    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+fasth_status host_step_impl(fasth_ctx c, const float* V, int d, int n, const float* X, const float* G, int m,
+                            int block_width, float* Y, float* dX, float* dV) {
     if (d < 1 || n < 0 || m < 0) return fail(FASTH_ERR_DIMENSION, "bad shape");
     const size_t nv = (size_t)d * n, nx = (size_t)d * m;
     const int saved = c->check_mode;
@@ -1443,6 +1449,30 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
     if (s == FASTH_OK) s = h;
     for (float* p : bufs) c->release(p);
     return s;
+}
+
+fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int n,
+                                         const float* X, const float* G, int m, int block_width,
+                                         float* Y, float* dX, float* dV) {
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    // The call is synchronous (host buffers in and out).  On the legacy
+    // default stream (which cannot be captured into the cached graph) it
+    // runs on a context-owned stream ordered after the legacy stream's work.
+    cudaStream_t user = c->stream;
+    if (user == nullptr || user == cudaStreamLegacy) {
+        if (!c->host_stream) {
+            CU(cudaStreamCreateWithFlags(&c->host_stream, cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&c->host_ev, cudaEventDisableTiming));
+        }
+        CU(cudaEventRecord(c->host_ev, user));
+        CU(cudaStreamWaitEvent(c->host_stream, c->host_ev, 0));
+        c->stream = c->host_stream;
+        c->after_stream_wait = true;
+        fasth_status s = host_step_impl(c, V, d, n, X, G, m, block_width, Y, dX, dV);
+        c->stream = user;
+        return s;
+    }
+    return host_step_impl(c, V, d, n, X, G, m, block_width, Y, dX, dV);
 }
 
 // ---- SVD layer -------------------------------------------------------------

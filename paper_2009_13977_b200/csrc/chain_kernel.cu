@@ -237,8 +237,16 @@ __global__ void __launch_bounds__(NT, 1) sweep_kernel(SweepArgs a) {
         // ([slot][source CTA][M tile][lane][4]): one 16-byte push per peer
         const uint32_t off = (uint32_t)((((slot * C + (int)rank) * MT + mt) * 32 + lane) * 16);
         const uint32_t bar = exb_local + slot * 8;
-        for (int dst = kc; dst < C; dst += KS)
-            dev::st_async_f32x4(dev::mapa(zr_local + off, dst), v.x, v.y, v.z, v.w, dev::mapa(bar, dst));
+        if (C == 1) {  // st.async needs a peer CTA: local store + completion on the own barrier
+            if (kc == 0) {
+                const float w[4] = {v.x, v.y, v.z, v.w};
+                dev::put4_local(zr_local + off, w);
+                dev::complete_tx_local(bar, 16u);
+            }
+        } else {
+            for (int dst = kc; dst < C; dst += KS)
+                dev::st_async_f32x4(dev::mapa(zr_local + off, dst), v.x, v.y, v.z, v.w, dev::mapa(bar, dst));
+        }
     };
 
     // debug phase trace (FASTH_TRACE): clock64 per phase.  Slots: 0 top,

@@ -234,10 +234,16 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             const int slot = s % NSLOTV;
             const uint32_t off = zr_u32 + (uint32_t)((((slot * C + (int)rank) * MT) * 128 + lane * 4) * 4);
             const uint32_t rbar_l = exb_u32 + 8u * slot;
-            for (int dst = warp; dst < C; dst += NR) {
-                const uint32_t rz = dev::mapa(off, dst), rb = dev::mapa(rbar_l, dst);
+            if (C == 1) {
 #pragma unroll
-                for (int mt = 0; mt < MT; ++mt) push4(rz + mt * 512u, sum[mt], rb);
+                for (int mt = 0; mt < MT; ++mt) dev::put4_local(off + mt * 512u, sum[mt]);
+                dev::complete_tx_local(rbar_l, (uint32_t)MT * 16u);
+            } else {
+                for (int dst = warp; dst < C; dst += NR) {
+                    const uint32_t rz = dev::mapa(off, dst), rb = dev::mapa(rbar_l, dst);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) push4(rz + mt * 512u, sum[mt], rb);
+                }
             }
         }
     };

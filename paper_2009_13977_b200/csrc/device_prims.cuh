@@ -125,6 +125,22 @@ __device__ __forceinline__ void st_async_f32x2(uint32_t raddr, float a, float b,
         : "memory");
 }
 
+// DSMEM push to the executing CTA itself when the cluster has one CTA (st.async
+// needs a peer): plain shared stores, then this lane's bytes are completed on
+// the barrier behind a CTA fence (release pattern), as st.async would.
+__device__ __forceinline__ void put4_local(uint32_t addr, const float (&v)[4]) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(__float_as_uint(v[0])),
+                 "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3]))
+                 : "memory");
+}
+__device__ __forceinline__ void complete_tx_local(uint32_t bar, uint32_t bytes) {
+    asm volatile(
+        "fence.acq_rel.cta;\n"
+        "mbarrier.complete_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(bar),
+        "r"(bytes)
+        : "memory");
+}
+
 __device__ __forceinline__ void st_async_f32x4(uint32_t raddr, float a, float b, float c, float d,
                                                uint32_t rbar) {
     asm volatile(
