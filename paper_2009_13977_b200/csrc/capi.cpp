@@ -1035,6 +1035,19 @@ bool vec_ok(const float* p, int64_t ld) { return !p || ((ld % 4) == 0 && !(reint
 
 // Output `out` (d x m, column-major, ld) through a packed temporary when the
 // epilogue's 16-byte stores cannot write it in place.
+// dV bucket events (fasth_ctx_set_dv_events) describe the caller's dV in
+// fasth_backward / fasth_forward_backward; internal calls that compute dV into
+// temporaries (SVD legs, the host entry, the tuner) run with them switched off.
+struct DvEventsOff {
+    fasth_ctx c;
+    std::vector<cudaEvent_t> saved;
+    explicit DvEventsOff(fasth_ctx cx) : c(cx) { saved.swap(c->dv_events); }
+    ~DvEventsOff() {
+        c->dv_events.swap(saved);
+        c->dv_used = 0;
+    }
+};
+
 struct OutBuf {
     fasth_ctx c;
     float* user;
@@ -1455,6 +1468,7 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
                                          const float* X, const float* G, int m, int block_width,
                                          float* Y, float* dX, float* dV) {
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    DvEventsOff no_buckets(c);  // dV comes back in host memory
     // The call is synchronous (host buffers in and out).  On the legacy
     // default stream (which cannot be captured into the cached graph) it
     // runs on a context-owned stream ordered after the legacy stream's work.
@@ -1518,6 +1532,7 @@ fasth_status lb_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd_ta
                              int64_t lddv, float* dsigma) {
     const int m = st->m, k = st->k;
     float *dT2 = nullptr, *dT1 = nullptr, *dvrev = nullptr;
+    DvEventsOff no_buckets(c);  // the legs below write temporaries, not the caller's dV
     fasth_status s = c->alloc_n((size_t)p->out_dim * m, &dT2);
     do {
         if (s) break;
@@ -2127,6 +2142,7 @@ fasth_status fasth_tune_block_width(fasth_ctx c, int d, int m, int timed, uint64
         *out = std::max(1, (int)std::lround(std::sqrt((double)d)));
         return FASTH_OK;
     }
+    DvEventsOff no_buckets(c);  // timing runs write scratch gradients
     static std::mutex mu;
     static std::map<std::pair<int, int>, int> cache;
     {

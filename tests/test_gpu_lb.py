@@ -399,3 +399,28 @@ def test_large_batch_sigma_ops(op, monkeypatch):
     print(f"{op}: rel err {err:.2e}, {launches} launches")
     assert launches > 20, launches
     assert err <= TOL and rel(Y0, want) <= TOL
+
+
+def test_dv_buckets_not_reported_for_internal_dv(monkeypatch):
+    """Bucket events describe the caller's dV of fasth_backward /
+    fasth_forward_backward only: the SVD legs (temporaries) and the host
+    entry (dV returned in host memory) report no buckets."""
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.setenv("FASTH_LB", "1")
+    d, m = 512, 1024
+    g = torch.Generator(device="cuda").manual_seed(31)
+    p = fb.SvdParam(d, d, torch.randn(d, d, device="cuda", generator=g), torch.randn(d, d, device="cuda", generator=g),
+                    torch.rand(d, device="cuda", generator=g) + 0.5)
+    X = torch.randn(m, d, device="cuda", generator=g).t()
+    G = torch.randn(m, d, device="cuda", generator=g).t()
+    ctx = fb.Context(0)
+    ctx.set_dv_buckets(4)
+    fb.fasth_forward_backward(p.V, X, G, 32, ctx=ctx)
+    assert len(ctx.dv_buckets()) == 1  # d = 512: one 512-row block
+    _, t = fb.svd_forward(p, X, 32, ctx=ctx)
+    fb.svd_backward(p, t, G)
+    torch.cuda.synchronize()
+    assert ctx.dv_buckets() == []
+    Vh, Xh, Gh = p.V.cpu().pin_memory(), X.t().contiguous().cpu().pin_memory(), G.t().contiguous().cpu().pin_memory()
+    fb.forward_backward_host(Vh, Xh, Gh, 32, ctx=ctx)
+    assert ctx.dv_buckets() == []
