@@ -427,7 +427,14 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         if (tm) tm->end(s, "lb_build_tri_inv");
         LBTRY(cudaGetLastError());
     }
-    for (int w = 0; w < 2; ++w) {  // WfR = T V_j, WbR = T^T V_j  (B x d per block)
+    // WfR = T V_j, WbR = T^T V_j  (B x d per block); WbR is the backward's
+    // operand: on the second stream, beside WfR and the first forward block
+    if (two) {
+        LBTRY(cudaEventRecord(st->ev[3], s));
+        LBTRY(cudaStreamWaitEvent(sx, st->ev[3], 0));
+    }
+    for (int w = 0; w < 2; ++w) {
+        const cudaStream_t sw = w == 1 ? sx : s;
         Gemm g;
         g.M = B;
         g.N = d;
@@ -441,8 +448,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g.d_hi = w == 0 ? WfH : WbH;
         g.d_lo = w == 0 ? WfL : WbL;
         g.lds = d;
-        LB_GEMM(g, s, "lb_build_w");
+        LB_GEMM(g, sw, "lb_build_w");
     }
+    if (two) LBTRY(cudaEventRecord(st->ev[6], sx));
     // ---- forward: stage nb = split X; stage j = output of block j
     if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[1], 0));
     for (int j = nb - 1; j >= 0; --j) {
@@ -488,6 +496,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             LB_GEMM(g, s, "lb_f2_update");
         }
     }
+    if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[6], 0));  // join: WbR built
     if (nlaunch) *nlaunch = nl;
     return cudaGetLastError();
 }
