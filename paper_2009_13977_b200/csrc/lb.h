@@ -127,10 +127,12 @@ size_t workspace_floats(int d, int n, int m, bool want_dv);
 // called with g_split = true — the fused call)
 cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
                     int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
-                    Timer* tm = nullptr, const Streams* st = nullptr, const float* G = nullptr, int64_t ldg = 0);
+                    Timer* tm = nullptr, const Streams* st = nullptr, const float* G = nullptr, int64_t ldg = 0,
+                    bool* k1_pre = nullptr);
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
                      int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm = nullptr,
-                     const Streams* st = nullptr, bool g_split = false, DvNotify* nt = nullptr);
+                     const Streams* st = nullptr, bool g_split = false, DvNotify* nt = nullptr,
+                     bool k1_pre = false);
 cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, const float* G,
                              int64_t ldg, int m, float* Y, int64_t ldy, float* dX, int64_t lddx, float* dV,
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,

@@ -371,8 +371,9 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
 // forward stage for the backward half.
 cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, int64_t ldx, int m, float* Y,
                     int64_t ldy, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm,
-                    const Streams* st, const float* G, int64_t ldg) {
+                    const Streams* st, const float* G, int64_t ldg, bool* k1_pre) {
     int nl = 0;
+    if (k1_pre) *k1_pre = false;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
     if (Y && ((ldy % 4) || (reinterpret_cast<uintptr_t>(Y) & 15))) return cudaErrorInvalidValue;
@@ -450,6 +451,22 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g.lds = d;
         LB_GEMM(g, sw, "lb_build_w");
     }
+    // fused step (G given): the gradient chain's first product Zb_0 = G WbR_0^T
+    // needs only G and WbR, so it runs beside the forward chain (no split-K
+    // scratch at this batch: nothing shared with the main stream)
+    if (two && G && k1_pre && !b.ksc && !getenv("FASTH_LB_NO_EARLY_K1")) {
+        Gemm g;
+        g.M = m;
+        g.N = B;
+        g.seg[0].A = Operand{Gh[0], Gl[0], m, d, d};
+        g.seg[0].B = Operand{WbH, WbL, n, d, d};
+        g.seg[0].K = d;
+        g.d_hi = b.ZbTh2[0];
+        g.d_lo = b.ZbTl2[0];
+        g.lds = B;
+        LB_GEMM(g, sx, "lb_k1_zb");
+        *k1_pre = true;
+    }
     if (two) LBTRY(cudaEventRecord(st->ev[6], sx));
     // ---- forward: stage nb = split X; stage j = output of block j
     if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[1], 0));
@@ -504,7 +521,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
 // Backward chain and dV from the forward's workspace (same d, n, m).
 cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX, int64_t lddx, float* dV,
                      int64_t lddv, float* ws, cudaStream_t s, int num_sms, int* nlaunch, Timer* tm,
-                     const Streams* st, bool g_split, DvNotify* nt) {
+                     const Streams* st, bool g_split, DvNotify* nt, bool k1_pre) {
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
@@ -525,7 +542,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     int cur = 0;
     for (int j = 0; j < nb; ++j) {
         float *ZbTh = b.ZbTh2[j & 1], *ZbTl = b.ZbTl2[j & 1];
-        {
+        if (!(j == 0 && k1_pre)) {
             Gemm g;  // ZbT = G WbR_j^T, Zb = transpose
             g.split_scratch = b.ksc;
             g.split_scratch_floats = b.ksc_n;
@@ -640,8 +657,10 @@ cudaError_t forward_backward(const float* V, int64_t ldv, int d, int n, const fl
                              int64_t lddv, float* ws, ErrWord* err, cudaStream_t s, int num_sms, int* nlaunch,
                              Timer* tm, const Streams* st, DvNotify* nt) {
     int n1 = 0, n2 = 0;
-    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1, tm, st, G, ldg);
-    if (e == cudaSuccess) e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm, st, true, nt);
+    bool k1_pre = false;
+    cudaError_t e = forward(V, ldv, d, n, X, ldx, m, Y, ldy, ws, err, s, num_sms, &n1, tm, st, G, ldg, &k1_pre);
+    if (e == cudaSuccess)
+        e = backward(d, n, m, G, ldg, dX, lddx, dV, lddv, ws, s, num_sms, &n2, tm, st, true, nt, k1_pre);
     if (nlaunch) *nlaunch = n1 + n2;
     return e;
 }
