@@ -93,7 +93,9 @@ fasth_status fasth_ctx_trim(fasth_ctx ctx);
  * chain paths once after the whole dV.  fasth_ctx_dv_buckets copies up to
  * `max` row_end values of the last call and returns the bucket count (0: no
  * events recorded; -1: bad arguments).  Bucket bounds are known when the
- * call returns (before the device work completes). */
+ * call returns (before the device work completes).  The SVD layer, the
+ * host-buffer entry and the tuner compute dV into temporaries or host memory
+ * and record no buckets. */
 fasth_status fasth_ctx_set_dv_events(fasth_ctx ctx, void* const* events, int count);
 int fasth_ctx_dv_buckets(fasth_ctx ctx, int64_t* row_end, int max);
 
