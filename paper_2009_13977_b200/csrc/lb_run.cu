@@ -618,7 +618,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 }
             }
         }
-        {
+        if (j < nb - 1 || dX) {  // the last update only produces dX
             // block j-1's dV read the G buffer this update overwrites
             if (two && j > 0) LBTRY(cudaStreamWaitEvent(s, st->ev[4 + ((j - 1) & 1)], 0));
             Gemm g;  // G <- G - 2 ZbT VT_j^T
@@ -639,9 +639,10 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.d_lo = Gl[cur ^ 1];
             g.lds = d;
             g.split_trunc = true;
-            if (j == nb - 1) {
+            if (j == nb - 1) {  // dX only: no later block reads the split gradient
                 g.d_f32 = dX;
                 g.ldd = lddx;
+                g.d_hi = g.d_lo = nullptr;
             }
             LB_GEMM(g, s, "lb_k4_update");
         }

@@ -424,3 +424,23 @@ def test_dv_buckets_not_reported_for_internal_dv(monkeypatch):
     Vh, Xh, Gh = p.V.cpu().pin_memory(), X.t().contiguous().cpu().pin_memory(), G.t().contiguous().cpu().pin_memory()
     fb.forward_backward_host(Vh, Xh, Gh, 32, ctx=ctx)
     assert ctx.dv_buckets() == []
+
+
+def test_large_batch_without_dx(monkeypatch):
+    """dX not requested (NULL through the C ABI): the last gradient update is
+    skipped; Y and dV unchanged bit for bit."""
+    from paper_2009_13977_b200 import fasth as fb
+    monkeypatch.setenv("FASTH_LB", "1")
+    n = d = 1024
+    m = 1024
+    V, X, G = inputs(n, d, m, seed=41)
+    ctx = fb.Context(0)
+    Y0, b0 = fb.fasth_forward_backward(V, X, G, 32, ctx=ctx)
+    Y1 = torch.empty(m, d, device="cuda").t()
+    dV1 = torch.empty(n, d, device="cuda")
+    P = C.c_void_p
+    rc = ctx.lib.fasth_forward_backward(ctx.h, P(V.data_ptr()), d, d, n, P(X.data_ptr()), d, P(G.data_ptr()), d, m,
+                                        32, P(Y1.data_ptr()), d, None, d, P(dV1.data_ptr()), d)
+    torch.cuda.synchronize()
+    assert rc == 0
+    assert torch.equal(Y0, Y1) and torch.equal(b0.grad_vectors, dV1)
