@@ -101,7 +101,7 @@ struct Timer {
 // block j runs), with reusable fork/join events.  nullptr: one stream.
 struct Streams {
     cudaStream_t aux = nullptr;
-    cudaEvent_t ev[12] = {};  // 0-7: large-batch step, 8-11: SVD layer legs (capi.cpp)
+    cudaEvent_t ev[16] = {};  // 0-7, 12-15: large-batch step, 8-11: SVD layer legs (capi.cpp)
 };
 
 // dV completion per row bucket (batch-sharded data parallelism, SURVEY

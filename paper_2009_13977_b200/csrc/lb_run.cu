@@ -273,9 +273,9 @@ size_t workspace_floats(int d, int n, int m, bool want_dv) {
     f += 4 * (size_t)nb * bb;       // T, T^T split
     f += 4 * nd;                    // WfR, WbR split
     f += 2 * (size_t)(nb + 1) * md;  // forward stages split
-    f += 2 * (size_t)m * B * 2;     // ZbT (x2) split
+    f += 2 * (size_t)m * B * 3;     // ZbT (x3) split
     f += 2 * (size_t)n * m;         // ZfT of all blocks (m x n) split
-    f += 4 * md;                    // two gradient buffers split
+    f += 6 * md;                    // three gradient buffers split
     (void)want_dv;                  // the forward carves the backward's buffers too
     f += 16 * bb + 3 * bb;          // Q partials, Q, S split
     f += 8 * (size_t)B * d;         // dV partials
@@ -300,7 +300,7 @@ struct Bufs {
     size_t nd = 0, md = 0, bb = 0;
     float *Vh, *Vl, *VTh, *VTl, *Gp, *Mm, *Dinv, *Th, *Tl, *TTh, *TTl, *WfH, *WfL, *WbH, *WbL;
     float *Sth[kMaxStages], *Stl[kMaxStages];
-    float *ZbTh2[2], *ZbTl2[2], *ZfAh, *ZfAl, *Gh[2], *Gl[2];  // ZfA: m x n, block j = columns jB..
+    float *ZbTh2[3], *ZbTl2[3], *ZfAh, *ZfAl, *Gh[3], *Gl[3];  // ZfA: m x n, block j = columns jB..
     float *Qp, *Qs, *Sh, *Sl, *dVp;
     float* ksc;  // split-K scratch of the small-batch chain products (m < 1024)
     int64_t ksc_n;
@@ -326,9 +326,9 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
         b.Sth[j] = c.take(md);
         b.Stl[j] = c.take(md);
     }
-    for (int i = 0; i < 2; ++i) b.ZbTh2[i] = c.take((size_t)m * B), b.ZbTl2[i] = c.take((size_t)m * B);
+    for (int i = 0; i < 3; ++i) b.ZbTh2[i] = c.take((size_t)m * B), b.ZbTl2[i] = c.take((size_t)m * B);
     b.ZfAh = c.take((size_t)m * n), b.ZfAl = c.take((size_t)m * n);
-    b.Gh[0] = c.take(md), b.Gh[1] = c.take(md), b.Gl[0] = c.take(md), b.Gl[1] = c.take(md);
+    for (int i = 0; i < 3; ++i) b.Gh[i] = c.take(md), b.Gl[i] = c.take(md);
     b.Qp = c.take(ksQ * bb);
     b.Qs = c.take(bb);
     b.Sh = c.take(bb);
@@ -530,18 +530,19 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     LB_ALIASES;
     cudaError_t e;
     // ---- backward.  Block j: K1 (Zb) on the main stream, then Q and dV of
-    // block j on the second stream while the main stream updates G (K4); Zb
-    // is double buffered, and K4 of block j+1 (which overwrites block j's G)
-    // waits for block j's dV.
+    // block j on the second stream while the main stream updates G (K4).  G
+    // and Zb are triple buffered (block j uses buffer j % 3), so the main
+    // stream runs up to two blocks ahead of the dV stream: K4 of block j
+    // (which overwrites buffer (j+1) % 3) waits only for block j-2's dV.
     if (!g_split) {
         ++nl;
         LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s, true));
     }
     const bool two = st && st->aux && want_dv;
     cudaStream_t sa = two ? st->aux : s;
-    int cur = 0;
     for (int j = 0; j < nb; ++j) {
-        float *ZbTh = b.ZbTh2[j & 1], *ZbTl = b.ZbTl2[j & 1];
+        const int cur = j % 3, nxt = (j + 1) % 3;
+        float *ZbTh = b.ZbTh2[cur], *ZbTl = b.ZbTl2[cur];
         if (!(j == 0 && k1_pre)) {
             Gemm g;  // ZbT = G WbR_j^T, Zb = transpose
             g.split_scratch = b.ksc;
@@ -607,7 +608,7 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             }
             ++nl;
             dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv, lddv);
-            if (two) LBTRY(cudaEventRecord(st->ev[4 + (j & 1)], sa));
+            if (two) LBTRY(cudaEventRecord(st->ev[12 + cur], sa));
             if (nt && nt->count > 0) {  // last block of its bucket: rows up to here are final
                 const int nbk = std::min(nt->count, nb);
                 const int bk = (int)((int64_t)j * nbk / nb);
@@ -619,8 +620,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             }
         }
         if (j < nb - 1 || dX) {  // the last update only produces dX
-            // block j-1's dV read the G buffer this update overwrites
-            if (two && j > 0) LBTRY(cudaStreamWaitEvent(s, st->ev[4 + ((j - 1) & 1)], 0));
+            // block j-2's dV read the G / Zb buffers this update and the next
+            // K1 overwrite
+            if (two && j >= 2) LBTRY(cudaStreamWaitEvent(s, st->ev[12 + (j - 2) % 3], 0));
             Gemm g;  // G <- G - 2 ZbT VT_j^T
             g.split_scratch = b.ksc;
             g.split_scratch_floats = b.ksc_n;
@@ -635,8 +637,8 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.c_hi = Gh[cur];
             g.c_single = true;
             g.ldc = d;
-            g.d_hi = Gh[cur ^ 1];
-            g.d_lo = Gl[cur ^ 1];
+            g.d_hi = Gh[nxt];
+            g.d_lo = Gl[nxt];
             g.lds = d;
             g.split_trunc = true;
             if (j == nb - 1) {  // dX only: no later block reads the split gradient
@@ -646,9 +648,8 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             }
             LB_GEMM(g, s, "lb_k4_update");
         }
-        cur ^= 1;
     }
-    if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[4 + ((nb - 1) & 1)], 0));  // join: dV complete
+    if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[12 + (nb - 1) % 3], 0));  // join: dV complete
     if (nlaunch) *nlaunch = nl;
     return cudaGetLastError();
 }
