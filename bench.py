@@ -25,9 +25,15 @@ Rows of the JSON line:
             headers compiled as-is) via bench::run_bench on all host threads.
 
 --impl reference times that CPU reference alone (rank 0 only) on the same
-config and prints the same line with "impl": "reference".
-N > 1 (torchrun): weak scaling, each rank runs the batch-32 step on its own
-shard and the summed dV is all-reduced over NCCL inside the timed step.
+config (the whole job's batch, 32 x N columns) and prints the same line with
+"impl": "reference".
+N > 1: weak scaling, each rank runs the batch-32 step on its own shard and the
+summed dV is all-reduced over NCCL inside the timed step.  Launched under
+torchrun (the driver's form) or directly as ``python bench.py --gpus N``, in
+which case it re-executes itself under torch.distributed.run with N ranks.
+The `config5` object is BASELINE configs[4] as the north_star states it:
+d = 2048, global batch 65536 sharded over the N ranks (strong scaling; the
+1-GPU point runs the whole batch).
 """
 from __future__ import annotations
 
@@ -148,25 +154,33 @@ def cpu_sequential(d, m, b, reps=8):
     return mean * 1e6, std * 1e6
 
 
+def headline_config(world):
+    """The `config` object of both arms (same keys, same values)."""
+    return {"workload": "FastH fwd+bwd op=mul (fasth_forward + fasth_backward, bench.hpp:147-151)",
+            "d": D, "n": D, "block_width": B, "batch_per_gpu": M, "global_batch": M * world,
+            "parallelism": f"batch-sharded dp{world}" if world > 1 else "single GPU"}
+
+
 def run_reference_impl(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    try:
-        us, std, cores, kind = cpu_reference(D, M, B, max(args.steps, 1), args.warmup)
+    world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
+    try:  # the whole job's batch (32 per GPU) on the host's cores
+        us, std, cores, kind = cpu_reference(D, M * world, B, max(args.steps, 1), args.warmup)
     except Exception as e:  # the reference always builds here; report, don't fake
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref failed: {e}"}))
         return
     line = {
-        "impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": us, "unit": "us/step", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us / 1e3,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference generator bench.hpp:117, seed 0)",
-        "config": {"workload": "FastH fwd+bwd op=mul", "d": D, "n": D, "block_width": B,
-                   "batch": M, "algo": "fasth (reference CPU, all host threads)"},
-        "tflops": flops_alg(D, D, M, B) / (us * 1e-6) / 1e12,
+        "config": headline_config(world),
+        "algo": "fasth (reference CPU, all host threads)",
+        "tflops": flops_alg(D, D, M * world, B) / (us * 1e-6) / 1e12,
         "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": kind,
-                         "sample": f"run_bench op=mul d={D} m={M} k={B} algo=fasth, "
+                         "sample": f"run_bench op=mul d={D} m={M * world} k={B} algo=fasth, "
                                    f"{args.steps} reps after warm-up (std {std:.1f} us)"},
         "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -218,18 +232,22 @@ def layer_line(local, steps=50, warmup=5):
             "data": "synthetic: normalised N(0,1) vectors, sigma ~ U(0.5, 2)"}
 
 
-def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
-    """BASELINE.json configs[4]: d = 2048 FastH fwd+bwd at 8192 columns per GPU
-    (weak: a 8192*world batch sharded by columns), dV all-reduced over NCCL
-    when world > 1.  Runs the tcgen05 large-batch path (lb.h).  Synthetic
-    N(0,1) inputs on the device; CUDA events around `steps` steps, max over
-    ranks; every step touches ~1.5 GB, so L2 (126 MB) holds nothing across
-    steps."""
+def large_batch_line(world, rank, local, peak_3xtf32, global_batch=65536, steps=10, warmup=3):
+    """BASELINE.json configs[4]: d = 2048 FastH fwd+bwd on a global batch of
+    65536 columns sharded over the ranks (strong scaling: 65536 on one GPU,
+    8192 per GPU on eight), dV all-reduced over NCCL when world > 1 (row
+    buckets overlapped with the backward).  Runs the tcgen05 large-batch path
+    (lb.h).  Synthetic N(0,1) inputs on the device; CUDA events around
+    `steps` steps, max over ranks; every step touches GBs, so L2 (126 MB)
+    holds nothing across steps."""
     import torch
     import torch.distributed as dist
 
     from paper_2009_13977_b200 import fasth as fb
-    d, b, m = 2048, 32, 8192
+    from paper_2009_13977_b200.sharding import shard_range
+    d, b = 2048, 32
+    lo, hi = shard_range(global_batch, world, rank)
+    m = hi - lo
     g = torch.Generator(device="cuda").manual_seed(0)
     V = torch.randn(d, d, device="cuda", generator=g)
     g.manual_seed(1000 + rank)
@@ -269,7 +287,7 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ctx.check()
-    flops = (12.0 * d * d * m + 4.0 * d * d * b) * world
+    flops = 12.0 * d * d * global_batch + 4.0 * d * d * b * world
     tf = flops / (ms * 1e-3) / 1e12
     # per-kernel: CUDA events around every launch of the large-batch path
     # (ctx timing mode), untimed steps, one stream (concurrent kernels would
@@ -304,14 +322,29 @@ def large_batch_line(world, rank, local, peak_3xtf32, steps=10, warmup=3):
             "flops_per_launch": fl[top],
             "note": "3xTF32 useful flops; CUDA events per launch on the context stream (kernels serialised "
                     "for this pass); ncu tensor-pipe activity of these GEMMs in profiles/r01_lb_*_full.txt"}
-    return {"workload": "BASELINE configs[4]: FastH fwd+bwd d=2048, batch-sharded, dV all-reduced (NCCL, "
-                        "4 row buckets overlapped with the backward)",
-            "roofline": roof, "kernels": kern,
-            "d": d, "batch_per_gpu": m, "global_batch": m * world, "n_gpus": world,
+    return {"workload": "BASELINE configs[4]: FastH fwd+bwd d=2048, global batch 65536 batch-sharded, dV "
+                        "all-reduced (NCCL, 4 row buckets overlapped with the backward)",
+            "scaling": "strong", "roofline": roof, "kernels": kern,
+            "d": d, "batch_per_gpu": m, "global_batch": global_batch, "n_gpus": world,
             "us_per_step": ms * 1e3, "tflops": tf, "frac_3xtf32_peak": tf / (peak_3xtf32 * world),
             "steps": steps, "warmup": warmup, "gpu_launches_per_step": launches,
             "path": "large-batch: 512-wide WY blocks on the tcgen05 3xTF32 GEMM (cta_group::2)",
             "data": "synthetic N(0,1) on device", "l2": "working set ~1.5 GB per step (> L2)"}
+
+
+def relaunch(args):
+    """`python bench.py --gpus N` outside torchrun: re-execute under
+    torch.distributed.run with N ranks on this node (the driver's form)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")        # NCCL's init log (rings / NVLS) stays visible on stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -323,10 +356,13 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=150, help="reps of the cpu_baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-config5", action="store_true", help="skip the large-batch (config 5) line")
+    ap.add_argument("--config5-batch", type=int, default=65536, help="config 5 global batch (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference_impl(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
 
     import numpy as np
     import torch
@@ -337,6 +373,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -393,9 +431,24 @@ def main():
             step()
     torch.cuda.synchronize()
     launches0 = ctx.launch_count
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=stream):
-        g_y, g_back = fb.fasth_forward_backward(Vd, Xd, Gd, B, ctx=ctx, out=(Yd, dXd, dVd))
+    # the NCCL all-reduce of dV is captured into the same graph (N > 1); if
+    # the capture is refused it stays eager after the replay
+    ar_in_graph = world > 1
+    try:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            g_y, g_back = fb.fasth_forward_backward(Vd, Xd, Gd, B, ctx=ctx, out=(Yd, dXd, dVd))
+            if ar_in_graph:
+                dist.all_reduce(g_back.grad_vectors)
+    except Exception:  # noqa: BLE001
+        if not ar_in_graph:
+            raise
+        torch.cuda.synchronize()
+        ar_in_graph = False
+        launches0 = ctx.launch_count
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            g_y, g_back = fb.fasth_forward_backward(Vd, Xd, Gd, B, ctx=ctx, out=(Yd, dXd, dVd))
     launches_per_step = ctx.launch_count - launches0
     torch.cuda.synchronize()
     # the same work as the reference's two calls (fasth_forward, then
@@ -429,7 +482,7 @@ def main():
                 flush.zero_()
                 ev[i][0].record(stream)
                 graph.replay()
-                if world > 1:
+                if world > 1 and not ar_in_graph:
                     dist.all_reduce(g_back.grad_vectors)
                 ev[i][1].record(stream)
         torch.cuda.synchronize()
@@ -551,13 +604,16 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": us_per_step / 1e3,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": f"synthetic ({src}, seed {SEED})",
-        "config": {"workload": "FastH fwd+bwd (fasth_forward + fasth_backward as fasth_forward_backward), op=mul",
-                   "d": D, "n": D, "block_width": B, "batch_per_gpu": M, "global_batch": M * world,
-                   "parallelism": f"batch-sharded dp{world}" if world > 1 else "single GPU",
-                   "l2": "flushed (256 MiB write) before every timed step",
-                   "timing": "CUDA graph replay, CUDA events on the launch stream"},
-        "tflops": flops_alg(D, D, M, B) / (us_per_step * 1e-6) / 1e12,
+        "config": headline_config(world),
+        "api": "fasth_forward_backward (fasth_forward + fasth_backward in one call, G known up front as in "
+               "bench.hpp:147-151)",
+        "timing": {"l2": "flushed (256 MiB write) before every timed step",
+                   "how": "CUDA graph replay, CUDA events on the launch stream, max over ranks"},
+        "tflops": flops_alg(D, D, M * world, B) / (us_per_step * 1e-6) / 1e12,
         "eager_us_per_step": eager_us,
+        "two_call": {"value": two_call_us, "unit": "us/step",
+                     "api": "fasth_forward then fasth_backward on its tape (the training-path call pair, "
+                            "fasth.hpp:40,69), CUDA graph, L2 flushed"},
         "two_call_us_per_step": two_call_us,
         "parity_max_rel_err": parity,
         "kernel_share": {k: round(v[0] / step_ms, 4) for k, v in ktimes.items()} if step_ms else {},
@@ -574,6 +630,8 @@ def main():
                 "timing": "host wall clock per call (median), copies and sync inside",
                 "api": "fasth_forward_backward_host (C ABI, pinned host buffers)"},
         "gpu_launches": launches_per_step * args.steps,
+        "allreduce": ("NCCL all-reduce(SUM) of dV captured in the step's CUDA graph" if ar_in_graph else
+                      "eager NCCL all-reduce(SUM) of dV after the graph replay") if world > 1 else None,
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
@@ -591,7 +649,7 @@ def main():
             line["config2_layer"] = {"unavailable": str(e)[:200]}
     if not args.no_config5:
         try:
-            line["config5"] = large_batch_line(world, rank, local, peak_3xtf32)
+            line["config5"] = large_batch_line(world, rank, local, peak_3xtf32, args.config5_batch)
         except Exception as e:  # noqa: BLE001 - the headline line must still print
             line["config5"] = {"unavailable": str(e)[:200]}
     if rank == 0:

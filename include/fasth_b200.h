@@ -63,9 +63,13 @@ int fasth_version(void);
 
 /* Context: one per (device, stream).  stream == NULL -> the legacy default
  * stream.  Replaces the reference's process-global worker count
- * (parallel.hpp:12-30): parallelism here is the grid. */
+ * (parallel.hpp:12-30): parallelism here is the grid.  Every call runs on the
+ * context's device whatever the calling thread's current device is. */
 fasth_status fasth_ctx_create(int device, void* stream, fasth_ctx* out);
 fasth_status fasth_ctx_destroy(fasth_ctx ctx);
+/* Rebind the context to another stream.  The new stream is ordered after all
+ * work already enqueued on the old one (one event), so pool buffers and tapes
+ * are never touched by two streams at once. */
 fasth_status fasth_ctx_set_stream(fasth_ctx ctx, void* stream);
 fasth_status fasth_ctx_set_check(fasth_ctx ctx, int mode);
 /* Synchronise the stream and report (then clear) latched device errors. */
@@ -193,7 +197,8 @@ fasth_status fasth_svd_forward_backward(fasth_ctx ctx, const fasth_svd_param* p,
                                         int64_t lddu, float* dV, int64_t lddv, float* dsigma);
 
 /* svd_step (svd_layer.hpp:158) fused with clamp_sigma (svd_layer.hpp:196)
- * when clamp_eps >= 0: v <- v - eta dv, sigma <- sigma - eta dsigma.
+ * when clamp_eps is in [0, 1) (-1: no clamp; any other value is rejected):
+ * v <- v - eta dv, sigma <- sigma - eta dsigma.
  * Outputs may alias the inputs (in-place update).  A vector whose updated
  * ||v||^2 <= 1e-30 raises FASTH_ERR_DEGENERATE naming the chain and index
  * (svd_layer.hpp:174-179); the outputs are then unspecified. */

@@ -176,6 +176,7 @@ struct fasth_ctx_s {
     HostGraphKey host_key;
     std::vector<void*> host_bufs;
     int64_t host_launches = 0;
+    cudaEvent_t switch_ev = nullptr;     // fasth_ctx_set_stream: old stream -> new stream ordering
     cudaStream_t host_stream = nullptr;  // host-buffer entry on the legacy stream (fasth_forward_backward_host)
     cudaEvent_t host_ev = nullptr;
     void drop_host_graph() {
@@ -333,6 +334,30 @@ struct fasth_svd_tape_s {
     fasth_tape u = nullptr;  // U leg; null if nu == 0
     float* T1 = nullptr;     // V^T X, in_dim x m
 };
+
+// Every entry point runs on its context's device, whatever the calling
+// thread's current device is, and restores the caller's device on return.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (dev < 0) return;
+        int cur = -1;
+        if (cudaGetDevice(&cur) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        if (cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+inline int dev_of(fasth_ctx c) { return c ? c->device : -1; }
+inline int dev_of(fasth_tape t) { return t && t->ctx ? t->ctx->device : -1; }
+inline int dev_of(fasth_svd_plan p) { return p && p->ctx ? p->ctx->device : -1; }
+inline int dev_of(fasth_svd_tape t) { return t && t->ctx ? t->ctx->device : -1; }
 
 // defined in the extern "C" block below (large-batch path selection)
 extern "C" bool use_large_batch(int d, int n, int m);
@@ -897,6 +922,7 @@ fasth_status fasth_ctx_create(int device, void* stream, fasth_ctx* out) {
 }
 
 fasth_status fasth_ctx_destroy(fasth_ctx c) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return FASTH_OK;
     c->drop_host_graph();
     cudaStreamSynchronize(c->stream);
@@ -912,6 +938,7 @@ fasth_status fasth_ctx_destroy(fasth_ctx c) {
     if (c->logdet_d) cudaFree(c->logdet_d);
 
     if (c->err_h) cudaFreeHost(c->err_h);
+    if (c->switch_ev) cudaEventDestroy(c->switch_ev);
     if (c->lb_st.aux) {
         cudaStreamDestroy(c->lb_st.aux);
         for (auto ev : c->lb_st.ev)
@@ -922,13 +949,33 @@ fasth_status fasth_ctx_destroy(fasth_ctx c) {
 }
 
 fasth_status fasth_ctx_set_stream(fasth_ctx c, void* stream) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
-    if (c->stream != static_cast<cudaStream_t>(stream)) c->drop_host_graph();
-    c->stream = static_cast<cudaStream_t>(stream);
+    cudaStream_t next = static_cast<cudaStream_t>(stream);
+    if (c->stream == next) return FASTH_OK;
+    c->drop_host_graph();
+    // The memory pool recycles a released buffer at once, assuming stream
+    // order; tapes are read by later calls.  Switching streams therefore
+    // orders the new stream after everything enqueued on the old one (one
+    // event), so no buffer or tape is reused or read while the old stream
+    // still works on it.  Not across a stream being captured into a graph
+    // (the capture owns the ordering there).
+    cudaStreamCaptureStatus a = cudaStreamCaptureStatusNone, b = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &a);
+    cudaStreamIsCapturing(next, &b);
+    cudaGetLastError();
+    if (a == cudaStreamCaptureStatusNone && b == cudaStreamCaptureStatusNone) {
+        if (!c->switch_ev) CU(cudaEventCreateWithFlags(&c->switch_ev, cudaEventDisableTiming));
+        CU(cudaEventRecord(c->switch_ev, c->stream));
+        CU(cudaStreamWaitEvent(next, c->switch_ev, 0));
+        c->after_stream_wait = true;
+    }
+    c->stream = next;
     return FASTH_OK;
 }
 
 fasth_status fasth_ctx_set_check(fasth_ctx c, int mode) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || (mode != FASTH_CHECK_SYNC && mode != FASTH_CHECK_DEFERRED))
         return fail(FASTH_ERR_INVALID, "bad check mode");
     c->check_mode = mode;
@@ -936,6 +983,7 @@ fasth_status fasth_ctx_set_check(fasth_ctx c, int mode) {
 }
 
 fasth_status fasth_ctx_check(fasth_ctx c) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     return c->harvest();
 }
@@ -943,17 +991,20 @@ fasth_status fasth_ctx_check(fasth_ctx c) {
 int64_t fasth_ctx_launch_count(fasth_ctx c) { return c ? c->launches : 0; }
 
 fasth_status fasth_device_alloc(fasth_ctx c, int64_t bytes, void** out) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !out || bytes < 0) return fail(FASTH_ERR_INVALID, "fasth_device_alloc: bad argument");
     return c->alloc((size_t)bytes, out);
 }
 
 fasth_status fasth_device_free(fasth_ctx c, void* ptr) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     c->release(ptr);
     return FASTH_OK;
 }
 
 fasth_status fasth_copy(fasth_ctx c, void* dst, const void* src, int64_t bytes, int kind) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || bytes < 0 || kind < 0 || kind > 2) return fail(FASTH_ERR_INVALID, "fasth_copy: bad argument");
     if (bytes == 0) return FASTH_OK;
     const cudaMemcpyKind k = kind == 0   ? cudaMemcpyHostToDevice
@@ -964,12 +1015,14 @@ fasth_status fasth_copy(fasth_ctx c, void* dst, const void* src, int64_t bytes, 
 }
 
 fasth_status fasth_ctx_synchronize(fasth_ctx c) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     CU(cudaStreamSynchronize(c->stream));
     return FASTH_OK;
 }
 
 fasth_status fasth_ctx_set_dv_events(fasth_ctx c, void* const* events, int count) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || count < 0 || (count > 0 && !events)) return fail(FASTH_ERR_INVALID, "fasth_ctx_set_dv_events: bad argument");
     c->dv_events.assign(reinterpret_cast<const cudaEvent_t*>(events), reinterpret_cast<const cudaEvent_t*>(events) + count);
     c->dv_row_end.assign(count, 0);
@@ -978,6 +1031,7 @@ fasth_status fasth_ctx_set_dv_events(fasth_ctx c, void* const* events, int count
 }
 
 int fasth_ctx_dv_buckets(fasth_ctx c, int64_t* row_end, int max) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || max < 0 || (max > 0 && !row_end)) return -1;
     const int k = std::min(max, c->dv_used);
     for (int i = 0; i < k; ++i) row_end[i] = c->dv_row_end[i];
@@ -985,6 +1039,7 @@ int fasth_ctx_dv_buckets(fasth_ctx c, int64_t* row_end, int max) {
 }
 
 fasth_status fasth_ctx_set_timing(fasth_ctx c, int mode) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || mode < 0 || mode > 2) return fail(FASTH_ERR_INVALID, "fasth_ctx_set_timing: bad argument");
     if (c->timing == 2)
         c->release_timing_events();
@@ -996,6 +1051,7 @@ fasth_status fasth_ctx_set_timing(fasth_ctx c, int mode) {
 }
 
 int fasth_ctx_kernel_times(fasth_ctx c, char* buf, int buflen) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !buf || buflen <= 0) return -1;
     c->collect_timing();
     std::string out;
@@ -1010,6 +1066,7 @@ int fasth_ctx_kernel_times(fasth_ctx c, char* buf, int buflen) {
 }
 
 fasth_status fasth_ctx_trim(fasth_ctx c) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return FASTH_OK;
     CU(cudaStreamSynchronize(c->stream));
     std::lock_guard<std::mutex> lk(c->mu);
@@ -1024,11 +1081,14 @@ fasth_status fasth_ctx_trim(fasth_ctx c) {
 // measured faster than the chain kernels (scripts/small_batch_probe.py, one
 // B200): m >= 1024 at d >= 512, m >= 128 at d >= 1024 (2.3-5x over the panel
 // sweep at d >= 2048), m >= 64 at d >= 4096; FASTH_LB=0/1 forces the choice.
-// Shapes must meet its alignment (n a multiple of 128, d and m of 4).
+// Any shape runs there (ragged ones on zero-padded dimensions, lb.h Dims), so
+// it also takes every d the chain kernels cannot hold (cluster of at most 16
+// CTAs x 256-row slabs: d > 4096) at any batch.
+constexpr int kChainMaxD = 4096;
 bool use_large_batch(int d, int n, int m) {
     if (!fasthb::lb::supported(d, n, m)) return false;
     if (const char* e = getenv("FASTH_LB")) return atoi(e) != 0;
-    return (m >= 1024 && d >= 512) || (m >= 128 && d >= 1024) || (m >= 64 && d >= 4096);
+    return (m >= 1024 && d >= 512) || (m >= 128 && d >= 1024) || (m >= 64 && d >= 4096) || d > kChainMaxD;
 }
 
 bool vec_ok(const float* p, int64_t ld) { return !p || ((ld % 4) == 0 && !(reinterpret_cast<uintptr_t>(p) & 15)); }
@@ -1212,6 +1272,7 @@ fasth_status lb_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, 
 fasth_status fasth_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int n, const float* X,
                            int64_t ldx, int m, int block_width, float* Y, int64_t ldy,
                            fasth_tape* tape) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     if (d < 1) return fail(FASTH_ERR_DIMENSION, "fasth_forward: chain dim must be >= 1");
     if (n < 0 || m < 0) return fail(FASTH_ERR_DIMENSION, "fasth_forward: negative shape");
@@ -1246,6 +1307,7 @@ fasth_status fasth_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int 
 
 fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, float* dX,
                             int64_t lddx, float* dV, int64_t lddv) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !t) return fail(FASTH_ERR_INVALID, "fasth_backward: null ctx or tape");
     const int d = t->plan.d, n = t->plan.n, m = t->m;
     c->dv_used = 0;
@@ -1287,11 +1349,13 @@ fasth_status fasth_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t l
 }
 
 fasth_status fasth_tape_destroy(fasth_tape t) {
+    DeviceGuard dg_(dev_of(t));
     free_tape(t);
     return FASTH_OK;
 }
 
 fasth_status fasth_tape_info(fasth_tape t, int* d, int* n, int* m, int* block_width, int* q) {
+    DeviceGuard dg_(dev_of(t));
     if (!t) return fail(FASTH_ERR_INVALID, "null tape");
     if (d) *d = t->plan.d;
     if (n) *n = t->plan.n;
@@ -1305,6 +1369,7 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
                                     const float* X, int64_t ldx, const float* G, int64_t ldg,
                                     int m, int block_width, float* Y, int64_t ldy, float* dX,
                                     int64_t lddx, float* dV, int64_t lddv) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     if (d < 1) return fail(FASTH_ERR_DIMENSION, "fasth_forward: chain dim must be >= 1");
     if (n < 0 || m < 0) return fail(FASTH_ERR_DIMENSION, "fasth_forward: negative shape");
@@ -1467,6 +1532,7 @@ fasth_status host_step_impl(fasth_ctx c, const float* V, int d, int n, const flo
 fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int n,
                                          const float* X, const float* G, int m, int block_width,
                                          float* Y, float* dX, float* dV) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     DvEventsOff no_buckets(c);  // dV comes back in host memory
     // The call is synchronous (host buffers in and out).  On the legacy
@@ -1493,10 +1559,12 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
 fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan, const float* X,
                               int64_t ldx, int m, int block_width, float* Y, int64_t ldy, fasth_svd_tape* tape);
 
-// Both legs on the large-batch path (same thresholds as fasth_forward).
+// Both legs on the large-batch path (same thresholds as fasth_forward; a leg
+// too tall for the chain kernels takes both there).
 bool svd_large_batch(const fasth_svd_param* p, int m) {
-    return m > 0 && p->nu > 0 && p->nv > 0 && use_large_batch(p->in_dim, p->nv, m) &&
-           use_large_batch(p->out_dim, p->nu, m);
+    if (m <= 0 || p->nu <= 0 || p->nv <= 0) return false;
+    const bool u = use_large_batch(p->out_dim, p->nu, m), v = use_large_batch(p->in_dim, p->nv, m);
+    return (u && v) || (u && p->out_dim > kChainMaxD) || (v && p->in_dim > kChainMaxD);
 }
 
 // Large-batch SVD layer forward (svd_layer.hpp:106-116): the V^T leg is the V
@@ -1567,11 +1635,13 @@ fasth_status lb_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd_ta
 fasth_status fasth_svd_forward(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx,
                                int m, int block_width, float* Y, int64_t ldy,
                                fasth_svd_tape* tape) {
+    DeviceGuard dg_(dev_of(c));
     return svd_forward_impl(c, p, nullptr, X, ldx, m, block_width, Y, ldy, tape);
 }
 
 fasth_status fasth_svd_plan_create(fasth_ctx c, const fasth_svd_param* p, int m, int block_width,
                                    int on_side_stream, fasth_svd_plan* out) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !out) return fail(FASTH_ERR_INVALID, "svd_plan_create: null argument");
     *out = nullptr;
     TRY(check_param("svd_plan_create", p));
@@ -1610,6 +1680,7 @@ fasth_status fasth_svd_plan_create(fasth_ctx c, const fasth_svd_param* p, int m,
 }
 
 fasth_status fasth_svd_plan_destroy(fasth_svd_plan pl) {
+    DeviceGuard dg_(dev_of(pl));
     if (!pl) return FASTH_OK;
     free_tape(pl->u);
     free_tape(pl->v);
@@ -1621,6 +1692,7 @@ fasth_status fasth_svd_plan_destroy(fasth_svd_plan pl) {
 fasth_status fasth_svd_forward_planned(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan,
                                        const float* X, int64_t ldx, int m, int block_width, float* Y,
                                        int64_t ldy, fasth_svd_tape* tape) {
+    DeviceGuard dg_(dev_of(c));
     if (!plan) return fail(FASTH_ERR_INVALID, "svd_forward_planned: null plan");
     if (plan->used) return fail(FASTH_ERR_INVALID, "svd_forward_planned: plan already consumed");
     if (plan->out_dim != p->out_dim || plan->in_dim != p->in_dim || plan->m != m || plan->b != block_width)
@@ -1718,6 +1790,7 @@ fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_p
 fasth_status fasth_svd_backward(fasth_ctx c, const fasth_svd_param* p, fasth_svd_tape st,
                                 const float* G, int64_t ldg, float* dX, int64_t lddx, float* dU,
                                 int64_t lddu, float* dV, int64_t lddv, float* dsigma) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !st) return fail(FASTH_ERR_INVALID, "svd_backward: null ctx or tape");
     TRY(check_param("svd_backward", p));
     if (p->out_dim != st->out_dim || p->in_dim != st->in_dim)
@@ -1789,6 +1862,7 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
                                         const float* G, int64_t ldg, int m, int block_width, float* Y,
                                         int64_t ldy, float* dX, int64_t lddx, float* dU, int64_t lddu,
                                         float* dV, int64_t lddv, float* dsigma) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     TRY(check_param("svd_forward_backward", p));
     TRY(check_mat("svd_forward: X", X, ldx, p->in_dim, m));
@@ -1909,6 +1983,7 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
 }
 
 fasth_status fasth_svd_tape_destroy(fasth_svd_tape st) {
+    DeviceGuard dg_(dev_of(st));
     if (!st) return FASTH_OK;
     free_tape(st->u);
     free_tape(st->v);
@@ -1921,10 +1996,13 @@ fasth_status fasth_svd_step(fasth_ctx c, const fasth_svd_param* p, const float* 
                             const float* dV, int64_t lddv, const float* dsigma, float eta,
                             float clamp_eps, float* U_out, int64_t ldou, float* V_out,
                             int64_t ldov, float* sigma_out) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     TRY(check_param("svd_step", p));
     if (!std::isfinite(eta)) return fail(FASTH_ERR_INVALID, "svd_step: eta not finite");
-    if (clamp_eps >= 1.f) return fail(FASTH_ERR_INVALID, "clamp_sigma: epsilon outside [0, 1)");
+    // clamp_eps == -1: no clamp; otherwise clamp_sigma's domain (svd_layer.hpp:196-198)
+    if (clamp_eps != -1.f && !(clamp_eps >= 0.f && clamp_eps < 1.f))
+        return fail(FASTH_ERR_INVALID, "clamp_sigma: epsilon outside [0, 1)");
     TRY(check_mat("svd_step: dU", dU, lddu, p->out_dim, p->nu));
     TRY(check_mat("svd_step: dV", dV, lddv, p->in_dim, p->nv));
     TRY(check_mat("svd_step: U_out", U_out, ldou, p->out_dim, p->nu));
@@ -1945,6 +2023,7 @@ fasth_status fasth_svd_step(fasth_ctx c, const fasth_svd_param* p, const float* 
 
 fasth_status fasth_clamp_sigma(fasth_ctx c, const float* sigma, int k, float epsilon,
                                float* sigma_out) {
+    DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
     if (!(epsilon >= 0.f && epsilon < 1.f))
         return fail(FASTH_ERR_INVALID, "clamp_sigma: epsilon outside [0, 1)");
@@ -1995,20 +2074,24 @@ fasth_status sigma_op(fasth_ctx c, const fasth_svd_param* p, const float* X, int
 
 fasth_status fasth_apply_inverse(fasth_ctx c, const fasth_svd_param* p, const float* X,
                                  int64_t ldx, int m, int b, float* Y, int64_t ldy) {
+    DeviceGuard dg_(dev_of(c));
     return sigma_op(c, p, X, ldx, m, b, Y, ldy, 1, "apply_inverse");
 }
 
 fasth_status fasth_apply_exponential(fasth_ctx c, const fasth_svd_param* p, const float* X,
                                      int64_t ldx, int m, int b, float* Y, int64_t ldy) {
+    DeviceGuard dg_(dev_of(c));
     return sigma_op(c, p, X, ldx, m, b, Y, ldy, 2, "apply_exponential");
 }
 
 fasth_status fasth_apply_cayley(fasth_ctx c, const fasth_svd_param* p, const float* X,
                                 int64_t ldx, int m, int b, float* Y, int64_t ldy) {
+    DeviceGuard dg_(dev_of(c));
     return sigma_op(c, p, X, ldx, m, b, Y, ldy, 3, "apply_cayley");
 }
 
 fasth_status fasth_log_abs_det(fasth_ctx c, const fasth_svd_param* p, double* out) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !out) return fail(FASTH_ERR_INVALID, "null argument");
     TRY(check_param("log_abs_det", p));
     if (p->out_dim != p->in_dim)
@@ -2059,6 +2142,7 @@ fasth_status fasth_svd_file_info(const char* path, int* out_dim, int* in_dim, in
 
 fasth_status fasth_svd_load(fasth_ctx c, const char* path, float* U, int64_t ldu, float* V, int64_t ldv,
                             float* sigma) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !path) return fail(FASTH_ERR_INVALID, "null argument");
     std::ifstream is(path, std::ios::binary);
     if (!is) return fail(FASTH_ERR_INVALID, "load_svd_param_file: cannot open %s", path);
@@ -2108,6 +2192,7 @@ fasth_status fasth_svd_load(fasth_ctx c, const char* path, float* U, int64_t ldu
 }
 
 fasth_status fasth_svd_save(fasth_ctx c, const fasth_svd_param* p, const char* path) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !path) return fail(FASTH_ERR_INVALID, "null argument");
     TRY(check_param("save_svd_param", p));
     const int k = std::min(p->out_dim, p->in_dim);
@@ -2137,6 +2222,7 @@ fasth_status fasth_svd_save(fasth_ctx c, const fasth_svd_param* p, const char* p
 }
 
 fasth_status fasth_tune_block_width(fasth_ctx c, int d, int m, int timed, uint64_t seed, int* out) {
+    DeviceGuard dg_(dev_of(c));
     if (!c || !out || d < 1 || m < 0) return fail(FASTH_ERR_INVALID, "fasth_tune_block_width: bad argument");
     if (!timed) {  // fasth.hpp:149-152
         *out = std::max(1, (int)std::lround(std::sqrt((double)d)));

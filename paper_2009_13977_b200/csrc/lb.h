@@ -117,7 +117,16 @@ struct DvNotify {
     int used = 0;
 };
 
-// The whole large-batch step (lb_run.cu).
+// The whole large-batch step (lb_run.cu).  Any shape: internally the step runs
+// on padded dimensions (pad_dims) — zero coordinates past d, zero samples past
+// m and zero vectors past n, whose diagonal entry of the triangular factor is
+// set to 1 so that they are exact identities — and the outputs are cut back.
+struct Dims {
+    int d, n, m;      // the caller's shape
+    int dp, np, mp;   // the padded shape every product runs on
+    bool padded() const { return dp != d || np != n || mp != m; }
+};
+Dims pad_dims(int d, int n, int m);
 int pick_block(int n);
 bool supported(int d, int n, int m);
 size_t workspace_floats(int d, int n, int m, bool want_dv);
@@ -146,9 +155,12 @@ cudaError_t reverse_vectors(const float* src, int64_t lds, int d, int n, float* 
 // (trunc: the (x, x - trunc_tf32(x)) form, see Gemm::split_trunc)
 cudaError_t split(const float* x, int64_t ldx, int rows, int cols, float* hi, float* lo,
                   int64_t ldo, cudaStream_t s, bool trunc = false);
-// VT = V^T split: V is n x d (ldv), VT d x n
+// the same into the top-left corner of a zero-padded rows_out x cols_out output
+cudaError_t split_pad(const float* x, int64_t ldx, int rows, int cols, int rows_out, int cols_out, float* hi,
+                      float* lo, int64_t ldo, cudaStream_t s, bool trunc = false);
+// VT = V^T split: V is n x d (ldv), VT d x n (zero-padded to d_out x n_out when given)
 cudaError_t split_transpose(const float* v, int64_t ldv, int n, int d, float* hi, float* lo,
-                            int64_t ldo, cudaStream_t s);
+                            int64_t ldo, cudaStream_t s, int n_out = -1, int d_out = -1);
 
 }  // namespace lb
 }  // namespace fasthb

@@ -43,9 +43,25 @@ __global__ void split4_kernel(const float4* __restrict__ x, int64_t ldx4, int ro
     }
 }
 
-// out (d x n) = split(V^T), V n x d
-__global__ void split_t_kernel(const float* __restrict__ v, int64_t ldv, int n, int d, float* __restrict__ hi,
-                               float* __restrict__ lo, int64_t ldo) {
+// Padded split: the rows x cols input lands in the top-left corner of a
+// rows_out x cols_out split output whose remaining entries are zero (ragged
+// shapes on the large-batch path: zero samples, zero coordinates and zero
+// vectors have no effect on the product, lb_run.cu).
+__global__ void split_pad_kernel(const float* __restrict__ x, int64_t ldx, int rows, int cols, int rows_out,
+                                 int cols_out, float* __restrict__ hi, float* __restrict__ lo, int64_t ldo,
+                                 bool trunc) {
+    const int64_t total = (int64_t)rows_out * cols_out;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / cols_out), c = (int)(i % cols_out);
+        const float v = (r < rows && c < cols) ? x[r * ldx + c] : 0.f;
+        hi[r * ldo + c] = split_hi(v, trunc);
+        lo[r * ldo + c] = split_lo(v, trunc);
+    }
+}
+
+// out (d_out x n_out) = split(V^T), V n x d; entries past (d, n) are zero
+__global__ void split_t_kernel(const float* __restrict__ v, int64_t ldv, int n, int d, int n_out, int d_out,
+                               float* __restrict__ hi, float* __restrict__ lo, int64_t ldo) {
     __shared__ float t[32][33];
     const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;  // i over n (rows of V), j over d
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
@@ -55,7 +71,7 @@ __global__ void split_t_kernel(const float* __restrict__ v, int64_t ldv, int n, 
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int j = j0 + r, i = i0 + threadIdx.x;
-        if (j < d && i < n) {
+        if (j < d_out && i < n_out) {
             const float x = t[threadIdx.x][r];
             const float h = rn_hi(x);
             hi[(int64_t)j * ldo + i] = h;
@@ -100,11 +116,22 @@ cudaError_t reverse_vectors(const float* src, int64_t lds, int d, int n, float* 
     return cudaGetLastError();
 }
 
+cudaError_t split_pad(const float* x, int64_t ldx, int rows, int cols, int rows_out, int cols_out, float* hi,
+                      float* lo, int64_t ldo, cudaStream_t s, bool trunc) {
+    if (rows_out == rows && cols_out == cols) return split(x, ldx, rows, cols, hi, lo, ldo, s, trunc);
+    if (rows_out <= 0 || cols_out <= 0) return cudaSuccess;
+    split_pad_kernel<<<grid_for((int64_t)rows_out * cols_out), 256, 0, s>>>(x, ldx, rows, cols, rows_out, cols_out,
+                                                                           hi, lo, ldo, trunc);
+    return cudaGetLastError();
+}
+
 cudaError_t split_transpose(const float* v, int64_t ldv, int n, int d, float* hi, float* lo, int64_t ldo,
-                            cudaStream_t s) {
-    if (n <= 0 || d <= 0) return cudaSuccess;
-    dim3 grid((d + 31) / 32, (n + 31) / 32);
-    split_t_kernel<<<grid, dim3(32, 8), 0, s>>>(v, ldv, n, d, hi, lo, ldo);
+                            cudaStream_t s, int n_out, int d_out) {
+    if (n_out < 0) n_out = n;
+    if (d_out < 0) d_out = d;
+    if (n_out <= 0 || d_out <= 0) return cudaSuccess;
+    dim3 grid((d_out + 31) / 32, (n_out + 31) / 32);
+    split_t_kernel<<<grid, dim3(32, 8), 0, s>>>(v, ldv, n, d, n_out, d_out, hi, lo, ldo);
     return cudaGetLastError();
 }
 

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "lb.h"
 
@@ -17,9 +18,11 @@ __device__ __forceinline__ float rn_hi(float x) {
 }
 
 // M_z = diag(G_z) + 2 striu(G_z), G_z = sum of the ks Gram partials
-// (flags a degenerate / non-finite ||v_i||^2 like the block builder)
-__global__ void gram_reduce_kernel(const float* __restrict__ part, int ks, int B, int nz, float* __restrict__ Mm,
-                                   ErrWord* err) {
+// (flags a degenerate / non-finite ||v_i||^2 like the block builder).
+// Padding vectors (index >= n_valid) are zero: their row and column of M are
+// zero, and a unit diagonal entry makes each an exact identity factor.
+__global__ void gram_reduce_kernel(const float* __restrict__ part, int ks, int B, int nz, int n_valid,
+                                   float* __restrict__ Mm, ErrWord* err) {
     const int64_t per = (int64_t)B * B, total = per * nz;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = e / per, w = e % per;
@@ -27,8 +30,9 @@ __global__ void gram_reduce_kernel(const float* __restrict__ part, int ks, int B
         float g = 0.f;
         if (j >= i)
             for (int s = 0; s < ks; ++s) g += part[(z * ks + s) * per + w];
-        Mm[e] = j > i ? 2.f * g : (j == i ? g : 0.f);
-        if (j == i && (!(g > 1e-30f) || !isfinite(g))) {
+        const bool pad = z * B + i >= n_valid;
+        Mm[e] = j > i ? 2.f * g : (j == i ? (pad ? 1.f : g) : 0.f);
+        if (j == i && !pad && (!(g > 1e-30f) || !isfinite(g))) {
             atomicOr(&err->flags, isfinite(g) ? kErrDegenerate : kErrNonFinite);
             atomicMin(&err->index, (int)(z * B + i));
             err->chain = 0;
@@ -229,15 +233,18 @@ __global__ void s_from_q_kernel(const float* __restrict__ Q, int B, float* __res
     }
 }
 
-// dV rows (B x d) = sum of ks partials
-__global__ void dv_reduce_kernel(const float* __restrict__ part, int ks, int B, int d, float* __restrict__ dV,
-                                 int64_t lddv) {
+// dV rows (B x d) = sum of ks partials; only rows < rows_valid and columns
+// < d_valid (the caller's shape) are written
+__global__ void dv_reduce_kernel(const float* __restrict__ part, int ks, int B, int d, int rows_valid, int d_valid,
+                                 float* __restrict__ dV, int64_t lddv) {
     const int64_t per = (int64_t)B * d;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < per; e += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e / d), c = (int)(e % d);
+        if (r >= rows_valid || c >= d_valid) continue;
         float s = 0.f;
 #pragma unroll 4
         for (int k = 0; k < ks; ++k) s += __ldg(part + k * per + e);
-        dV[(e / d) * lddv + e % d] = s;
+        dV[(int64_t)r * lddv + c] = s;
     }
 }
 
@@ -251,8 +258,18 @@ int pick_block(int n) {
     return 0;
 }
 
+// The products need d and m multiples of 4 (16-byte TMA strides), n a
+// multiple of the block width and d >= 128, m >= 16 (tile shapes).
+Dims pad_dims(int d, int n, int m) {
+    Dims D{d, n, m, 0, 0, 0};
+    D.dp = std::max(128, (d + 3) / 4 * 4);
+    D.np = std::max(128, (n + 127) / 128 * 128);
+    D.mp = std::max(16, (m + 3) / 4 * 4);
+    return D;
+}
+
 bool supported(int d, int n, int m) {
-    return d >= 128 && d % 4 == 0 && n >= 128 && pick_block(n) > 0 && m >= 16 && m % 4 == 0;
+    return d >= 1 && n >= 1 && m >= 1 && d <= (1 << 24) && n <= (1 << 24) && m <= (1 << 26);
 }
 
 // split-K scratch for the chain products when the batch is too small for
@@ -262,7 +279,9 @@ int64_t small_batch_scratch(int d, int n, int m) {
     return m < 1024 ? std::min<int64_t>((int64_t)64 * m * std::max(d, n), (int64_t)32 << 20) : 0;
 }
 
-size_t workspace_floats(int d, int n, int m, bool want_dv) {
+size_t workspace_floats(int d0, int n0, int m0, bool want_dv) {
+    const Dims D = pad_dims(d0, n0, m0);
+    const int d = D.dp, n = D.np, m = D.mp;
     const int B = pick_block(n), nb = n / B;
     const size_t nd = (size_t)n * d, md = (size_t)m * d, bb = (size_t)B * B;
     size_t f = 0;
@@ -293,13 +312,13 @@ struct Carver {
 };
 
 namespace {
-constexpr int kMaxStages = 65;
 
 struct Bufs {
+    Dims D{};
     int B = 0, nb = 0;
     size_t nd = 0, md = 0, bb = 0;
     float *Vh, *Vl, *VTh, *VTl, *Gp, *Mm, *Dinv, *Th, *Tl, *TTh, *TTl, *WfH, *WfL, *WbH, *WbL;
-    float *Sth[kMaxStages], *Stl[kMaxStages];
+    std::vector<float*> Sth, Stl;  // forward stages 0..nb
     float *ZbTh2[3], *ZbTl2[3], *ZfAh, *ZfAl, *Gh[3], *Gl[3];  // ZfA: m x n, block j = columns jB..
     float *Qp, *Qs, *Sh, *Sl, *dVp;
     float* ksc;  // split-K scratch of the small-batch chain products (m < 1024)
@@ -308,11 +327,15 @@ struct Bufs {
 constexpr int ksG = 4, ksQ = 16, ksV = 4;  // split-K counts (128 CTAs each: one tile per CTA)
 
 // The workspace is carved identically by the forward and the backward half.
-bool carve(float* ws, int d, int n, int m, Bufs& b) {
+// (padded dimensions, pad_dims)
+bool carve(float* ws, int d0, int n0, int m0, Bufs& b) {
+    b.D = pad_dims(d0, n0, m0);
+    const int d = b.D.dp, n = b.D.np, m = b.D.mp;
     b.B = pick_block(n);
     if (!b.B) return false;
     b.nb = n / b.B;
-    if (b.nb + 1 > kMaxStages) return false;
+    b.Sth.assign(b.nb + 1, nullptr);
+    b.Stl.assign(b.nb + 1, nullptr);
     const int B = b.B, nb = b.nb;
     const size_t nd = b.nd = (size_t)n * d, md = b.md = (size_t)m * d, bb = b.bb = (size_t)B * B;
     Carver c{ws};
@@ -357,7 +380,7 @@ bool carve(float* ws, int d, int n, int m, Bufs& b) {
     (void)bb;                                                                                                \
     float *Vh = b.Vh, *Vl = b.Vl, *VTh = b.VTh, *VTl = b.VTl, *Gp = b.Gp, *Mm = b.Mm, *Dinv = b.Dinv;       \
     float *Th = b.Th, *Tl = b.Tl, *TTh = b.TTh, *TTl = b.TTl, *WfH = b.WfH, *WfL = b.WfL, *WbH = b.WbH;      \
-    float *WbL = b.WbL, **Sth = b.Sth, **Stl = b.Stl, *ZfAh = b.ZfAh, *ZfAl = b.ZfAl;                        \
+    float *WbL = b.WbL, **Sth = b.Sth.data(), **Stl = b.Stl.data(), *ZfAh = b.ZfAh, *ZfAl = b.ZfAl;                        \
     float **Gh = b.Gh, **Gl = b.Gl;                                                                          \
     float *Qp = b.Qp, *Qs = b.Qs, *Sh = b.Sh, *Sl = b.Sl, *dVp = b.dVp;                                    \
     (void)Vh, (void)Vl, (void)VTh, (void)VTl, (void)Gp, (void)Mm, (void)Dinv, (void)Th, (void)Tl, (void)TTh; \
@@ -376,7 +399,9 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
     if (k1_pre) *k1_pre = false;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
-    if (Y && ((ldy % 4) || (reinterpret_cast<uintptr_t>(Y) & 15))) return cudaErrorInvalidValue;
+    const Dims D = b.D;
+    const bool pad = D.padded();  // Y is then cut out of the last stage
+    if (Y && !pad && ((ldy % 4) || (reinterpret_cast<uintptr_t>(Y) & 15))) return cudaErrorInvalidValue;
     LB_ALIASES;
     cudaError_t e;
     // the input splits do not depend on the build: on the second stream (the
@@ -387,18 +412,20 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         LBTRY(cudaEventRecord(st->ev[0], s));
         LBTRY(cudaStreamWaitEvent(sx, st->ev[0], 0));
     }
-    ++nl;
-    LBTRY(split(X, ldx, m, d, Sth[nb], Stl[nb], d, sx, true));  // stages: (x, x - trunc(x))
+    ++nl;  // stages: (x, x - trunc(x))
+    LBTRY(split_pad(X, ldx, D.m, D.d, D.mp, D.dp, Sth[nb], Stl[nb], D.dp, sx, true));
     if (G) {
         ++nl;
-        LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, sx, true));
+        LBTRY(split_pad(G, ldg, D.m, D.d, D.mp, D.dp, Gh[0], Gl[0], D.dp, sx, true));
     }
     if (two) LBTRY(cudaEventRecord(st->ev[1], sx));
     // ---- build: split V and V^T, Gram per block, T~, WfR = T~ V_j, WbR = T~^T V_j
     ++nl;
-    LBTRY(split(V, ldv, n, d, Vh, Vl, d, s));
+    LBTRY(split_pad(V, ldv, D.n, D.d, D.np, D.dp, Vh, Vl, D.dp, s));
     ++nl;
-    LBTRY(split_transpose(V, ldv, n, d, VTh, VTl, n, s));
+    LBTRY(split_transpose(V, ldv, D.n, D.d, VTh, VTl, D.np, s, D.np, D.dp));
+    // from here on every product runs on the padded shape
+    d = D.dp, n = D.np, m = D.mp;
     int g_ks = ksG;
     {
         Gemm g;
@@ -415,7 +442,7 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
         g_ks = g.ksplit;
     }
     ++nl;
-    gram_reduce_kernel<<<grid_for(nb * bb), 256, 0, s>>>(Gp, g_ks, B, nb, Mm, err);
+    gram_reduce_kernel<<<grid_for(nb * bb), 256, 0, s>>>(Gp, g_ks, B, nb, D.n, Mm, err);
     {
         ++nl;
         diag_inv_kernel<<<dim3(B / 32, nb), 32, 0, s>>>(Mm, B, Dinv);
@@ -506,13 +533,16 @@ cudaError_t forward(const float* V, int64_t ldv, int d, int n, const float* X, i
             g.d_lo = Stl[j];
             g.lds = d;
             g.split_trunc = true;
-            if (j == 0) {
+            if (j == 0 && !pad) {
                 g.d_f32 = Y;
                 g.ldd = ldy;
             }
             LB_GEMM(g, s, "lb_f2_update");
         }
     }
+    if (pad && Y)  // the last stage holds the output itself (hi of the trunc split is x)
+        LBTRY(cudaMemcpy2DAsync(Y, ldy * sizeof(float), Sth[0], (size_t)d * sizeof(float), (size_t)D.d * sizeof(float),
+                                D.m, cudaMemcpyDeviceToDevice, s));
     if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[6], 0));  // join: WbR built
     if (nlaunch) *nlaunch = nl;
     return cudaGetLastError();
@@ -525,7 +555,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     int nl = 0;
     Bufs b;
     if (!supported(d, n, m) || !carve(ws, d, n, m, b)) return cudaErrorInvalidValue;
-    if (dX && ((lddx % 4) || (reinterpret_cast<uintptr_t>(dX) & 15))) return cudaErrorInvalidValue;
+    const Dims D = b.D;
+    const bool pad = D.padded();  // dX is then cut out of the last gradient buffer
+    if (dX && !pad && ((lddx % 4) || (reinterpret_cast<uintptr_t>(dX) & 15))) return cudaErrorInvalidValue;
     const bool want_dv = dV != nullptr;
     LB_ALIASES;
     cudaError_t e;
@@ -536,8 +568,9 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
     // (which overwrites buffer (j+1) % 3) waits only for block j-2's dV.
     if (!g_split) {
         ++nl;
-        LBTRY(split(G, ldg, m, d, Gh[0], Gl[0], d, s, true));
+        LBTRY(split_pad(G, ldg, D.m, D.d, D.mp, D.dp, Gh[0], Gl[0], D.dp, s, true));
     }
+    d = D.dp, n = D.np, m = D.mp;
     const bool two = st && st->aux && want_dv;
     cudaStream_t sa = two ? st->aux : s;
     for (int j = 0; j < nb; ++j) {
@@ -607,14 +640,15 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
                 v_ks = g.ksplit;
             }
             ++nl;
-            dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, dV + (size_t)j * B * lddv, lddv);
+            dv_reduce_kernel<<<grid_for((int64_t)B * d), 256, 0, sa>>>(dVp, v_ks, B, d, D.n - j * B, D.d,
+                                                                       dV + (size_t)j * B * lddv, lddv);
             if (two) LBTRY(cudaEventRecord(st->ev[12 + cur], sa));
             if (nt && nt->count > 0) {  // last block of its bucket: rows up to here are final
                 const int nbk = std::min(nt->count, nb);
                 const int bk = (int)((int64_t)j * nbk / nb);
                 if (j + 1 == nb || (int)((int64_t)(j + 1) * nbk / nb) != bk) {
                     LBTRY(cudaEventRecord(nt->ev[bk], sa));
-                    nt->row_end[bk] = std::min<int64_t>(n, (int64_t)(j + 1) * B);
+                    nt->row_end[bk] = std::min<int64_t>(D.n, (int64_t)(j + 1) * B);
                     nt->used = bk + 1;
                 }
             }
@@ -641,12 +675,15 @@ cudaError_t backward(int d, int n, int m, const float* G, int64_t ldg, float* dX
             g.d_lo = Gl[nxt];
             g.lds = d;
             g.split_trunc = true;
-            if (j == nb - 1) {  // dX only: no later block reads the split gradient
+            if (j == nb - 1 && !pad) {  // dX only: no later block reads the split gradient
                 g.d_f32 = dX;
                 g.ldd = lddx;
                 g.d_hi = g.d_lo = nullptr;
             }
             LB_GEMM(g, s, "lb_k4_update");
+            if (j == nb - 1 && pad && dX)  // hi of the trunc split is the gradient itself
+                LBTRY(cudaMemcpy2DAsync(dX, lddx * sizeof(float), Gh[nxt], (size_t)d * sizeof(float),
+                                        (size_t)D.d * sizeof(float), D.m, cudaMemcpyDeviceToDevice, s));
         }
     }
     if (two) LBTRY(cudaStreamWaitEvent(s, st->ev[12 + (nb - 1) % 3], 0));  // join: dV complete

@@ -74,10 +74,15 @@ struct B2Smem {
         o += (size_t)(BS + BS * BS) * 4;
         total = o;
         // [Wf | Sf^T] and [Wb | Sb^T] rows (pitch BS+4) alias blocks i-1, i+1
-        // and the partial band, all dead by then
+        // and the partial band, all dead by then — when they fit there: the
+        // reduced band and rinv / M2 are read while the rows are written, so
+        // otherwise (tall slabs, small BS) the rows get their own region
         ws = vt + (size_t)BS * P * 4;
         const size_t need = (size_t)2 * (RB + BS) * (BS + 4) * 4;
-        if (ws + need > total) total = ws + need;
+        if (ws + need > gr) {
+            ws = (total + 15) / 16 * 16;
+            total = ws + need;
+        }
     }
 };
 

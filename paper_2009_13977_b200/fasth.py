@@ -218,6 +218,24 @@ def _out_ld(T, d: int, m: int, what: str) -> int:
     return max(T.stride(1) if m > 1 else d, d, 1)
 
 
+def _check_out(T, like: torch.Tensor, what: str) -> torch.Tensor:
+    """A caller-provided output: float32 on the input's device (shape and
+    column-major layout are checked by _out_ld)."""
+    if not isinstance(T, torch.Tensor) or T.dtype != torch.float32 or T.device != like.device:
+        raise Error(f"out {what}: expected a float32 tensor on {like.device}")
+    return T
+
+
+def _host_f32(T, shape, what: str) -> torch.Tensor:
+    """A host buffer of the host-buffer entry: CPU float32, C-contiguous, the
+    given shape (the C ABI reads and writes it through raw pointers)."""
+    if not isinstance(T, torch.Tensor) or T.is_cuda or T.dtype != torch.float32 or not T.is_contiguous() \
+            or tuple(T.shape) != tuple(shape):
+        raise DimensionError(f"forward_backward_host: {what} must be a contiguous CPU float32 tensor of shape "
+                             f"{tuple(shape)}")
+    return T
+
+
 def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None and t.numel() > 0 else None
 
@@ -267,8 +285,8 @@ def fasth_forward(V: torch.Tensor, X: torch.Tensor, block_width: int, *, ctx: Co
     if n > 0 and dv != d:
         raise DimensionError("fasth_forward: X row count != chain dim")
     c = _ctx(ctx, X)
-    Y = _new_out(d, m, X) if out is None else out
-    ldy = max(Y.stride(1), d, 1)
+    Y = _new_out(d, m, X) if out is None else _check_out(out, X, "Y")
+    ldy = _out_ld(Y, d, m, "Y")
     h = C.c_void_p()
     _check(c.lib.fasth_forward(c.h, _ptr(V), ldv, d, n, _ptr(X), ldx, m, int(block_width),
                                _ptr(Y), ldy, C.byref(h) if record else None))
@@ -326,14 +344,19 @@ def forward_backward_host(V, X, G, block_width: int, *, ctx: Context | None = No
     preallocated (pinned) ones."""
     c = ctx if ctx is not None else default_context()
     c.bind_stream()
+    if not isinstance(V, torch.Tensor) or V.dim() != 2 or not isinstance(X, torch.Tensor) or X.dim() != 2:
+        raise DimensionError("forward_backward_host: V must be (n, d) and X (m, d)")
     n, d = V.shape
     m = X.shape[0]
+    _host_f32(V, (n, d), "V")
+    _host_f32(X, (m, d), "X")
+    _host_f32(G, (m, d), "G")
     if out is None:
         Y = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
         dX = torch.empty((m, d), dtype=torch.float32, pin_memory=True)
         dV = torch.empty((n, d), dtype=torch.float32, pin_memory=True)
     else:
-        Y, dX, dV = out
+        Y, dX, dV = (_host_f32(t, sh, w) for t, sh, w in zip(out, ((m, d), (m, d), (n, d)), ("Y", "dX", "dV")))
     _check(c.lib.fasth_forward_backward_host(c.h, _ptr(V), d, n, _ptr(X), _ptr(G), m,
                                              int(block_width), _ptr(Y), _ptr(dX), _ptr(dV)))
     return Y, dX, dV
@@ -491,7 +514,15 @@ def svd_forward_backward(p: SvdParam, X: torch.Tensor, G: torch.Tensor, block_wi
 
 def svd_step(p: SvdParam, g: SvdGradients, eta: float, *, clamp_epsilon: float | None = None,
              inplace: bool = False, ctx: Context | None = None) -> SvdParam:
-    """svd_layer.hpp:158 (optionally fused with clamp_sigma, :196)."""
+    """svd_layer.hpp:158 (optionally fused with clamp_sigma, :196).
+
+    The reference's svd_step is pure (it returns a new SvdParam and rejects a
+    degenerate update before anything changes).  ``inplace=True`` writes the
+    update into ``p`` itself, so a degeneracy error raised by the step leaves
+    ``p`` already updated; use the default (a new parameter) where that
+    matters."""
+    if clamp_epsilon is not None and not (0.0 <= float(clamp_epsilon) < 1.0):
+        raise Error("clamp_sigma: epsilon outside [0, 1)")
     pc = p._c()
     if g.grad_U_vectors.shape != p.U.shape or g.grad_V_vectors.shape != p.V.shape or \
             g.grad_sigma.numel() != p.sigma.numel():
