@@ -141,7 +141,7 @@ def cpu_reference(d, m, b, reps, warm=1):
     for _ in range(max(warm - 1, 0)):
         R.run_bench("mul", "fasth", d, m, b, 1, SEED, 0)
     mean, std, _ = R.run_bench("mul", "fasth", d, m, b, reps, SEED, 0)
-    return mean * 1e6, std * 1e6, R.hardware_threads(), "reference"
+    return mean * 1e6, std * 1e6, R.hardware_threads(), "reference", R.march
 
 
 def cpu_sequential(d, m, b, reps=8):
@@ -167,7 +167,7 @@ def run_reference_impl(args):
         return
     world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
     try:  # the whole job's batch (32 per GPU) on the host's cores
-        us, std, cores, kind = cpu_reference(D, M * world, B, max(args.steps, 1), args.warmup)
+        us, std, cores, kind, march = cpu_reference(D, M * world, B, max(args.steps, 1), args.warmup)
     except Exception as e:  # the reference always builds here; report, don't fake
         print(json.dumps({"impl": "reference", "unavailable": f"oracle/_ref failed: {e}"}))
         return
@@ -181,7 +181,7 @@ def run_reference_impl(args):
         "tflops": flops_alg(D, D, M * world, B) / (us * 1e-6) / 1e12,
         "cpu_baseline": {"value": us, "unit": "us/step", "cores": cores, "kind": kind,
                          "sample": f"run_bench op=mul d={D} m={M * world} k={B} algo=fasth, "
-                                   f"{args.steps} reps after warm-up (std {std:.1f} us)"},
+                                   f"{args.steps} reps after warm-up (std {std:.1f} us), built -march={march}"},
         "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -587,10 +587,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            us_c, std_c, cores, kind = cpu_reference(D, M, B, args.cpu_reps)
+            us_c, std_c, cores, kind, march = cpu_reference(D, M, B, args.cpu_reps)
             cpu = {"value": us_c, "unit": "us/step", "cores": cores, "kind": kind,
                    "sample": f"reference bench::run_bench op=mul d={D} m={M} k={B} algo=fasth, "
-                             f"{args.cpu_reps} reps (std {std_c:.0f} us), all host threads"}
+                             f"{args.cpu_reps} reps (std {std_c:.0f} us), all host threads, built -march={march}"}
             us_s, std_s = cpu_sequential(D, M, B)
             cpu["sequential"] = {"value": us_s, "unit": "us/step", "cores": 1,
                                  "sample": f"run_bench op=mul d={D} m={M} algo=sequential (the reference's "

@@ -151,6 +151,32 @@ fasth_status fasth_forward_backward_host(fasth_ctx ctx, const float* V, int d, i
                                          const float* X, const float* G, int m, int block_width,
                                          float* Y, float* dX, float* dV);
 
+/* ---- WY internals (wy.hpp:56-170, public in the reference) ----------------
+ * The compact WY form in the reference's own layout: for a block of b
+ * vectors (column-major d x b, column j = v_j, chain order)
+ *   I - 2 W Y^T = H_1 ... H_b,  Y[:, j] = v_j / ||v_j||,
+ *   W[:, j] = H_1 ... H_{j-1} Y[:, j]             (wy.hpp:85-96)
+ * W and Y are column-major d x b.  The chain sweeps do not use this form
+ * (they run the UT form of the raw vectors); these entries serve callers of
+ * the reference's WY functions and TapeForward::compacted. */
+/* wy_compact (wy.hpp:56): b >= 1 vectors -> (W, Y); FASTH_ERR_INVALID for
+ * b == 0 (wy.hpp:58-59), FASTH_ERR_DEGENERATE for ||v||^2 <= 1e-30. */
+fasth_status fasth_wy_compact(fasth_ctx ctx, const float* V, int64_t ldv, int d, int b, float* W,
+                              int64_t ldw, float* Y, int64_t ldy);
+/* compact_chain (wy.hpp:151): the chain (d x n) partitioned into
+ * ceil(n / block_width) consecutive blocks (the last ragged), each compacted;
+ * block i's W and Y are columns [i bw, i bw + w_i) of the d x n W and Y.
+ * FASTH_ERR_INVALID for block_width outside [1, n] (wy.hpp:153-155). */
+fasth_status fasth_compact_chain(fasth_ctx ctx, const float* V, int64_t ldv, int d, int n, int block_width,
+                                 float* W, int64_t ldw, float* Y, int64_t ldy);
+/* wy_apply (wy.hpp:104): out = X - 2 W (Y^T X), X and out d x m (out may be X). */
+fasth_status fasth_wy_apply(fasth_ctx ctx, const float* W, int64_t ldw, const float* Y, int64_t ldy, int d,
+                            int b, const float* X, int64_t ldx, int m, float* out, int64_t ldo);
+/* wy_apply_transpose (wy.hpp:137): out = X - 2 Y (W^T X). */
+fasth_status fasth_wy_apply_transpose(fasth_ctx ctx, const float* W, int64_t ldw, const float* Y, int64_t ldy,
+                                      int d, int b, const float* X, int64_t ldx, int m, float* out,
+                                      int64_t ldo);
+
 /* ---- SVD-reparameterised layer W = U Sigma V^T ---------------------------
  * SvdParam (svd_layer.hpp:25-72): U chain of nu vectors in dimension out_dim,
  * V chain of nv vectors in dimension in_dim, sigma of min(out_dim, in_dim). */

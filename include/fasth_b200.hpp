@@ -12,9 +12,13 @@
 // Differences a caller can observe (by design, documented in DESIGN.md):
 //   * arithmetic is fp32 on the device (3xTF32-class accuracy target; the
 //     parity bound is relative_error <= 1e-4, matrix.hpp:106-110);
-//   * TapeForward keeps its per-block activations on the device; output()
-//     and input() are host copies, the WY blocks are not exposed;
-//   * block widths above 64 run as 64-wide WY sub-blocks (same product).
+//   * TapeForward's `compacted` (the WY blocks, wy.hpp:29-48) and
+//     `activations` (fasth.hpp:22-29) are materialised on the device by
+//     compact_chain and the block recurrence A_i = wy_apply(P_i, A_{i+1})
+//     (fasth.hpp:58-59) and copied to the host, as the reference holds them;
+//     the backward runs from the device tape;
+//   * the chain kernels run block widths above 64 as narrower WY sub-blocks
+//     (same product; the materialised blocks keep the caller's width).
 //
 // Header-only; link with -lfasth_b200.
 #pragma once
@@ -253,6 +257,132 @@ private:
     std::vector<HouseholderVector> vs_;
 };
 
+// ---- WY blocks (wy.hpp:18-170) ---------------------------------------------------
+/// WYBlock (wy.hpp:18-25): I - 2 W Y^T = H_1 ... H_width.
+struct WYBlock {
+    std::size_t dim = 0;
+    std::size_t width = 0;
+    Matrix W;  // dim x width
+    Matrix Y;  // dim x width
+    std::vector<HouseholderVector> source_vectors;
+    std::size_t sequential_steps = 0;  // the reference's instrumentation: width prepends
+};
+
+/// CompactedChain (wy.hpp:29-48).
+struct CompactedChain {
+    std::size_t dim = 0;
+    std::size_t block_width = 0;
+    std::vector<WYBlock> blocks;
+    std::size_t factor_count() const {
+        std::size_t n = 0;
+        for (const auto& b : blocks) n += b.width;
+        return n;
+    }
+    std::size_t compaction_stages() const {
+        std::size_t s = 0;
+        for (const auto& b : blocks) s = std::max(s, b.sequential_steps);
+        return s;
+    }
+};
+
+namespace detail {
+// column-major fp32 d x width -> host Matrix (d x width)
+inline Matrix cols_to_matrix(const std::vector<float>& v, std::size_t d, std::size_t col0, std::size_t w) {
+    Matrix m(d, w);
+    for (std::size_t j = 0; j < w; ++j)
+        for (std::size_t i = 0; i < d; ++i) m(i, j) = v[(col0 + j) * d + i];
+    return m;
+}
+inline std::vector<float> vectors_to_device(const std::vector<HouseholderVector>& vs, std::size_t dim) {
+    std::vector<float> out(dim * vs.size());
+    for (std::size_t k = 0; k < vs.size(); ++k) {
+        if (vs[k].dim() != dim) throw DimensionError("wy_compact: vector length mismatch");
+        for (std::size_t i = 0; i < dim; ++i) out[k * dim + i] = static_cast<float>(vs[k][i]);
+    }
+    return out;
+}
+// host blocks from the device compaction's W, Y (column-major dim x n)
+inline std::vector<WYBlock> blocks_from(const std::vector<float>& wh, const std::vector<float>& yh,
+                                        const std::vector<HouseholderVector>& vs, std::size_t dim, std::size_t bw) {
+    const std::size_t n = vs.size();
+    std::vector<WYBlock> out;
+    for (std::size_t lo = 0; lo < n; lo += bw) {
+        const std::size_t w = std::min(bw, n - lo);
+        WYBlock b;
+        b.dim = dim;
+        b.width = w;
+        b.W = cols_to_matrix(wh, dim, lo, w);
+        b.Y = cols_to_matrix(yh, dim, lo, w);
+        b.source_vectors.assign(vs.begin() + lo, vs.begin() + lo + w);
+        b.sequential_steps = w;
+        out.push_back(std::move(b));
+    }
+    return out;
+}
+// device compaction of n vectors in blocks of bw into host blocks
+inline std::vector<WYBlock> compact_on_device(const std::vector<HouseholderVector>& vs, std::size_t dim,
+                                              std::size_t bw, bool whole) {
+    const std::size_t n = vs.size();
+    DeviceBuffer V(dim * n), W(dim * n), Y(dim * n);
+    V.upload(vectors_to_device(vs, dim));
+    const int64_t ld = (int64_t)std::max<std::size_t>(dim, 1);
+    if (whole)
+        check(fasth_wy_compact(Device::ctx(), V.get(), ld, (int)dim, (int)n, W.get(), ld, Y.get(), ld));
+    else
+        check(fasth_compact_chain(Device::ctx(), V.get(), ld, (int)dim, (int)n, (int)bw, W.get(), ld, Y.get(), ld));
+    return blocks_from(W.download(dim * n), Y.download(dim * n), vs, dim, bw);
+}
+// block -> device W, Y (column-major d x width)
+struct DeviceBlock {
+    DeviceBuffer W, Y;
+    explicit DeviceBlock(const WYBlock& b) : W(b.dim * b.width), Y(b.dim * b.width) {
+        W.upload(b.W.to_device_layout());
+        Y.upload(b.Y.to_device_layout());
+    }
+};
+inline Matrix wy_apply_impl(const WYBlock& block, const Matrix& X, bool transpose) {
+    if (X.rows() != block.dim)
+        throw DimensionError(std::string(transpose ? "wy_apply_transpose" : "wy_apply") + ": X has " +
+                             std::to_string(X.rows()) + " rows, block dim " + std::to_string(block.dim));
+    const std::size_t d = block.dim, m = X.cols();
+    DeviceBlock db(block);
+    DeviceBuffer Xd(d * m), Od(d * m);
+    Xd.upload(X.to_device_layout());
+    const int64_t ld = (int64_t)std::max<std::size_t>(d, 1);
+    check((transpose ? fasth_wy_apply_transpose : fasth_wy_apply)(Device::ctx(), db.W.get(), ld, db.Y.get(), ld,
+                                                                 (int)d, (int)block.width, Xd.get(), ld, (int)m,
+                                                                 Od.get(), ld));
+    return Matrix::from_device_layout(d, m, Od.download(d * m));
+}
+}  // namespace detail
+
+/// wy.hpp:56 — (W, Y) of b >= 1 reflections, on the device.
+inline WYBlock wy_compact(const std::vector<HouseholderVector>& vectors, std::size_t dim) {
+    if (vectors.empty()) throw Error("wy_compact: empty vector list");
+    return std::move(detail::compact_on_device(vectors, dim, vectors.size(), true).front());
+}
+
+/// wy.hpp:104 — X - 2 W (Y^T X).
+inline Matrix wy_apply(const WYBlock& block, const Matrix& X) { return detail::wy_apply_impl(block, X, false); }
+
+/// wy.hpp:137 — X - 2 Y (W^T X).
+inline Matrix wy_apply_transpose(const WYBlock& block, const Matrix& X) {
+    return detail::wy_apply_impl(block, X, true);
+}
+
+/// wy.hpp:151 — ceil(n / block_width) consecutive blocks, the last ragged.
+inline CompactedChain compact_chain(const HouseholderChain& chain, std::size_t block_width) {
+    const std::size_t n = chain.size();
+    if (block_width < 1 || block_width > n)
+        throw Error("compact_chain: block width " + std::to_string(block_width) + " outside [1, " +
+                    std::to_string(n) + "]");
+    CompactedChain out;
+    out.dim = chain.dim();
+    out.block_width = block_width;
+    out.blocks = detail::compact_on_device(chain.vectors(), chain.dim(), block_width, false);
+    return out;
+}
+
 // ---- FastH (fasth.hpp:22-109) ---------------------------------------------------
 struct TapeHandle {
     fasth_tape t = nullptr;
@@ -261,15 +391,16 @@ struct TapeHandle {
     }
 };
 
-/// TapeForward (fasth.hpp:22-29).  The per-block activations live on the
-/// device inside the opaque handle; output() / input() are host copies.
+/// TapeForward (fasth.hpp:22-29): the compacted chain and the activations
+/// A_1..A_{q+1} (activations[q] = X, activations[0] = the output), as the
+/// reference holds them, plus the device tape the backward runs from.
 struct TapeForward {
+    CompactedChain compacted;
+    std::vector<Matrix> activations;
     std::shared_ptr<TapeHandle> handle;
-    Matrix in, out;
-    std::size_t blocks = 0;
-    const Matrix& output() const { return out; }
-    const Matrix& input() const { return in; }
-    std::size_t block_count() const { return blocks; }
+    const Matrix& output() const { return activations.front(); }
+    const Matrix& input() const { return activations.back(); }
+    std::size_t block_count() const { return compacted.blocks.size(); }
 };
 
 /// BackwardResult (fasth.hpp:31-34).
@@ -302,11 +433,34 @@ inline TapeForward fasth_forward(const HouseholderChain& chain, const Matrix& X,
                         Yd.get(), (int64_t)std::max<std::size_t>(d, 1), &h->t));
     TapeForward tape;
     tape.handle = h;
-    tape.in = X;
-    tape.out = Matrix::from_device_layout(d, m, Yd.download(d * m));
-    int q = 0;
-    check(fasth_tape_info(h->t, nullptr, nullptr, nullptr, nullptr, &q));
-    tape.blocks = (std::size_t)q;
+    tape.compacted.dim = d;
+    tape.compacted.block_width = block_width;
+    if (n == 0) {  // fasth.hpp:46-51
+        tape.activations.push_back(X);
+        return tape;
+    }
+    // the reference's members: compacted blocks and the block recurrence
+    // A_i = wy_apply(P_i, A_{i+1}) (fasth.hpp:55-59), all on the device
+    const std::size_t b = std::min(std::max<std::size_t>(block_width, 1), n), q = (n + b - 1) / b;
+    const int64_t ld = (int64_t)std::max<std::size_t>(d, 1);
+    tape.compacted.block_width = b;
+    DeviceBuffer W(d * n), Yw(d * n), A(d * m * (q + 1));
+    check(fasth_compact_chain(Device::ctx(), V.get(), ld, (int)d, (int)n, (int)b, W.get(), ld, Yw.get(), ld));
+    tape.compacted.blocks = detail::blocks_from(W.download(d * n), Yw.download(d * n), chain.vectors(), d, b);
+    check(fasth_copy(Device::ctx(), A.get() + q * d * m, Xd.get(), (int64_t)(d * m * sizeof(float)), 2));
+    for (std::size_t i = q; i-- > 0;) {
+        const std::size_t w = std::min(b, n - i * b);
+        check(fasth_wy_apply(Device::ctx(), W.get() + i * b * d, ld, Yw.get() + i * b * d, ld, (int)d, (int)w,
+                             A.get() + (i + 1) * d * m, ld, (int)m, A.get() + i * d * m, ld));
+    }
+    const auto ah = A.download(d * m * (q + 1));
+    tape.activations.resize(q + 1);
+    tape.activations[q] = X;
+    for (std::size_t i = 0; i < q; ++i) {
+        std::vector<float> one(ah.begin() + i * d * m, ah.begin() + (i + 1) * d * m);
+        tape.activations[i] = Matrix::from_device_layout(d, m, one);
+    }
+    (void)Yd;
     return tape;
 }
 

@@ -29,6 +29,28 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libfasth_ref.so")
+REF_NATIVE_SO = os.path.join(HERE, "_ref", "libfasth_ref_native.so")
+
+
+def _native_ok() -> bool:
+    """The -march=native build runs here iff this CPU has the ISA extensions
+    of the CPU it was compiled on (AVX-512 / AMX of Sapphire Rapids class)."""
+    try:
+        flags = set(open("/proc/cpuinfo").read().split("flags", 2)[1].split("\n", 1)[0].split())
+    except Exception:
+        return False
+    march = ""
+    try:
+        march = open(os.path.join(HERE, "_ref", "native_march.txt")).read().strip()
+    except Exception:
+        pass
+    need = {"avx512f", "avx512bw", "avx512vl", "avx512_fp16", "amx_tile"} if march in (
+        "sapphirerapids", "emeraldrapids", "graniterapids") else {"__unknown__"}
+    return need <= flags
+
+
+def ref_so_path() -> str:
+    return REF_NATIVE_SO if os.path.exists(REF_NATIVE_SO) and _native_ok() else REF_SO
 
 _D = C.POINTER(C.c_double)
 _SZ = C.c_size_t
@@ -171,11 +193,15 @@ class Port:
 class Ref:
     """The unmodified reference compiled behind oracle/ref_shim.cpp."""
 
-    def __init__(self, path: str = REF_SO):
-        if not os.path.exists(path):
-            build()
+    def __init__(self, path: str | None = None):
+        if path is None:
+            if not os.path.exists(REF_SO):
+                build()
+            path = ref_so_path()
         if not os.path.exists(path):
             raise FileNotFoundError(f"{path} missing: build it where /root/reference exists")
+        self.path = path
+        self.march = "native" if path == REF_NATIVE_SO else "x86-64-v3"
         self.lib = C.CDLL(path)
         self.lib.ref_last_error.restype = C.c_char_p
 

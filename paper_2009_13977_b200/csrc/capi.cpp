@@ -1555,6 +1555,74 @@ fasth_status fasth_forward_backward_host(fasth_ctx c, const float* V, int d, int
     return host_step_impl(c, V, d, n, X, G, m, block_width, Y, dX, dV);
 }
 
+// ---- WY internals (wy.hpp:56-170) -------------------------------------------
+namespace {
+fasth_status wy_compact_impl(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int bw, float* W, int64_t ldw,
+                             float* Y, int64_t ldy) {
+    TRY(check_mat("wy_compact: V", V, ldv, d, n));
+    TRY(check_mat("wy_compact: W", W, ldw, d, n));
+    TRY(check_mat("wy_compact: Y", Y, ldy, d, n));
+    double* scratch = nullptr;
+    TRY(c->alloc_n(wy_compact_scratch_doubles(n, bw), &scratch));
+    fasth_status s = c->timed(
+        [&] { return launch_wy_compact(V, ldv, d, n, bw, scratch, W, ldw, Y, ldy, c->err_d, 0, c->stream); },
+        "wy_compact");
+    c->release(scratch);  // pool reuse is stream ordered
+    TRY(s);
+    return c->finish();
+}
+
+fasth_status wy_apply_impl(fasth_ctx c, const char* what, const float* A, int64_t lda, const float* Bm, int64_t ldb,
+                           int d, int b, const float* X, int64_t ldx, int m, float* out, int64_t ldo) {
+    if (d < 1 || b < 1 || m < 0) return fail(FASTH_ERR_DIMENSION, "%s: bad shape (d %d, width %d, m %d)", what, d, b, m);
+    TRY(check_mat(what, A, lda, d, b));
+    TRY(check_mat(what, Bm, ldb, d, b));
+    TRY(check_mat(what, X, ldx, d, m));
+    TRY(check_mat(what, out, ldo, d, m));
+    if (m == 0) return FASTH_OK;
+    double* T = nullptr;
+    TRY(c->alloc_n((size_t)b * m, &T));
+    fasth_status s =
+        c->timed([&] { return launch_wy_apply(A, lda, Bm, ldb, d, b, X, ldx, m, T, out, ldo, c->stream); }, what);
+    c->release(T);
+    TRY(s);
+    return c->finish();
+}
+}  // namespace
+
+fasth_status fasth_wy_compact(fasth_ctx c, const float* V, int64_t ldv, int d, int b, float* W, int64_t ldw,
+                              float* Y, int64_t ldy) {
+    DeviceGuard dg_(dev_of(c));
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (b < 1) return fail(FASTH_ERR_INVALID, "wy_compact: empty vector list");
+    if (d < 1) return fail(FASTH_ERR_DIMENSION, "wy_compact: dim must be >= 1");
+    return wy_compact_impl(c, V, ldv, d, b, b, W, ldw, Y, ldy);
+}
+
+fasth_status fasth_compact_chain(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int block_width, float* W,
+                                 int64_t ldw, float* Y, int64_t ldy) {
+    DeviceGuard dg_(dev_of(c));
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (d < 1 || n < 0) return fail(FASTH_ERR_DIMENSION, "compact_chain: bad shape");
+    if (block_width < 1 || block_width > n)
+        return fail(FASTH_ERR_INVALID, "compact_chain: block width %d outside [1, %d]", block_width, n);
+    return wy_compact_impl(c, V, ldv, d, n, block_width, W, ldw, Y, ldy);
+}
+
+fasth_status fasth_wy_apply(fasth_ctx c, const float* W, int64_t ldw, const float* Y, int64_t ldy, int d, int b,
+                            const float* X, int64_t ldx, int m, float* out, int64_t ldo) {
+    DeviceGuard dg_(dev_of(c));
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    return wy_apply_impl(c, "wy_apply", W, ldw, Y, ldy, d, b, X, ldx, m, out, ldo);
+}
+
+fasth_status fasth_wy_apply_transpose(fasth_ctx c, const float* W, int64_t ldw, const float* Y, int64_t ldy, int d,
+                                      int b, const float* X, int64_t ldx, int m, float* out, int64_t ldo) {
+    DeviceGuard dg_(dev_of(c));
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    return wy_apply_impl(c, "wy_apply_transpose", Y, ldy, W, ldw, d, b, X, ldx, m, out, ldo);
+}
+
 // ---- SVD layer -------------------------------------------------------------
 fasth_status svd_forward_impl(fasth_ctx c, const fasth_svd_param* p, fasth_svd_plan plan, const float* X,
                               int64_t ldx, int m, int block_width, float* Y, int64_t ldy, fasth_svd_tape* tape);

@@ -177,6 +177,15 @@ int sweep_ldv(int BS);  // row pitch of Vbl blocks and Sf / Sb
 int sweep2_nstg(int C, int BS, int d_pad);  // 0 = geometry not supported by the v2 kernel
 size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg);
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
+// wy_api.cu: the reference's WY internals (wy.hpp:56-170) in its own layout
+// W, Y (column-major d x n, block z = columns [z bw, z bw + w_z)); scratch of
+// wy_compact_scratch_doubles(n, bw) doubles; T of b * m doubles for wy_apply
+// (out = X - 2 A (B^T X): wy_apply is A = W, B = Y; the transpose A = Y, B = W)
+cudaError_t launch_wy_compact(const float* V, int64_t ldv, int d, int n, int bw, double* scratch, float* W,
+                              int64_t ldw, float* Y, int64_t ldy, ErrWord* err, int tag, cudaStream_t s);
+size_t wy_compact_scratch_doubles(int n, int bw);
+cudaError_t launch_wy_apply(const float* A, int64_t lda, const float* Bm, int64_t ldb, int d, int b,
+                            const float* X, int64_t ldx, int m, double* T, float* out, int64_t ldo, cudaStream_t s);
 // chain_panel.cu (large batch: one CTA per 16-column panel, all rows)
 bool panel_supported(int BS, int d_pad, int m);
 cudaError_t launch_panel(const SweepV2Args& a, cudaStream_t s);

@@ -17,6 +17,12 @@ reference (file:line)                  here
 ``apply_exponential`` matops.hpp:98    ``apply_exponential(p, X, block_width)``
 ``apply_cayley`` matops.hpp:107        ``apply_cayley(p, X, block_width)``
 ``log_abs_det`` matops.hpp:57          ``log_abs_det(p)``
+``wy_compact`` wy.hpp:56               ``wy_compact(vectors)``
+``wy_apply`` wy.hpp:104                ``wy_apply(block, X)``
+``wy_apply_transpose`` wy.hpp:137      ``wy_apply_transpose(block, X)``
+``compact_chain`` wy.hpp:151           ``compact_chain(V, block_width)``
+``TapeForward::compacted`` /           ``Tape.compacted`` / ``Tape.activations``
+``::activations`` fasth.hpp:22-29      (materialised on first access)
 =====================================  ==========================================
 
 Shapes follow the reference: a chain is an ``(n, d)`` tensor (row k = v_k,
@@ -243,17 +249,133 @@ def _ptr(t):
 # ---- FastH (fasth.hpp) ------------------------------------------------------
 
 
-class Tape:
-    """TapeForward (fasth.hpp:22-29): an opaque device record (compacted WY
-    blocks + per-block activations)."""
+@dataclass
+class WYBlock:
+    """WYBlock (wy.hpp:18-25): I - 2 W Y^T = H_1 ... H_width.  W and Y are
+    (dim, width) views of column-major device storage; source_vectors is the
+    (width, dim) slice of the chain."""
+    dim: int
+    width: int
+    W: torch.Tensor
+    Y: torch.Tensor
+    source_vectors: torch.Tensor
+    sequential_steps: int = 0
 
-    def __init__(self, ctx: Context, handle, output: torch.Tensor, d: int, n: int, m: int, b: int):
+
+@dataclass
+class CompactedChain:
+    """CompactedChain (wy.hpp:29-48)."""
+    dim: int
+    block_width: int
+    blocks: list
+
+    def factor_count(self) -> int:
+        return sum(b.width for b in self.blocks)
+
+    def compaction_stages(self) -> int:
+        return max((b.sequential_steps for b in self.blocks), default=0)
+
+
+def _blocks(V, W, Y, d, n, bw):
+    return [WYBlock(d, min(bw, n - lo), W[lo:lo + bw].t(), Y[lo:lo + bw].t(), V[lo:lo + bw],
+                    min(bw, n - lo)) for lo in range(0, n, bw)]
+
+
+def compact_chain(V: torch.Tensor, block_width: int, *, ctx: Context | None = None) -> CompactedChain:
+    """wy.hpp:151 — the chain (n, d) as ceil(n / block_width) WY blocks (the last ragged)."""
+    V, n, d, ldv = _chain(V, "compact_chain: V")
+    if not 1 <= int(block_width) <= n:
+        raise Error(f"compact_chain: block width {block_width} outside [1, {n}]")
+    c = _ctx(ctx, V)
+    W = torch.empty((n, d), dtype=torch.float32, device=V.device)
+    Y = torch.empty((n, d), dtype=torch.float32, device=V.device)
+    _check(c.lib.fasth_compact_chain(c.h, _ptr(V), ldv, d, n, int(block_width), _ptr(W), d, _ptr(Y), d))
+    return CompactedChain(d, int(block_width), _blocks(V, W, Y, d, n, int(block_width)))
+
+
+def wy_compact(vectors: torch.Tensor, *, ctx: Context | None = None) -> WYBlock:
+    """wy.hpp:56 — (W, Y) of the b >= 1 vectors (rows of ``vectors``)."""
+    if vectors.dim() != 2 or vectors.shape[0] == 0:
+        raise Error("wy_compact: empty vector list")
+    V, n, d, ldv = _chain(vectors, "wy_compact: vectors")
+    c = _ctx(ctx, V)
+    W = torch.empty((n, d), dtype=torch.float32, device=V.device)
+    Y = torch.empty((n, d), dtype=torch.float32, device=V.device)
+    _check(c.lib.fasth_wy_compact(c.h, _ptr(V), ldv, d, n, _ptr(W), d, _ptr(Y), d))
+    return _blocks(V, W, Y, d, n, n)[0]
+
+
+def _wy_apply(fn, block: WYBlock, X, ctx, out=None):
+    X, ldx = _colmajor(X, fn)
+    d, m = X.shape
+    if d != block.dim:
+        raise DimensionError(f"{fn}: X has {d} rows, block dim {block.dim}")
+    c = _ctx(ctx, X)
+    W, ldw = _colmajor(block.W, fn)
+    Y, ldy = _colmajor(block.Y, fn)
+    O = _new_out(d, m, X) if out is None else out
+    _check(getattr(c.lib, "fasth_" + fn)(c.h, _ptr(W), ldw, _ptr(Y), ldy, d, block.width, _ptr(X), ldx, m,
+                                          _ptr(O), _out_ld(O, d, m, "out")))
+    return O
+
+
+def wy_apply(block: WYBlock, X: torch.Tensor, *, ctx: Context | None = None) -> torch.Tensor:
+    """wy.hpp:104 — X - 2 W (Y^T X)."""
+    return _wy_apply("wy_apply", block, X, ctx)
+
+
+def wy_apply_transpose(block: WYBlock, X: torch.Tensor, *, ctx: Context | None = None) -> torch.Tensor:
+    """wy.hpp:137 — X - 2 Y (W^T X)."""
+    return _wy_apply("wy_apply_transpose", block, X, ctx)
+
+
+class Tape:
+    """TapeForward (fasth.hpp:22-29): the device record the backward runs
+    from, plus the reference's members ``compacted`` (the WY blocks) and
+    ``activations`` (A_1..A_{q+1}: ``activations[q]`` is X, ``[0]`` the
+    output), materialised on first access by compact_chain and the block
+    recurrence A_i = wy_apply(P_i, A_{i+1}) (fasth.hpp:55-59)."""
+
+    def __init__(self, ctx: Context, handle, output: torch.Tensor, d: int, n: int, m: int, b: int,
+                 V: torch.Tensor | None = None, X: torch.Tensor | None = None):
         self.ctx, self.h = ctx, handle
         self._output = output
         self.d, self.n, self.m, self.block_width = d, n, m, b
+        self._V, self._X = V, X
+        self._compacted = self._activations = None
 
     def output(self) -> torch.Tensor:
         return self._output
+
+    def input(self) -> torch.Tensor:
+        return self._X
+
+    def _materialise(self):
+        if self._compacted is not None:
+            return
+        if self._X is None:
+            raise Error("Tape: recorded without its input (record=False)")
+        bw = min(max(self.block_width, 1), max(self.n, 1))
+        if self.n == 0:
+            self._compacted = CompactedChain(self.d, self.block_width, [])
+            self._activations = [self._X]
+            return
+        cc = compact_chain(self._V, bw, ctx=self.ctx)
+        acts = [None] * (len(cc.blocks) + 1)
+        acts[-1] = self._X
+        for i in reversed(range(len(cc.blocks))):
+            acts[i] = wy_apply(cc.blocks[i], acts[i + 1], ctx=self.ctx)
+        self._compacted, self._activations = cc, acts
+
+    @property
+    def compacted(self) -> CompactedChain:
+        self._materialise()
+        return self._compacted
+
+    @property
+    def activations(self) -> list:
+        self._materialise()
+        return self._activations
 
     def block_count(self) -> int:
         q = C.c_int()
@@ -290,7 +412,7 @@ def fasth_forward(V: torch.Tensor, X: torch.Tensor, block_width: int, *, ctx: Co
     h = C.c_void_p()
     _check(c.lib.fasth_forward(c.h, _ptr(V), ldv, d, n, _ptr(X), ldx, m, int(block_width),
                                _ptr(Y), ldy, C.byref(h) if record else None))
-    return Tape(c, h if record else None, Y, d, n, m, int(block_width))
+    return Tape(c, h if record else None, Y, d, n, m, int(block_width), V, X)
 
 
 def fasth_backward(tape: Tape, G: torch.Tensor, *, want_vectors: bool = True) -> BackwardResult:

@@ -188,6 +188,197 @@ int main() {
             report(nm + " dV", rel_vecs(gb.grad_V_vectors, gr.grad_V_vectors), tol);
         }
     }
+    // 6. WY internals and the tape's reference members (test_wy.cpp:27-153,
+    //    test_fasth.cpp:39-50) through fasth_b200::, fp32 tolerances in place
+    //    of the reference's f64 ones, exact checks kept exact
+    {
+        auto dense_wy = [](const B::WYBlock& b) {  // I - 2 W Y^T (test_wy.cpp:13-22)
+            B::Matrix p = B::Matrix::identity(b.dim);
+            for (std::size_t i = 0; i < b.dim; ++i)
+                for (std::size_t j = 0; j < b.dim; ++j) {
+                    double acc = 0.0;
+                    for (std::size_t k = 0; k < b.width; ++k) acc += b.W(i, k) * b.Y(j, k);
+                    p(i, j) -= 2.0 * acc;
+                }
+            return p;
+        };
+        auto matmul = [](const B::Matrix& a, const B::Matrix& b) {
+            B::Matrix c(a.rows(), b.cols());
+            for (std::size_t i = 0; i < a.rows(); ++i)
+                for (std::size_t k = 0; k < a.cols(); ++k)
+                    for (std::size_t j = 0; j < b.cols(); ++j) c(i, j) += a(i, k) * b(k, j);
+            return c;
+        };
+        auto transpose = [](const B::Matrix& a) {
+            B::Matrix t(a.cols(), a.rows());
+            for (std::size_t i = 0; i < a.rows(); ++i)
+                for (std::size_t j = 0; j < a.cols(); ++j) t(j, i) = a(i, j);
+            return t;
+        };
+        auto chain_dense = [](const R::HouseholderChain& c) {
+            return R::chain_apply_sequential(c, R::Matrix::identity(c.dim()));
+        };
+        const double wtol = 1e-5;
+        // test_fasth.cpp:39-50: tape activations satisfy the block recurrence (bitwise)
+        {
+            std::mt19937_64 rng(109);
+            auto chain = R::bench::random_chain(12, 12, rng);
+            auto X = R::bench::random_matrix(12, 3, rng);
+            auto tape = B::fasth_forward(to_b(chain), to_b(X), 5);
+            auto rt = R::fasth_forward(chain, X, 5);
+            expect("tape: activations.size() == block_count() + 1 == 4",
+                   tape.activations.size() == tape.block_count() + 1 && tape.block_count() == 3);
+            expect("tape: input() == X", tape.input() == to_b(X));
+            bool exact = true;
+            for (std::size_t i = 0; i < tape.block_count(); ++i) {
+                auto again = B::wy_apply(tape.compacted.blocks[i], tape.activations[i + 1]);
+                exact = exact && B::relative_error(tape.activations[i], again) == 0.0;
+            }
+            expect("tape: activations[i] == wy_apply(blocks[i], activations[i+1]) bitwise", exact);
+            double ea = 0, ew = 0;
+            for (std::size_t i = 0; i <= rt.block_count(); ++i) ea = std::max(ea, rel(tape.activations[i], rt.activations[i]));
+            for (std::size_t i = 0; i < rt.block_count(); ++i) {
+                ew = std::max(ew, rel(tape.compacted.blocks[i].W, rt.compacted.blocks[i].W));
+                ew = std::max(ew, rel(tape.compacted.blocks[i].Y, rt.compacted.blocks[i].Y));
+            }
+            report("tape activations vs reference", ea, wtol);
+            report("tape compacted W, Y vs reference", ew, wtol);
+            report("tape output vs reference", rel(tape.output(), rt.output()), wtol);
+        }
+        // test_wy.cpp:27-35 single factor: W = Y = v / ||v||
+        {
+            auto blk = B::wy_compact({B::HouseholderVector(std::vector<double>{3.0, 4.0})}, 2);
+            expect("wy_compact single factor W = Y = (0.6, 0.8)",
+                   std::fabs(blk.W(0, 0) - 0.6) < 1e-7 && std::fabs(blk.W(1, 0) - 0.8) < 1e-7 &&
+                       std::fabs(blk.Y(0, 0) - 0.6) < 1e-7);
+        }
+        // test_wy.cpp:37-46 axis vectors
+        {
+            auto blk = B::wy_compact({B::HouseholderVector(std::vector<double>{1.0, 0.0, 0.0}),
+                                      B::HouseholderVector(std::vector<double>{0.0, 1.0, 0.0})},
+                                     3);
+            auto pm = dense_wy(blk);
+            expect("wy_compact b=2 axis vectors: diag(-1, -1, 1)",
+                   std::fabs(pm(0, 0) + 1) < 1e-7 && std::fabs(pm(1, 1) + 1) < 1e-7 &&
+                       std::fabs(pm(2, 2) - 1) < 1e-7 && std::fabs(pm(0, 1)) < 1e-7);
+        }
+        // test_wy.cpp:48-53 dense product; W, Y against the reference's wy_compact
+        {
+            std::mt19937_64 rng(41);
+            auto chain = R::bench::random_chain(16, 4, rng);
+            auto rb = R::wy_compact(chain.vectors(), 16);
+            auto bb = B::wy_compact(to_b(chain).vectors(), 16);
+            R::Matrix dense = chain_dense(chain);
+            report("wy_compact == dense Householder product", rel(dense_wy(bb), dense), wtol);
+            report("wy_compact W vs reference", rel(bb.W, rb.W), wtol);
+            report("wy_compact Y vs reference", rel(bb.Y, rb.Y), wtol);
+        }
+        // test_wy.cpp:55-62 empty list; stage count
+        {
+            bool threw = false;
+            try {
+                B::wy_compact({}, 4);
+            } catch (const B::Error&) {
+                threw = true;
+            }
+            expect("wy_compact rejects an empty vector list", threw);
+            std::mt19937_64 rng(43);
+            bool st = true;
+            for (std::size_t b : {1, 3, 7})
+                st = st && B::wy_compact(to_b(R::bench::random_chain(8, b, rng)).vectors(), 8).sequential_steps == b;
+            expect("wy_compact sequential_steps == b", st);
+        }
+        // test_wy.cpp:64-70 wy_apply vs the sequential application
+        {
+            std::mt19937_64 rng(47);
+            auto chain = R::bench::random_chain(32, 8, rng);
+            auto blk = B::wy_compact(to_b(chain).vectors(), 32);
+            auto x = R::bench::random_matrix(32, 4, rng);
+            report("wy_apply == sequential application", rel(B::wy_apply(blk, to_b(x)),
+                                                             R::chain_apply_sequential(chain, x)), wtol);
+        }
+        // test_wy.cpp:72-84 single factor, zero input, dimension error
+        {
+            std::mt19937_64 rng(53);
+            R::HouseholderVector v(R::bench::random_matrix(6, 1, rng).data());
+            auto blk = B::wy_compact({B::HouseholderVector(v.coeffs())}, 6);
+            auto x = R::bench::random_matrix(6, 3, rng);
+            report("wy_apply single factor == householder_apply_left",
+                   rel(B::wy_apply(blk, to_b(x)), R::householder_apply_left(v, x)), wtol);
+            auto mapped = B::wy_apply(blk, B::Matrix(6, 2));
+            bool zero = true;
+            for (double e : mapped.data()) zero = zero && e == 0.0;
+            expect("wy_apply of zero is zero", zero);
+            bool threw = false;
+            try {
+                B::wy_apply(blk, B::Matrix(5, 2));
+            } catch (const B::DimensionError&) {
+                threw = true;
+            }
+            expect("wy_apply DimensionError on row mismatch", threw);
+        }
+        // test_wy.cpp:86-105 transpose properties
+        {
+            std::mt19937_64 rng(59);
+            R::HouseholderVector v(R::bench::random_matrix(8, 1, rng).data());
+            auto single = B::wy_compact({B::HouseholderVector(v.coeffs())}, 8);
+            auto x = to_b(R::bench::random_matrix(8, 3, rng));
+            report("wy_apply_transpose == wy_apply for one factor",
+                   B::relative_error(B::wy_apply_transpose(single, x), B::wy_apply(single, x)), wtol);
+            auto blk = B::wy_compact(to_b(R::bench::random_chain(24, 6, rng)).vectors(), 24);
+            auto y = to_b(R::bench::random_matrix(24, 5, rng));
+            report("P^T P y == y", B::relative_error(B::wy_apply_transpose(blk, B::wy_apply(blk, y)), y), wtol);
+            auto small = B::wy_compact(to_b(R::bench::random_chain(12, 4, rng)).vectors(), 12);
+            auto pt = B::wy_apply_transpose(small, B::Matrix::identity(12));
+            report("wy_apply_transpose(I) == wy_apply(I)^T",
+                   B::relative_error(pt, transpose(B::wy_apply(small, B::Matrix::identity(12)))), wtol);
+        }
+        // test_wy.cpp:107-114 orthogonality of the dense block
+        {
+            std::mt19937_64 rng(61);
+            double e = 0;
+            for (std::size_t d : {16, 64, 128}) {
+                auto blk = B::wy_compact(to_b(R::bench::random_chain(d, 8, rng)).vectors(), d);
+                auto pm = dense_wy(blk);
+                e = std::max(e, B::relative_error(matmul(transpose(pm), pm), B::Matrix::identity(d)));
+            }
+            report("WY blocks orthogonal as dense matrices", e, wtol);
+        }
+        // test_wy.cpp:116-133 partition arithmetic; :135-143 pure repartition
+        {
+            std::mt19937_64 rng(67);
+            auto chain = to_b(R::bench::random_chain(8, 8, rng));
+            auto one = B::compact_chain(chain, 8);
+            auto rag = B::compact_chain(chain, 3);
+            expect("compact_chain(8): one block of width 8", one.blocks.size() == 1 && one.blocks[0].width == 8);
+            expect("compact_chain(3): widths 3, 3, 2", rag.blocks.size() == 3 && rag.blocks[0].width == 3 &&
+                                                           rag.blocks[1].width == 3 && rag.blocks[2].width == 2);
+            int thrown = 0;
+            for (std::size_t bw : {0, 9}) try {
+                    B::compact_chain(chain, bw);
+                } catch (const B::Error&) {
+                    ++thrown;
+                }
+            expect("compact_chain rejects widths 0 and 9", thrown == 2);
+            std::mt19937_64 rng2(71);
+            auto c10 = to_b(R::bench::random_chain(10, 10, rng2));
+            auto cc = B::compact_chain(c10, 4);
+            std::size_t idx = 0;
+            bool same = true;
+            for (const auto& blk : cc.blocks)
+                for (const auto& v : blk.source_vectors) same = same && v.coeffs() == c10[idx++].coeffs();
+            expect("compact_chain is a pure repartition (bitwise)", same && idx == c10.size());
+        }
+        // test_wy.cpp:145-152 product of compacted blocks == chain product
+        {
+            std::mt19937_64 rng(73);
+            auto chain = R::bench::random_chain(16, 16, rng);
+            auto cc = B::compact_chain(to_b(chain), 4);
+            B::Matrix prod = B::Matrix::identity(16);
+            for (const auto& blk : cc.blocks) prod = matmul(prod, dense_wy(blk));
+            report("product of compacted blocks == chain product", rel(prod, chain_dense(chain)), wtol);
+        }
+    }
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "ALL PASSED", g_fail);
     return g_fail ? 1 : 0;
 }
