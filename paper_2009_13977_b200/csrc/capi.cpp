@@ -401,6 +401,10 @@ int next_pow2_min16(int x) {
 // wider blocks run as 64-wide (32-wide when d is large, to keep the chain
 // kernel's shared-memory stages in budget) sub-blocks: the same product.
 int internal_b(int d, int n, int b_user) {
+    // FASTH_INTERNAL_BS: the chain kernels' block width regardless of the
+    // caller's (the product does not depend on the blocking) — A/B knob
+    if (const char* e = getenv("FASTH_INTERNAL_BS"))
+        return std::max(1, std::min({atoi(e), kMaxBS, std::max(n, 1)}));
     const int b = std::min(std::max(b_user, 1), n);
     // 64-wide blocks only at d <= 512, 16-wide beyond d = 2048: past those
     // sizes the chain kernel's stages and exchange slots no longer fit shared
