@@ -1441,10 +1441,23 @@ fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, 
         if (xm && gm && ym && dxm) {
             x = const_cast<float*>(xm), g = const_cast<float*>(gm);
             y = const_cast<float*>(ym), dx = const_cast<float*>(dxm);
-            if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
+            // V in: an SM copy kernel over the pinned buffer's mapping (more
+            // PCIe reads in flight than the copy engine keeps: host_io.cu);
+            // FASTH_H2D=dma for cudaMemcpyAsync
+            const float* vm = mapped(V);
+            const char* h2d = getenv("FASTH_H2D");
+            if (nv && vm && !(h2d && !strcmp(h2d, "dma")))
+                TRY(c->timed([&] { return launch_stream_copy(vm, v, (int64_t)nv, c->num_sms, c->stream); }, "h2d_copy"));
+            else if (nv)
+                CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
             TRY(fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d, n ? dv : nullptr,
                                        d));
-            if (nv) CU(cudaMemcpyAsync(dV, dv, nv * 4, cudaMemcpyDeviceToHost, c->stream));
+            float* dvm = const_cast<float*>(mapped(dV));
+            const char* d2h = getenv("FASTH_D2H");
+            if (nv && dvm && d2h && !strcmp(d2h, "kernel"))
+                TRY(c->timed([&] { return launch_stream_copy(dv, dvm, (int64_t)nv, c->num_sms, c->stream); }, "d2h_copy"));
+            else if (nv)
+                CU(cudaMemcpyAsync(dV, dv, nv * 4, cudaMemcpyDeviceToHost, c->stream));
             return FASTH_OK;
         }
     }

@@ -51,7 +51,8 @@ if __name__ == "__main__":
     X = torch.randn(m, d, device="cuda").t()
     G = torch.randn(m, d, device="cuda").t()
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
-    for variant in ["", "FASTH_NO_PIPELINE", "FASTH_BUILD_V1", "FASTH_DV_V1", "FASTH_SWEEP_V1"]:
+    variants = os.environ.get("KT_VARIANTS", ",FASTH_NO_PIPELINE,FASTH_BUILD_V1,FASTH_DV_V1,FASTH_SWEEP_V1").split(",")
+    for variant in variants:
         if variant:
             os.environ[variant] = "1"
         ctx = fb.Context(0, deferred=True)
