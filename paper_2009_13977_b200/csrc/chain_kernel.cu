@@ -475,7 +475,10 @@ SweepGeom pick_geometry(int d, int m, int BS, int num_sms) {
     if (C < 1 || C > 16) C = 8;
     auto rc_of = [&](int c) { return ((d + c - 1) / c + 15) / 16 * 16; };
     constexpr size_t kBudget = 220 * 1024;
-    while (C < 16 && (sweep_smem_bytes(C, WC, BS, C * rc_of(C), 3) > kBudget || rc_of(C) > 256)) ++C;
+    // the packed-stage sweep (chain_v2.cu) fits as chosen: keep C (the v1
+    // kernel's larger footprint must not widen the cluster past the GPC fit)
+    const bool v2_fits = rc_of(C) <= 256 && sweep2_nstg(C, BS, C * rc_of(C)) >= 2;
+    while (!v2_fits && C < 16 && (sweep_smem_bytes(C, WC, BS, C * rc_of(C), 3) > kBudget || rc_of(C) > 256)) ++C;
     // the packed-stage sweep (chain_v2.cu) must fit: widen the cluster if not
     for (int c2 = C; c2 <= 16; ++c2)
         if (sweep2_nstg(c2, BS, c2 * rc_of(c2)) >= 2) {
