@@ -248,6 +248,12 @@ fasth_status fasth_apply_exponential(fasth_ctx ctx, const fasth_svd_param* p, co
 fasth_status fasth_apply_cayley(fasth_ctx ctx, const fasth_svd_param* p, const float* X,
                                 int64_t ldx, int m, int block_width, float* Y, int64_t ldy);
 fasth_status fasth_log_abs_det(fasth_ctx ctx, const fasth_svd_param* p, double* out);
+/* apply_pseudo_inverse (matops.hpp:158): Y = V Sigma^+ U^T X, rectangular
+ * parameters allowed: X is out_dim x m, Y in_dim x m; Sigma^+ reciprocates
+ * entries with |sigma| > tol and zeroes the rest.  FASTH_ERR_INVALID for
+ * tol < 0. */
+fasth_status fasth_apply_pseudo_inverse(fasth_ctx ctx, const fasth_svd_param* p, const float* X, int64_t ldx,
+                                        int m, double tol, int block_width, float* Y, int64_t ldy);
 
 /* ---- OSVD checkpoints (svd_layer.hpp:204-290) -------------------------------
  * The reference's flat little-endian format: "OSVD", version u32 (= 1),

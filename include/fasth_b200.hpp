@@ -652,6 +652,19 @@ inline Matrix apply_exponential(const SvdParam& p, const Matrix& X, std::size_t 
 inline Matrix apply_cayley(const SvdParam& p, const Matrix& X, std::size_t block_width) {
     return detail::sigma_op(fasth_apply_cayley, p, X, block_width);
 }
+/// matops.hpp:158 — W^+ X = V Sigma^+ U^T X (rectangular allowed).
+inline Matrix apply_pseudo_inverse(const SvdParam& p, const Matrix& X, double tol, std::size_t block_width) {
+    if (tol < 0.0) throw Error("apply_pseudo_inverse: negative tolerance");
+    if (X.rows() != p.out_dim) throw DimensionError("apply_pseudo_inverse: X row count mismatch");
+    detail::DeviceParam dp(p);
+    const std::size_t m = X.cols();
+    DeviceBuffer Xd(p.out_dim * m), Yd(p.in_dim * m);
+    Xd.upload(X.to_device_layout());
+    check(fasth_apply_pseudo_inverse(Device::ctx(), &dp.c, Xd.get(), (int64_t)std::max<std::size_t>(p.out_dim, 1),
+                                     (int)m, tol, (int)block_width, Yd.get(),
+                                     (int64_t)std::max<std::size_t>(p.in_dim, 1)));
+    return Matrix::from_device_layout(p.in_dim, m, Yd.download(p.in_dim * m));
+}
 /// matops.hpp:57
 inline double log_abs_det(const SvdParam& p) {
     detail::DeviceParam dp(p);

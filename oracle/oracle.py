@@ -360,6 +360,15 @@ class Ref:
                                      _p(sigma), _p(X), _p(Y)))
         return Y
 
+    def pinv(self, U, V, sigma, X, tol, b, out_dim, in_dim):
+        """apply_pseudo_inverse (matops.hpp:158): X (out_dim, m) -> (in_dim, m)."""
+        U, V, sigma, X = map(_f64, (U, V, sigma, X))
+        Y = np.empty((in_dim, X.shape[1]))
+        self._chk(self.lib.ref_pinv(_SZ(out_dim), _SZ(in_dim), _SZ(U.shape[0]), _SZ(V.shape[0]), _SZ(X.shape[1]),
+                                    _SZ(b), C.c_double(tol), _p(U) if U.size else None, _p(V) if V.size else None,
+                                    _p(sigma), _p(X), _p(Y)))
+        return Y
+
     def log_abs_det(self, sigma):
         sigma = _f64(sigma)
         out = C.c_double()

@@ -321,6 +321,15 @@ int ref_matop(int kind, std::size_t d, std::size_t nu, std::size_t nv, std::size
     });
 }
 
+/// apply_pseudo_inverse (matops.hpp:158), rectangular: X out x m -> Y in x m.
+int ref_pinv(std::size_t out, std::size_t in, std::size_t nu, std::size_t nv, std::size_t m, std::size_t b,
+             double tol, const double* U, const double* V, const double* sigma, const double* X, double* Y) {
+    return guarded([&] {
+        SvdParam p = param_in(out, in, nu, nv, U, V, sigma);
+        mat_out(apply_pseudo_inverse(p, mat_in(out, m, X), tol, b), Y);
+    });
+}
+
 int ref_log_abs_det(std::size_t d, const double* sigma, double* out) {
     return guarded([&] {
         SvdParam p;

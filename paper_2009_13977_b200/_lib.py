@@ -76,6 +76,8 @@ SIGNATURES = {
     "fasth_svd_save": (C.c_int, [VP, C.POINTER(SvdParamC), C.c_char_p]),
     "fasth_tune_block_width": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.c_uint64, C.POINTER(C.c_int)]),
     "fasth_log_abs_det": (C.c_int, [VP, C.POINTER(SvdParamC), C.POINTER(C.c_double)]),
+    "fasth_apply_pseudo_inverse": (C.c_int, [VP, C.POINTER(SvdParamC), VP, I64, C.c_int, C.c_double, C.c_int, VP,
+                                             I64]),
     "fasth_wy_compact": (C.c_int, [VP, VP, I64, C.c_int, C.c_int, VP, I64, VP, I64]),
     "fasth_compact_chain": (C.c_int, [VP, VP, I64, C.c_int, C.c_int, C.c_int, VP, I64, VP, I64]),
     "fasth_wy_apply": (C.c_int, [VP, VP, I64, VP, I64, C.c_int, C.c_int, VP, I64, C.c_int, VP, I64]),

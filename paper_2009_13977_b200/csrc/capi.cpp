@@ -2175,6 +2175,39 @@ fasth_status fasth_apply_cayley(fasth_ctx c, const fasth_svd_param* p, const flo
     return sigma_op(c, p, X, ldx, m, b, Y, ldy, 3, "apply_cayley");
 }
 
+// matops.hpp:158-175: W^+ X = V (Sigma^+ (U^T X)), rectangular allowed: X is
+// out_dim x m, Y in_dim x m; Sigma^+ reciprocates |sigma| > tol, zeroes the
+// rest, and maps the out_dim rows onto in_dim rows (zero past min_dim).
+fasth_status fasth_apply_pseudo_inverse(fasth_ctx c, const fasth_svd_param* p, const float* X, int64_t ldx, int m,
+                                        double tol, int b, float* Y, int64_t ldy) {
+    DeviceGuard dg_(dev_of(c));
+    if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    if (!(tol >= 0.0)) return fail(FASTH_ERR_INVALID, "apply_pseudo_inverse: negative tolerance");
+    TRY(check_param("apply_pseudo_inverse", p));
+    if (m < 0) return fail(FASTH_ERR_DIMENSION, "apply_pseudo_inverse: negative batch");
+    const int out = p->out_dim, in = p->in_dim, k = std::min(out, in);
+    TRY(check_mat("apply_pseudo_inverse: X", X, ldx, out, m));
+    TRY(check_mat("apply_pseudo_inverse: Y", Y, ldy, in, m));
+    float* f = nullptr;
+    float* t = nullptr;
+    TRY(c->alloc_n((size_t)std::max(k, 1), &f));
+    fasth_status s = c->alloc_n((size_t)out * std::max(m, 1), &t);
+    do {
+        if (s) break;
+        s = c->timed([&] { return launch_sigma_map(p->sigma, k, 4, f, c->err_d, c->stream, (float)tol); },
+                     "sigma_map");
+        if (s || m == 0) break;
+        // U^T X (the reversed U chain, matops.hpp:166), then V (Sigma^+ t) (:174)
+        s = apply_chain(c, p->U, p->ldu, out, p->nu, 1, 0, X, ldx, out, nullptr, m, b, t, out);
+        if (s) break;
+        s = apply_chain(c, p->V, p->ldv, in, p->nv, 0, 1, t, out, k, f, m, b, Y, ldy);
+    } while (0);
+    c->release(f);
+    c->release(t);
+    if (s == FASTH_OK) s = c->finish();
+    return s;
+}
+
 fasth_status fasth_log_abs_det(fasth_ctx c, const fasth_svd_param* p, double* out) {
     DeviceGuard dg_(dev_of(c));
     if (!c || !out) return fail(FASTH_ERR_INVALID, "null argument");

@@ -207,7 +207,7 @@ cudaError_t launch_step(const float* P, int64_t ldp, const float* dP, int64_t ld
 cudaError_t launch_sigma_step(const float* sigma, const float* dsigma, int k, float eta,
                               float clamp_eps, float* out, cudaStream_t s);
 cudaError_t launch_sigma_map(const float* sigma, int k, int kind, float* out, ErrWord* err,
-                             cudaStream_t s);
+                             cudaStream_t s, float tol = 0.f);
 cudaError_t launch_logdet(const float* sigma, int k, double* out, ErrWord* err,
                           cudaStream_t s);
 

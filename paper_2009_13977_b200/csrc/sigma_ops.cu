@@ -126,7 +126,7 @@ __global__ void sigma_step_kernel(const float* sigma, const float* dsigma, int k
     out[i] = s;
 }
 
-__global__ void sigma_map_kernel(const float* sigma, int k, int kind, float* out, ErrWord* err) {
+__global__ void sigma_map_kernel(const float* sigma, int k, int kind, float tol, float* out, ErrWord* err) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
     const float s = sigma[i];
@@ -139,6 +139,8 @@ __global__ void sigma_map_kernel(const float* sigma, int k, int kind, float* out
     } else if (kind == 3) {  // Cayley (1 - s) / (1 + s), pole at -1
         if (s == -1.f) atomicOr(&err->flags, kErrPole);
         f = (1.f - s) / (1.f + s);
+    } else if (kind == 4) {  // pseudo-inverse: 1/sigma where |sigma| > tol, else 0 (matops.hpp:166-167)
+        f = fabsf(s) > tol ? 1.f / s : 0.f;
     }
     out[i] = f;
 }
@@ -207,9 +209,9 @@ cudaError_t launch_sigma_step(const float* sigma, const float* dsigma, int k, fl
 }
 
 cudaError_t launch_sigma_map(const float* sigma, int k, int kind, float* out, ErrWord* err,
-                             cudaStream_t s) {
+                             cudaStream_t s, float tol) {
     if (k == 0) return cudaSuccess;
-    sigma_map_kernel<<<(k + 255) / 256, 256, 0, s>>>(sigma, k, kind, out, err);
+    sigma_map_kernel<<<(k + 255) / 256, 256, 0, s>>>(sigma, k, kind, tol, out, err);
     return cudaGetLastError();
 }
 

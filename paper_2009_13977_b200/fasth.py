@@ -17,6 +17,7 @@ reference (file:line)                  here
 ``apply_exponential`` matops.hpp:98    ``apply_exponential(p, X, block_width)``
 ``apply_cayley`` matops.hpp:107        ``apply_cayley(p, X, block_width)``
 ``log_abs_det`` matops.hpp:57          ``log_abs_det(p)``
+``apply_pseudo_inverse`` matops.hpp:158 ``apply_pseudo_inverse(p, X, tol, bw)``
 ``wy_compact`` wy.hpp:56               ``wy_compact(vectors)``
 ``wy_apply`` wy.hpp:104                ``wy_apply(block, X)``
 ``wy_apply_transpose`` wy.hpp:137      ``wy_apply_transpose(block, X)``
@@ -695,6 +696,23 @@ def apply_exponential(p: SvdParam, X, block_width: int, *, ctx=None):
 def apply_cayley(p: SvdParam, X, block_width: int, *, ctx=None):
     """matops.hpp:107 — (I - W)(I + W)^{-1} X for the symmetric form."""
     return _sigma_op("fasth_apply_cayley", p, X, block_width, ctx)
+
+
+def apply_pseudo_inverse(p: SvdParam, X, tol: float, block_width: int, *, ctx=None):
+    """matops.hpp:158 — W^+ X = V Sigma^+ U^T X (rectangular allowed: X is
+    (out_dim, m), the result (in_dim, m))."""
+    if tol < 0:
+        raise Error("apply_pseudo_inverse: negative tolerance")
+    X, ldx = _colmajor(X, "apply_pseudo_inverse")
+    if X.shape[0] != p.out_dim:
+        raise DimensionError("apply_pseudo_inverse: X row count mismatch")
+    pc = p._c()
+    c = _ctx(ctx, X)
+    m = X.shape[1]
+    Y = _new_out(p.in_dim, m, X)
+    _check(c.lib.fasth_apply_pseudo_inverse(c.h, C.byref(pc), _ptr(X), ldx, m, float(tol), int(block_width), _ptr(Y),
+                                            max(p.in_dim, 1)))
+    return Y
 
 
 def log_abs_det(p: SvdParam, *, ctx=None) -> float:

@@ -186,6 +186,10 @@ int main() {
             report(nm + " Y", rel(Yb, Yr), tol);
             report(nm + " dX", rel(gb.grad_input, gr.grad_input), tol);
             report(nm + " dV", rel_vecs(gb.grad_V_vectors, gr.grad_V_vectors), tol);
+            // matops.hpp:158 on the rectangular parameter
+            auto Xo = R::bench::random_matrix(o, 3, rng);
+            report(nm + " apply_pseudo_inverse", rel(B::apply_pseudo_inverse(pb, to_b(Xo), 0.6, 2),
+                                                     R::apply_pseudo_inverse(p, Xo, 0.6, 2)), tol);
         }
     }
     // 6. WY internals and the tape's reference members (test_wy.cpp:27-153,

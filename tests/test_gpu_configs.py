@@ -249,3 +249,22 @@ def test_ragged_shapes_forced_large_batch(fb, ref, d, n, m, monkeypatch):
     e2 = [rel(a, w) for a, w in zip((tape.output(), two.grad_input, two.grad_vectors), want)]
     record(f"forced large-batch d={d} n={n} m={m}", UX=e[0], dX=e[1], dV=e[2])
     assert max(e + e2) <= TOL, (e, e2)
+
+
+# ---- apply_pseudo_inverse (matops.hpp:158), rectangular ---------------------------
+
+@pytest.mark.parametrize("out_dim,in_dim,m,tol", [(784, 784, 32, 0.0), (96, 64, 8, 0.6), (64, 96, 5, 0.6),
+                                                  (300, 300, 17, 1.0)])
+def test_apply_pseudo_inverse_vs_reference(fb, ref, out_dim, in_dim, m, tol):
+    if not hasattr(ref, "pinv"):
+        pytest.skip("needs oracle/_ref")
+    U, V, s, _, _ = ref.gen_param(7 + out_dim, out_dim, in_dim, out_dim, in_dim, m)
+    X = np.random.default_rng(out_dim + in_dim).standard_normal((out_dim, m))
+    want = ref.pinv(U, V, s, X, tol, 32, out_dim, in_dim)
+    p = fb.SvdParam(out_dim, in_dim, dev(U), dev(V), dev(s))
+    got = fb.apply_pseudo_inverse(p, dev(X), tol, 32)
+    e = rel(got, want)
+    record(f"apply_pseudo_inverse {out_dim}x{in_dim} m={m} tol={tol}", Y=e)
+    assert e <= TOL, e
+    with pytest.raises(fb.Error):
+        fb.apply_pseudo_inverse(p, dev(X), -1.0, 32)
