@@ -10,7 +10,12 @@ flushed before every replay; prints one JSON line per measurement.
   config 4  depth-4 MLP of d = 784 SVD layers, one full training step
             (paper_2009_13977_b200/mlp.py)
 
-Usage: python scripts/bench_configs.py [--quick]
+With --cpu every config-3 line also carries the reference's own CPU time for
+the same op / d / b / batch (oracle/_ref = the unmodified reference compiled
+here: bench::run_bench, algo fasth, all host threads, bench.hpp:166-209) and
+the GPU speed-up over it.
+
+Usage: python scripts/bench_configs.py [--quick] [--cpu]
 """
 import json
 import os
@@ -81,12 +86,29 @@ def layer_us(d, b, m, ctx, kind):
     return timed_graph(step)
 
 
+def cpu_reference(op, d, b, m):
+    """bench::run_bench (bench.hpp:225) for one op on all host threads:
+    (mean us, reps, cores, -march of the build)."""
+    from oracle.oracle import Ref
+    R = Ref()
+    reps = 10 if d <= 512 else 5 if d <= 1024 else 2 if d <= 2048 else 1
+    R.run_bench(op, "fasth", d, m, b, 1, 0, 0)  # warm-up
+    mean, _, _ = R.run_bench(op, "fasth", d, m, b, reps, 0, 0)
+    return mean * 1e6, reps, R.hardware_threads(), R.march
+
+
 def main():
     quick = "--quick" in sys.argv
+    with_cpu = "--cpu" in sys.argv
     ctx = fb.Context(0, deferred=True)
     out = []
 
     def emit(rec):
+        if with_cpu and rec.get("config") == 3 and "us" in rec:
+            cu, reps, cores, march = cpu_reference(rec["op"], rec["d"], rec["b"], rec["batch"])
+            rec.update({"cpu_reference_us": cu, "gpu_speedup": cu / rec["us"],
+                        "cpu_sample": f"run_bench op={rec['op']} algo=fasth, {reps} reps, {cores} threads, "
+                                      f"-march={march}"})
         print(json.dumps(rec), flush=True)
         out.append(rec)
 
