@@ -307,8 +307,8 @@ struct fasth_tape_s {
     fasth_ctx ctx = nullptr;
     Plan plan;
     int m = 0, b_user = 0;
-    int C = 0, WC = 0, ngroups = 0, nstg = 3;
-    int v2nstg = 0;  // > 0: packed stages + chain_v2.cu sweep (else chain_kernel.cu)
+    int C = 0, WC = 0, ngroups = 0;
+    int v2nstg = 0;  // stage ring depth of the packed-stage sweep (chain_v2.cu)
     bool pipelined = false;  // build -> sweep -> dv overlapped through block counters
     float* tapeA = nullptr;  // activations per block
     float* zf = nullptr;
@@ -369,14 +369,10 @@ namespace {
 
 void free_plan(fasth_ctx c, Plan& p) {
     c->release(p.Vbl);
-    c->release(p.Wf);
-    c->release(p.Wb);
     c->release(p.Tt);
-    c->release(p.Sf);
-    c->release(p.Sb);
     c->release(p.Pf);
     c->release(p.Pb);
-    p.Vbl = p.Wf = p.Wb = p.Tt = p.Sf = p.Sb = p.Pf = p.Pb = nullptr;
+    p.Vbl = p.Tt = p.Pf = p.Pb = nullptr;
 }
 
 void free_tape(fasth_tape t) {
@@ -415,8 +411,7 @@ int internal_b(int d, int n, int b_user) {
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row
 // padding d_pad the chain geometry asks for.
 fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_pad, int cb, int n,
-                        int b_user, int reversed, int tag, bool packed, bool* pipelined, Plan* out,
-                        bool launch = true) {
+                        int b_user, int reversed, int tag, bool* pipelined, Plan* out) {
     Plan p;
     p.d = d;
     p.n = n;
@@ -429,39 +424,25 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
     // Build cluster: the chain kernel's cluster size, so each build CTA owns
     // the same 16-row-multiple slab the chain CTAs do.
     p.CB = cb;
-    if (build_smem_bytes(p.BS, p.d_pad / p.CB) > 227 * 1024)
+    if (build2_smem_bytes(p.BS, p.d_pad / p.CB) > 227 * 1024)
         return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for block width %d", d, p.b);
-    TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldv(p.BS), &p.Vbl));
+    TRY(c->alloc_n((size_t)p.q * p.d_pad * stage_ldv(p.BS), &p.Vbl));
     TRY(c->alloc_n((size_t)p.q * p.BS * p.BS, &p.Tt));
-    if (packed) {
-        const size_t sf = stage_floats(p.d_pad / p.CB, p.BS);
-        TRY(c->alloc_n((size_t)p.q * p.CB * sf, &p.Pf));
-        TRY(c->alloc_n((size_t)p.q * p.CB * sf, &p.Pb));
-    } else {
-        TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wf));
-        TRY(c->alloc_n((size_t)p.q * p.d_pad * sweep_ldw(p.BS), &p.Wb));
-        TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sf));
-        TRY(c->alloc_n((size_t)p.q * p.BS * (p.BS + 4), &p.Sb));
-    }
-    const bool b2 = packed && !getenv("FASTH_BUILD_V1") && build2_smem_bytes(p.BS, p.d_pad / p.CB) <= 227 * 1024;
+    const size_t sf = stage_floats(p.d_pad / p.CB, p.BS);
+    TRY(c->alloc_n((size_t)p.q * p.CB * sf, &p.Pf));
+    TRY(c->alloc_n((size_t)p.q * p.CB * sf, &p.Pb));
     if (pipelined && *pipelined) {
-        // device-resident calls: opt-in (FASTH_PIPELINE=1), profitable only
-        // once a block builds in well under the sweep's duration
-        // (scripts/trace_report.py --timeline); the host-buffer call
-        // (launch == false) pipelines behind its chunked upload instead
-        *pipelined = b2 && p.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ &&
-                     (getenv("FASTH_PIPELINE") || !launch) && !getenv("FASTH_NO_PIPELINE") && !getenv("FASTH_DV_V1");
+        // opt-in (FASTH_PIPELINE=1), profitable only once a block builds in
+        // well under the sweep's duration (scripts/trace_report.py --timeline)
+        *pipelined = p.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && getenv("FASTH_PIPELINE") &&
+                     !getenv("FASTH_NO_PIPELINE");
         if (*pipelined) {
             p.ready = c->counters;
             const char* nb = getenv("FASTH_BUILDERS");
-            p.nbuild = launch ? (nb ? std::max(1, atoi(nb)) : 12) : 0;
+            p.nbuild = nb ? std::max(1, atoi(nb)) : 12;
         }
     }
-    if (!launch) {
-        *out = p;
-        return b2 ? FASTH_OK : fail(FASTH_ERR_INVALID, "deferred build needs the packed-stage builder");
-    }
-    if (b2) {
+    {
         const char* prefix = getenv("FASTH_TRACE");
         const size_t ntr = (size_t)p.q * p.CB * 10;
         if (prefix) {  // dumped after the sweep (no sync here: keep the pipeline)
@@ -476,8 +457,6 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
             p.trace = nullptr;
         }
         TRY(bs);
-    } else {
-        TRY(c->timed([&] { return launch_build(p, V, ldv, c->err_d, c->stream); }, "wy_build"));
     }
     *out = p;
     return FASTH_OK;
@@ -498,37 +477,6 @@ fasth_status copy_cols(fasth_ctx c, const float* src, int64_t lds, float* dst, i
     CU(cudaMemcpy2DAsync(dst, ldd * sizeof(float), src, lds * sizeof(float), rows * sizeof(float),
                          cols, cudaMemcpyDeviceToDevice, c->stream));
     return FASTH_OK;
-}
-
-// Debug aid (FASTH_TRACE=<prefix>): record the sweep's per-phase clock64
-// stamps and dump them to <prefix>.<what>.bin (int32 nctas, int32 q, then
-// nctas*(q+1)*16 int64).  Synchronises; never used on the measured path.
-fasth_status launch_traced_sweep(fasth_ctx c, SweepArgs& a, int WC, const char* what) {
-    const char* prefix = getenv("FASTH_TRACE");
-    if (!prefix) {
-        a.trace = nullptr;
-        return c->timed([&] { return launch_sweep(a, WC, c->stream); }, what);
-    }
-    const int nctas = a.C * ((a.m + WC - 1) / WC);
-    const size_t n = (size_t)nctas * (a.q + 1) * 16;
-    long long* tr = nullptr;
-    CU(cudaMalloc(&tr, n * sizeof(long long)));
-    CU(cudaMemsetAsync(tr, 0, n * sizeof(long long), c->stream));
-    a.trace = tr;
-    fasth_status s = c->timed([&] { return launch_sweep(a, WC, c->stream); }, what);
-    a.trace = nullptr;
-    std::vector<long long> h(n);
-    CU(cudaMemcpyAsync(h.data(), tr, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CU(cudaStreamSynchronize(c->stream));
-    cudaFree(tr);
-    std::string path = std::string(prefix) + "." + (a.forward ? "fwd" : "bwd") + ".bin";
-    if (FILE* f = fopen(path.c_str(), "wb")) {
-        int hdr[2] = {nctas, a.q};
-        fwrite(hdr, sizeof(int), 2, f);
-        fwrite(h.data(), sizeof(long long), n, f);
-        fclose(f);
-    }
-    return s;
 }
 
 // Large batches run the panel kernel (chain_panel.cu: one CTA per 16-column
@@ -644,37 +592,14 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
         if (!t->tapeA) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeA));
         if (!t->zf) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zf));
     }
-    if (t->v2nstg) {
-        SweepV2Args a = v2_args(t);
-        a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, record);
-        // the builder was the previous launch; X predates it.  Not after a
-        // cross-stream event wait: a programmatic launch does not reliably
-        // honour a cudaStreamWaitEvent placed before it (measured)
-        a.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;
-        c->after_stream_wait = false;
-        return launch_traced_sweep2(c, a, "sweep(forward)");
-    }
-    SweepArgs a{};
-    a.Vbl = p.Vbl;
-    a.Wbl = p.Wf;
-    a.Sbl = p.Sf;
-    a.nstg = t->nstg;
-    a.C = t->C;
-    a.d = p.d;
-    a.d_pad = p.d_pad;
-    a.m = t->m;
-    a.q = p.q;
-    a.BS = p.BS;
-    a.forward = 1;
-    a.x_in = X;
-    a.ldx = ldx;
-    a.n_valid = t->n_valid;
-    a.scale = t->scale;
-    a.x_out = Y;
-    a.ldo = ldy;
-    a.tape = record ? t->tapeA : nullptr;
-    a.zhat = record ? t->zf : nullptr;
-    return launch_traced_sweep(c, a, t->WC, "sweep(forward)");
+    SweepV2Args a = v2_args(t);
+    a.dir[0] = v2_forward_dir(t, X, ldx, Y, ldy, record);
+    // the builder was the previous launch; X predates it.  Not after a
+    // cross-stream event wait: a programmatic launch does not reliably
+    // honour a cudaStreamWaitEvent placed before it (measured)
+    a.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;
+    c->after_stream_wait = false;
+    return launch_traced_sweep2(c, a, "sweep(forward)");
 }
 
 fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe = false);
@@ -696,34 +621,9 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
         TRY(c->alloc_n((size_t)p.d * std::max(t->m, 1), &dx));
         lddx = p.d;
     }
-    fasth_status s;
-    if (t->v2nstg) {
-        SweepV2Args a = v2_args(t);
-        a.dir[0] = v2_backward_dir(t, G, ldg, g_valid, g_scale, dx, lddx, want_dv);
-        s = launch_traced_sweep2(c, a, "sweep(backward)");
-    } else {
-    SweepArgs a{};
-    a.Vbl = p.Vbl;
-    a.Wbl = p.Wb;
-    a.Sbl = p.Sb;
-    a.nstg = t->nstg;
-    a.C = t->C;
-    a.d = p.d;
-    a.d_pad = p.d_pad;
-    a.m = t->m;
-    a.q = p.q;
-    a.BS = p.BS;
-    a.forward = 0;
-    a.x_in = G;
-    a.ldx = ldg;
-    a.n_valid = g_valid;
-    a.scale = g_scale;
-    a.x_out = dx;
-    a.ldo = lddx;
-    a.tape = want_dv ? t->tapeG : nullptr;
-    a.zhat = want_dv ? t->zb : nullptr;
-    s = launch_traced_sweep(c, a, t->WC, "sweep(backward)");
-    }
+    SweepV2Args a = v2_args(t);
+    a.dir[0] = v2_backward_dir(t, G, ldg, g_valid, g_scale, dx, lddx, want_dv);
+    fasth_status s = launch_traced_sweep2(c, a, "sweep(backward)");
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
@@ -769,7 +669,6 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
     v.zb = t->zb;
     v.dV = dV;
     v.lddv = lddv;
-    if (getenv("FASTH_DV_V1")) return c->timed([&] { return launch_dv(v, c->stream); }, "dv");
     return c->timed([&] { return launch_dv2(v, c->stream); }, "dv");
 }
 
@@ -779,10 +678,6 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
                                   int64_t ldy, const float* G, int64_t ldg, float* dX, int64_t lddx,
                                   float* dV, int64_t lddv) {
     const Plan& p = t->plan;
-    if (!t->v2nstg) {
-        TRY(run_forward(c, t, X, ldx, Y, ldy, true));
-        return run_backward(c, t, G, ldg, p.d, nullptr, dX, lddx, dV, lddv);
-    }
     const bool want_dv = dV != nullptr;
     if (!t->tapeA) TRY(c->alloc_n((size_t)p.q * t->ngroups * p.d_pad * t->WC, &t->tapeA));
     if (!t->zf) TRY(c->alloc_n((size_t)p.q * p.BS * t->m, &t->zf));
@@ -814,7 +709,7 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
-                      int reversed, int tag, fasth_tape* out, bool pipelined = false, bool launch = true) {
+                      int reversed, int tag, fasth_tape* out, bool pipelined = false) {
     fasth_tape t = new fasth_tape_s;
     t->ctx = c;
     t->m = m;
@@ -824,12 +719,14 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     const SweepGeom G = pick_geometry(d, m, BS, c->num_sms);
     t->C = G.C;
     t->WC = G.WC;
-    t->nstg = G.nstg;
     t->ngroups = (m + t->WC - 1) / t->WC;
-    t->v2nstg = getenv("FASTH_SWEEP_V1") ? 0 : sweep2_nstg(G.C, BS, G.d_pad);
-    t->pipelined = pipelined && t->v2nstg > 0;
-    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, t->v2nstg > 0, &t->pipelined,
-                                &t->plan, launch);
+    t->v2nstg = G.C > 0 ? sweep2_nstg(G.C, BS, G.d_pad) : 0;
+    if (t->v2nstg < 2) {
+        delete t;
+        return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for the chain kernels at block width %d", d, BS);
+    }
+    t->pipelined = pipelined;
+    fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, &t->pipelined, &t->plan);
     if (s != FASTH_OK) {
         delete t;
         return s;

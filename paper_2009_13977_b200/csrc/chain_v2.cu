@@ -4,7 +4,7 @@
 // wy.hpp:137-146) — optionally BOTH in one launch (fasth_forward_backward:
 // the two sweeps are independent once the WY blocks exist).
 //
-// Same algebra as chain_kernel.cu (look-ahead pipelined UT-form steps),
+// The look-ahead pipelined UT-form steps,
 //     Z_t     = sum_c L_t^c - 2 S_t Z_{t-1},      L_t = W_t^T X^(t-1) (per CTA rows)
 //     X^(t+1) = X^(t) - 2 V_t Z_t
 // re-laid out for instruction count, which is what bounds a 25-step chain on
@@ -30,6 +30,8 @@
 //             cluster (st.async + remote mbarrier complete_tx)
 //             B warps:   Z_t = sum_c L_t^c (fixed order) + (-2 S_t Z_{t-1})
 //   phase 2   row warps: X^(t+1) = X^(t) + V_t (-2 Z_t) in their accumulators
+#include <cstdlib>
+
 #include "device_prims.cuh"
 #include "fasth_internal.h"
 #include "frag_ops.cuh"
@@ -39,7 +41,11 @@ namespace {
 using namespace fo;
 
 constexpr int WCV = 8;     // batch columns per cluster (one MMA N tile)
-constexpr int NSLOTV = 4;  // exchange receive slots (WAR argument in chain_kernel.cu)
+// exchange receive slots.  WAR safety of slot t % 4: a peer pushes L_{t+4}
+// into it only after it has Z_{t+2}, which needs our L_{t+2}, pushed in our
+// step t+1 — after the barrier that ends our reads of slot t.  (With 3 slots
+// that push would be in step t itself, concurrent with the read.)
+constexpr int NSLOTV = 4;
 constexpr int MAXNR = 8;   // row warps
 
 struct V2Smem {
@@ -463,6 +469,32 @@ int sweep2_nstg(int C, int BS, int d_pad) {
     for (int n = 2; n <= 4; ++n)
         if (sweep2_smem_bytes(C, BS, d_pad, n) <= 227 * 1024) best = n;
     return best;
+}
+
+// Chain geometry: C CTAs per cluster split the rows into RC (a multiple of
+// 16) each; 8 batch columns per cluster.  ~80-row slabs up to 10 CTAs per
+// cluster (measured on B200 at d = 784: 10 x 80 beats 7 x 112 by ~4% per
+// fwd+bwd step; 12+ CTA clusters no longer fit the fused launch's 8 clusters
+// on the GPCs at once), else ~112-row slabs, widened until the packed-stage
+// sweep fits shared memory.  FASTH_CLUSTER overrides C.
+SweepGeom pick_geometry(int d, int m, int BS, int num_sms) {
+    (void)m;
+    (void)num_sms;
+    int C = (d + 79) / 80;
+    if (C > 10) C = (d + 111) / 112;
+    C = C < 1 ? 1 : C > 16 ? 16 : C;
+    if (const char* e = getenv("FASTH_CLUSTER")) C = atoi(e);
+    if (C < 1 || C > 16) C = 8;
+    auto rc_of = [&](int c) { return ((d + c - 1) / c + 15) / 16 * 16; };
+    SweepGeom G;
+    for (int c = C; c <= 16; ++c)
+        if (rc_of(c) <= 256 && sweep2_nstg(c, BS, c * rc_of(c)) >= 2) {
+            G.C = c;
+            G.RC = rc_of(c);
+            G.d_pad = c * G.RC;
+            return G;
+        }
+    return G;  // C == 0: d too large for the chain kernels at this block width
 }
 
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s) {

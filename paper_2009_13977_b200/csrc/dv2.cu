@@ -1,6 +1,6 @@
 // Backward step 2, v2: north_star subsystem (4), the per-reflection gradients
 // of every block (fasth.hpp:97-108, Eq. (5) householder_grad,
-// householder.hpp:148-179), as the closed-form blocked GEMM of dv.cu:
+// householder.hpp:148-179), as a closed-form blocked GEMM:
 //
 //   Q   = Z'f Z'b^T                       (BS x BS, K = m)
 //   K'  = striu(Q - Q^T)

@@ -48,11 +48,7 @@ struct Plan {
     int q = 0, BS = 0, d_pad = 0;
     int reversed = 0;
     int tag = 0;  // error-report tag (0 = U / plain chain, 1 = V)
-    float* Vbl = nullptr;        // [q][d_pad][BS+4]
-    float* Wf = nullptr;         // [q][d_pad][BS+8]  V T~^T  (forward partials)
-    float* Wb = nullptr;         // [q][d_pad][BS+8]  V T~    (backward partials)
-    float* Sf = nullptr;         // [q][BS][BS+4]   Wf_i^T V_{i+1}  (forward look-ahead)
-    float* Sb = nullptr;         // [q][BS][BS+4]   Wb_i^T V_{i-1}  (backward look-ahead)
+    float* Vbl = nullptr;        // [q][d_pad][BS+4]  raw block rows (gradient kernel)
     float* Tt = nullptr;         // [q][BS][BS]     T~ (diagnostics / tests)
     float* Pf = nullptr;         // packed forward stages  [q][CB][stage_floats] (step order)
     float* Pb = nullptr;         // packed backward stages [q][CB][stage_floats]
@@ -100,7 +96,7 @@ struct SweepDirV2 {
     const float* scale;   // optional per-row scale applied on load (Sigma)
     float* x_out;         // column-major d x m
     int64_t ldo;
-    float* tape;          // optional [q][ngroups][d_pad][WC] (same as SweepArgs)
+    float* tape;          // optional [q][ngroups][d_pad][WC] (header comment)
     float* zhat;          // optional [q][BS][m]
     int forward;
 };
@@ -119,24 +115,6 @@ struct SweepV2Args {
     int pdl;              // launched as a programmatic dependent of the builder
 };
 
-struct SweepArgs {
-    const float* Vbl;  // update operand  (X -= 2 V Z')
-    const float* Wbl;  // partial operand (Z' = W^T X): Wf forward, Wb backward
-    const float* Sbl;  // look-ahead corrections: Sf forward, Sb backward
-    int d, d_pad, m, q, BS;
-    int C;                // CTAs per cluster (rows split; d_pad / C is a multiple of 16)
-    int nstg;             // prefetch stages (3, or 2 at large d)
-    int forward;          // 1: Alg 1 step 2 (blocks q-1..0, T~), 0: Alg 2 step 1 (0..q-1, T~^T)
-    const float* x_in;    // column-major, rows < n_valid are read
-    int64_t ldx;
-    int n_valid;          // rows of x_in that exist (rest are zero)
-    const float* scale;   // optional per-row scale applied on load (Sigma)
-    float* x_out;         // column-major d x m
-    int64_t ldo;
-    float* tape;          // optional, see header comment
-    float* zhat;          // optional [q][BS][m]
-    long long* trace;     // optional phase timestamps (FASTH_TRACE): [CTA][q+1][8]
-};
 
 struct DvArgs {
     const float* Vbl;
@@ -157,23 +135,14 @@ struct DvArgs {
     int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
 };
 
-// wy_build.cu
-cudaError_t launch_build(const Plan& p, const float* V, int64_t ldv, ErrWord* err,
-                         cudaStream_t s);
-size_t build_smem_bytes(int BS, int RB);
 // wy_build2.cu (packed stages for chain_v2.cu)
 cudaError_t launch_build2(const Plan& p, const float* V, int64_t ldv, ErrWord* err, cudaStream_t s);
 size_t build2_smem_bytes(int BS, int RB);
-// chain_sweep.cu
-struct SweepGeom {
-    int C = 1, RC = 16, d_pad = 16, WC = 8, nstg = 3;
-};
-cudaError_t launch_sweep(const SweepArgs& a, int WC, cudaStream_t s);
-SweepGeom pick_geometry(int d, int m, int BS, int num_sms);
-size_t sweep_smem_bytes(int C, int WC, int BS, int d_pad, int nstg);
-int sweep_ldw(int BS);  // row pitch of Wf / Wb blocks
-int sweep_ldv(int BS);  // row pitch of Vbl blocks and Sf / Sb
 // chain_v2.cu
+struct SweepGeom {
+    int C = 0, RC = 16, d_pad = 16, WC = 8;  // C == 0: no geometry fits
+};
+SweepGeom pick_geometry(int d, int m, int BS, int num_sms);
 int sweep2_nstg(int C, int BS, int d_pad);  // 0 = geometry not supported by the v2 kernel
 size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg);
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
@@ -191,8 +160,6 @@ cudaError_t launch_wy_apply(const float* A, int64_t lda, const float* Bm, int64_
 // chain_panel.cu (large batch: one CTA per 16-column panel, all rows)
 bool panel_supported(int BS, int d_pad, int m);
 cudaError_t launch_panel(const SweepV2Args& a, cudaStream_t s);
-// dv.cu
-cudaError_t launch_dv(const DvArgs& a, cudaStream_t s);
 // dv2.cu (tapes with WC == 8)
 cudaError_t launch_dv2(const DvArgs& a, cudaStream_t s);
 // sigma_ops.cu

@@ -1,5 +1,5 @@
 // WY-block builder, v2: north_star subsystem (2) for the packed-stage chain
-// (chain_v2.cu).  Same product as wy_build.cu — the UT form of the
+// (chain_v2.cu): the UT form of the
 // reference's compact WY (wy_compact, wy.hpp:56-100),
 //     H_1 ... H_w = I - 2 V T~ V^T,   T~ = (diag(V^T V) + 2 striu(V^T V))^{-1}
 // with raw vectors — restructured around ONE cluster reduction:

@@ -1,6 +1,6 @@
 """Per-kernel device times of one fasth_forward_backward step (d, b, m from
 argv; default the metric config) for each first/second-generation kernel
-choice (FASTH_BUILD_V1 / FASTH_DV_V1 / FASTH_SWEEP_V1): the step is captured
+choice (KT_VARIANTS: comma-separated env knobs set to 1): the step is captured
 into a CUDA graph with the context's event timing on (mode 2), replayed with
 an L2 flush before each replay, and the per-kernel event times averaged.
 Prints one JSON line per variant."""
@@ -51,7 +51,7 @@ if __name__ == "__main__":
     X = torch.randn(m, d, device="cuda").t()
     G = torch.randn(m, d, device="cuda").t()
     flush = torch.empty(64 * 1024 * 1024, device="cuda")
-    variants = os.environ.get("KT_VARIANTS", ",FASTH_NO_PIPELINE,FASTH_BUILD_V1,FASTH_DV_V1,FASTH_SWEEP_V1").split(",")
+    variants = os.environ.get("KT_VARIANTS", ",FASTH_PIPELINE,FASTH_NO_PDL").split(",")
     for variant in variants:
         if variant:
             os.environ[variant] = "1"

@@ -1,9 +1,9 @@
 """numpy model of the exact arithmetic the CUDA kernels perform (test-only).
 
 It restates, in f64, the device algorithm of paper_2009_13977_b200/csrc:
-  * wy_build.cu   : T~ = (diag(V^T V) + 2 striu(V^T V))^{-1} on RAW vectors
-  * chain_sweep.cu: Z = V^T X ; Z' = T~ Z (fwd) / T~^T Z (bwd) ; X -= 2 V Z'
-  * dv.cu         : dV = -2 (A Z'b^T + G Z'f^T + 2 V striu(Q - Q^T)), Q = Z'f Z'b^T
+  * wy_build2.cu : T~ = (diag(V^T V) + 2 striu(V^T V))^{-1} on RAW vectors
+  * chain_v2.cu  : Z = V^T X ; Z' = T~ Z (fwd) / T~^T Z (bwd) ; X -= 2 V Z'
+  * dv2.cu       : dV = -2 (A Z'b^T + G Z'f^T + 2 V striu(Q - Q^T)), Q = Z'f Z'b^T
 so the CPU suite can check the kernels' closed forms against the reference
 oracle without a GPU (the GPU suite then checks the kernels themselves).
 """
