@@ -11,9 +11,11 @@ Sigma-side ops:
 
 with W_k = U_k Sigma_k V_k^T.  d log|det W| / d sigma_i = 1 / sigma_i
 (matops.hpp:57-66), so the regulariser enters dSigma in closed form.  All
-chain work (both legs of every layer, forward and backward), the
-step/clamp and log|det| run in the library's sm_100a kernels; the activation
-and the loss are elementwise torch ops on the same stream.
+chain work (both legs of every layer, forward and backward) and the
+step/clamp run in the library's sm_100a kernels; the activation, the loss
+and the regulariser's log|sigma| sum and -lam/sigma term are elementwise
+torch ops on the same stream (fb.log_abs_det is the library's kernel for
+log|det| but returns a host scalar, which would synchronise the step).
 """
 from __future__ import annotations
 
