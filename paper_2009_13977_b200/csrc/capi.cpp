@@ -449,7 +449,13 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
             CU(cudaMalloc(&p.trace, ntr * sizeof(long long)));
             CU(cudaMemsetAsync(p.trace, 0, ntr * sizeof(long long), c->stream));
         }
-        fasth_status bs = c->timed([&] { return launch_build2(p, V, ldv, c->err_d, c->stream); }, "wy_build");
+        // build4 unless the persistent (pipelined) builder is asked for, it
+        // does not fit shared memory, or FASTH_BUILD2=1 (A/B knob)
+        const bool v4 = !p.ready && p.nbuild == 0 && build4_smem_bytes(p.BS, p.d_pad / p.CB, p.CB) <= 227 * 1024 &&
+                        !(getenv("FASTH_BUILD2") && atoi(getenv("FASTH_BUILD2")) != 0);
+        fasth_status bs = c->timed([&] {
+            return v4 ? launch_build4(p, V, ldv, c->err_d, c->stream) : launch_build2(p, V, ldv, c->err_d, c->stream);
+        }, "wy_build");
         if (prefix) {
             c->build_trace = p.trace;
             c->build_trace_n = ntr;
@@ -602,7 +608,21 @@ fasth_status run_forward(fasth_ctx c, fasth_tape t, const float* X, int64_t ldx,
     return launch_traced_sweep2(c, a, "sweep(forward)");
 }
 
-fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe = false);
+fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe = false, int ndir = 2,
+                    int order = 0);
+
+// Gradient kernel overlapped with the sweep that feeds it: the sweep counts
+// each block's finished tape rows (done[i]) and the gradient kernel, launched
+// as its programmatic dependent, starts on a block as soon as both chains
+// have passed it.  Not for the panel sweep (it keeps no counters).
+// Opt-in (FASTH_DV_PIPE=1): measured slower at the metric config (the
+// per-step release fence that publishes a block costs ~900 cycles on the
+// warp that issues it, and every warp of the sweep is on the step's path).
+bool dv_pipe_ok(fasth_ctx c, const SweepV2Args& a) {
+    const char* e = getenv("FASTH_DV_PIPE");
+    if (!e || atoi(e) == 0) return false;
+    return a.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) && !getenv("FASTH_TRACE");
+}
 
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
 fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg, int g_valid,
@@ -623,11 +643,13 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     }
     SweepV2Args a = v2_args(t);
     a.dir[0] = v2_backward_dir(t, G, ldg, g_valid, g_scale, dx, lddx, want_dv);
+    const bool dvpipe = want_dv && !dv_side && dv_pipe_ok(c, a);
+    if (dvpipe) a.done = c->counters + kMaxPipeQ;
     fasth_status s = launch_traced_sweep2(c, a, "sweep(backward)");
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
-    if (!dv_side) return run_dv(c, t, dV, lddv);
+    if (!dv_side) return run_dv(c, t, dV, lddv, dvpipe, 1, 0);
     // gradient kernel on the side stream (off the dX critical path); the
     // caller joins on dv_side->ev[11]
     CU(cudaEventRecord(dv_side->ev[10], c->stream));
@@ -641,14 +663,19 @@ fasth_status run_backward(fasth_ctx c, fasth_tape t, const float* G, int64_t ldg
     return s;
 }
 
-fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe) {
+fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pipe, int ndir, int order) {
     const Plan& p = t->plan;
     DvArgs v{};
     if (pipe) {
         v.ready = c->counters;
         v.done = c->counters + kMaxPipeQ;
         v.dvcnt = c->counters + 2 * kMaxPipeQ;
-        v.done_target = (unsigned)(2 * t->ngroups * t->C);
+        v.done_target = (unsigned)(ndir * t->ngroups * t->C);
+        v.order = order;
+        // keep the gradient CTAs off the sweep's SMs (FASTH_DV_SMEM overrides)
+        const size_t sw = sweep2_smem_bytes(t->C, p.BS, p.d_pad, t->v2nstg);
+        v.min_smem = sw < 227 * 1024 ? 227 * 1024 - sw + 1024 : 0;
+        if (const char* e = getenv("FASTH_DV_SMEM")) v.min_smem = (size_t)atol(e);
     }
     v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
     c->after_stream_wait = false;
@@ -701,11 +728,13 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
         a.ready = c->counters;
         a.done = c->counters + kMaxPipeQ;
     }
+    const bool dvpipe = want_dv && !pipe && dv_pipe_ok(c, a);
+    if (dvpipe) a.done = c->counters + kMaxPipeQ;
     fasth_status s = launch_traced_sweep2(c, a, "sweep(fwd+bwd)");
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
-    return run_dv(c, t, dV, lddv, pipe);
+    return run_dv(c, t, dV, lddv, pipe || dvpipe, 2, dvpipe ? 1 : 0);
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,

@@ -86,7 +86,14 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     float* Qs = dsm + 2 * BS * LDZ;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
-    const int i = blockIdx.y;
+    // blocks in the order the sweeps finish them (pipelined step: the CTAs
+    // the scheduler places first are the ones whose inputs land first)
+    int i = blockIdx.y;
+    if (a.order == 1) {  // fused fwd+bwd: block i is final after step max(i, q-1-i)
+        const int q = a.q, k = i, lo = (q - 1) / 2, hi = q / 2;
+        if (q & 1) i = k == 0 ? lo : ((k & 1) ? lo - (k + 1) / 2 : lo + k / 2);
+        else i = (k & 1) ? hi + k / 2 : lo - k / 2;
+    }
     const int r0 = blockIdx.x * DV_ROWS + warp * 16;  // this warp's 16 rows
     const bool rows_ok = r0 < a.d_pad;
     const int m = a.m;
@@ -261,7 +268,11 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
 template <int BS>
 cudaError_t launch_dv2_t(const DvArgs& a, cudaStream_t s) {
     const dim3 grid((a.d_pad + DV_ROWS - 1) / DV_ROWS, a.q);
-    constexpr size_t smem = dv2_smem<BS>();
+    size_t smem = dv2_smem<BS>();
+    // pipelined behind the sweep: claim enough shared memory that no CTA
+    // lands on an SM a sweep CTA occupies (co-resident gradient work slows
+    // the latency-bound chain steps more than the overlap gains)
+    if (a.done && a.min_smem > smem) smem = a.min_smem;
     if (smem > 48 * 1024)
         if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(dv2_kernel<BS>), smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};

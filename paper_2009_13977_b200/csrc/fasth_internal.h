@@ -132,12 +132,18 @@ struct DvArgs {
     unsigned* done;
     unsigned* dvcnt;
     unsigned done_target;
+    size_t min_smem;  // pipelined: dynamic shared memory to request at least
+    int order;  // blockIdx.y -> block: 0 identity (backward sweep order), 1 middle-out (fused fwd+bwd)
     int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
 };
 
 // wy_build2.cu (packed stages for chain_v2.cu)
 cudaError_t launch_build2(const Plan& p, const float* V, int64_t ldv, ErrWord* err, cudaStream_t s);
 size_t build2_smem_bytes(int BS, int RB);
+// wy_build4.cu: same outputs, one cluster per block without cluster barriers
+// on the path (plain launches only: no ready counters / persistent tickets)
+cudaError_t launch_build4(const Plan& p, const float* V, int64_t ldv, ErrWord* err, cudaStream_t s);
+size_t build4_smem_bytes(int BS, int RB, int C);
 // chain_v2.cu
 struct SweepGeom {
     int C = 0, RC = 16, d_pad = 16, WC = 8;  // C == 0: no geometry fits

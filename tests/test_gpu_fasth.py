@@ -97,15 +97,58 @@ def test_pipelined_step_equals_serial_bitwise(fb, d, b, m):
     the counters reset: run it repeatedly."""
     rng = np.random.default_rng(11 * d + b + m)
     V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
-    ser = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
-    os.environ["FASTH_PIPELINE"] = "1"
+    # the persistent pipelined builder is build2's: compare with build2 serialised
+    os.environ["FASTH_BUILD2"] = "1"
     try:
+        ser = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
+        os.environ["FASTH_PIPELINE"] = "1"
         for _ in range(3):
             pip = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
             for u, w in zip(ser, pip):
                 assert np.array_equal(u, w)
     finally:
-        del os.environ["FASTH_PIPELINE"]
+        os.environ.pop("FASTH_PIPELINE", None)
+        del os.environ["FASTH_BUILD2"]
+
+
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (64, 8, 32), (2048, 32, 32), (200, 17, 33), (300, 16, 5)])
+def test_dv_pipelined_equals_serial_bitwise(fb, d, b, m):
+    """FASTH_DV_PIPE=1 (the gradient kernel started per block from the sweep's
+    counters) runs the same kernels: bit for bit, repeatedly (the counters
+    reset themselves), both entry points."""
+    rng = np.random.default_rng(13 * d + b + m)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    ser = [[host(t) for t in run_chain(fb, V, X, G, b, fused=f)] for f in (False, True)]
+    os.environ["FASTH_DV_PIPE"] = "1"
+    try:
+        for _ in range(3):
+            for f in (False, True):
+                pip = [host(t) for t in run_chain(fb, V, X, G, b, fused=f)]
+                for u, w in zip(ser[f], pip):
+                    assert np.array_equal(u, w)
+    finally:
+        del os.environ["FASTH_DV_PIPE"]
+
+
+@pytest.mark.parametrize("d,b,m", [(784, 32, 32), (64, 8, 32), (3072, 16, 32), (200, 17, 33), (130, 33, 7)])
+def test_build4_matches_build2_and_oracle(fb, oracle, d, b, m):
+    """The two WY builders (wy_build4.cu default, wy_build2.cu with
+    FASTH_BUILD2=1) are different arithmetic for the same T~ and W: both
+    within the parity bound of the reference's sequential product, and
+    within fp32 noise of each other."""
+    port, _ = oracle
+    rng = np.random.default_rng(17 * d + b + m)
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = port.fasth_fwd_bwd(V, X, G, b)
+    got4 = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
+    os.environ["FASTH_BUILD2"] = "1"
+    try:
+        got2 = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
+    finally:
+        del os.environ["FASTH_BUILD2"]
+    for a4, a2, w in zip(got4, got2, want):
+        assert rel(a4, w) <= TOL and rel(a2, w) <= TOL
+        assert rel(a4, a2) <= 2e-5
 
 
 @pytest.mark.parametrize("d,b,m", [(784, 32, 32), (256, 32, 200), (300, 32, 65), (2048, 32, 48), (128, 32, 1)])
