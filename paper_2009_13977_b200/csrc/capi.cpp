@@ -82,6 +82,38 @@ struct fasth_ctx_s {
     int counters_len = 0;
     double* logdet_d = nullptr;
     int64_t launches = 0;
+    // FASTH_STEPTRACE=<path>: non-synchronising global-timer stamps of the
+    // fused step's three kernels (builder, sweep, gradient; per CTA), written
+    // in place by the kernels and dumped to <path>.bin at fasth_ctx_check
+    // activations the next build's L2 prefetch covers (set by the entry, consumed by build_plan)
+    const float* pf[2] = {nullptr, nullptr};
+    int64_t pf_ld[2] = {0, 0};
+    long long* step_trace = nullptr;
+    int cur_m = 0;  // batch of the plan being built (step-trace sizing)
+    size_t st_build = 0, st_sweep = 0, st_dv = 0, st_total = 0;
+    int st_hdr[6] = {0, 0, 0, 0, 0, 0};  // q, C, build rows, sweep CTAs, dv CTAs, valid
+    long long* step_trace_area(size_t build_n, size_t sweep_n, size_t dv_n) {
+        const size_t tot = build_n + sweep_n + dv_n;
+        if (tot > st_total) {
+            if (step_trace) cudaFree(step_trace);
+            if (cudaMalloc(&step_trace, tot * sizeof(long long)) != cudaSuccess) step_trace = nullptr, st_total = 0;
+            else st_total = tot;
+        }
+        st_build = 0, st_sweep = build_n, st_dv = build_n + sweep_n;
+        return step_trace;
+    }
+    void dump_step_trace() {
+        const char* path = getenv("FASTH_STEPTRACE");
+        if (!path || !step_trace || !st_hdr[5]) return;
+        cudaStreamSynchronize(stream);
+        std::vector<long long> h(st_total);
+        cudaMemcpy(h.data(), step_trace, st_total * sizeof(long long), cudaMemcpyDeviceToHost);
+        if (FILE* f = fopen((std::string(path) + ".bin").c_str(), "wb")) {
+            fwrite(st_hdr, sizeof(int), 6, f);
+            fwrite(h.data(), sizeof(long long), st_total, f);
+            fclose(f);
+        }
+    }
     long long* build_trace = nullptr;  // FASTH_TRACE: pending builder stamps
     size_t build_trace_n = 0;
     int build_trace_rows = 0;
@@ -421,6 +453,9 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
     p.d_pad = d_pad;
     p.reversed = reversed;
     p.tag = tag;
+    p.pf[0] = c->pf[0], p.pf[1] = c->pf[1], p.pf_ld[0] = c->pf_ld[0], p.pf_ld[1] = c->pf_ld[1];
+    p.pf_rows = d, p.pf_cols = (c->pf[0] || c->pf[1]) ? c->cur_m : 0;
+    c->pf[0] = c->pf[1] = nullptr;
     // Build cluster: the chain kernel's cluster size, so each build CTA owns
     // the same 16-row-multiple slab the chain CTAs do.
     p.CB = cb;
@@ -445,6 +480,15 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
     {
         const char* prefix = getenv("FASTH_TRACE");
         const size_t ntr = (size_t)p.q * p.CB * 10;
+        if (!prefix && getenv("FASTH_STEPTRACE")) {  // builder rows of the step trace (fused step)
+            const size_t nsw = (size_t)2 * ((std::max(1, c->cur_m) + 7) / 8) * p.CB * (p.q + 1) * 16;
+            const size_t ndv = (size_t)((p.d_pad + 63) / 64) * p.q * 6;
+            if (long long* a = c->step_trace_area(ntr, nsw, ndv)) {
+                p.trace = a + c->st_build;
+                c->st_hdr[0] = p.q, c->st_hdr[1] = p.CB, c->st_hdr[2] = p.q * p.CB;
+                c->st_hdr[3] = c->st_hdr[4] = c->st_hdr[5] = 0;
+            }
+        }
         if (prefix) {  // dumped after the sweep (no sync here: keep the pipeline)
             CU(cudaMalloc(&p.trace, ntr * sizeof(long long)));
             CU(cudaMemsetAsync(p.trace, 0, ntr * sizeof(long long), c->stream));
@@ -501,7 +545,10 @@ fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what)
         return c->timed([&] { return launch_panel(a, c->stream); }, "panel(fwd/bwd)");
     }
     if (!prefix) {
-        a.trace = nullptr;
+        const bool st = getenv("FASTH_STEPTRACE") && c->step_trace && c->st_hdr[2] > 0 && a.ndir == 2;
+        a.trace = st ? c->step_trace + c->st_sweep : nullptr;
+        a.wtrace = nullptr;
+        if (st) c->st_hdr[3] = a.C * a.ngroups * a.ndir;
         return c->timed([&] { return launch_sweep2(a, c->stream); }, what);
     }
     const int nctas = a.C * a.ngroups * a.ndir;
@@ -679,6 +726,11 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
     }
     v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
     c->after_stream_wait = false;
+    if (getenv("FASTH_STEPTRACE") && c->step_trace && c->st_hdr[3] > 0) {
+        v.trace = c->step_trace + c->st_dv;
+        c->st_hdr[4] = ((p.d_pad + 63) / 64) * p.q;
+        c->st_hdr[5] = 1;
+    }
     v.Vbl = p.Vbl;
     v.d = p.d;
     v.d_pad = p.d_pad;
@@ -729,7 +781,10 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
         a.done = c->counters + kMaxPipeQ;
     }
     const bool dvpipe = want_dv && !pipe && dv_pipe_ok(c, a);
-    if (dvpipe) a.done = c->counters + kMaxPipeQ;
+    if (dvpipe) {
+        a.done = c->counters + kMaxPipeQ;
+        a.sig_from = (p.q - 1) / 2;  // no block is final in both chains before this step
+    }
     fasth_status s = launch_traced_sweep2(c, a, "sweep(fwd+bwd)");
     if (dx != dX) c->release(dx);
     TRY(s);
@@ -742,6 +797,7 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     fasth_tape t = new fasth_tape_s;
     t->ctx = c;
     t->m = m;
+    c->cur_m = m;
     t->b_user = b;
     t->n_valid = d;
     const int BS = next_pow2_min16(internal_b(d, n, b));
@@ -865,6 +921,7 @@ fasth_status fasth_ctx_destroy(fasth_ctx c) {
         for (void* p : kv.second) cudaFree(p);
     for (auto& kv : c->live) cudaFree(kv.first);
     if (c->counters) cudaFree(c->counters);
+    if (c->step_trace) cudaFree(c->step_trace);
     if (c->logdet_d) cudaFree(c->logdet_d);
 
     if (c->err_h) cudaFreeHost(c->err_h);
@@ -915,6 +972,7 @@ fasth_status fasth_ctx_set_check(fasth_ctx c, int mode) {
 fasth_status fasth_ctx_check(fasth_ctx c) {
     DeviceGuard dg_(dev_of(c));
     if (!c) return fail(FASTH_ERR_INVALID, "null ctx");
+    c->dump_step_trace();
     return c->harvest();
 }
 
@@ -1225,7 +1283,10 @@ fasth_status fasth_forward(fasth_ctx c, const float* V, int64_t ldv, int d, int 
     }
     if (use_large_batch(d, n, m)) return lb_forward(c, V, ldv, d, n, X, ldx, m, block_width, Y, ldy, tape);
     fasth_tape t = nullptr;
-    TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t));
+    c->pf[0] = X, c->pf_ld[0] = ldx;
+    const fasth_status s0 = new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t);
+    c->pf[0] = c->pf[1] = nullptr;  // consumed by the build (or dropped on failure)
+    TRY(s0);
     fasth_status s = run_forward(c, t, X, ldx, Y, ldy, tape != nullptr);
     if (s == FASTH_OK) s = c->finish();
     if (s == FASTH_OK && tape)
@@ -1320,7 +1381,10 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
     if (use_large_batch(d, n, m))
         return run_large_batch(c, V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy, dX, lddx, dV, lddv);
     fasth_tape t = nullptr;
-    TRY(new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr));
+    c->pf[0] = X, c->pf_ld[0] = ldx, c->pf[1] = G, c->pf_ld[1] = ldg;
+    const fasth_status s0 = new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr);
+    c->pf[0] = c->pf[1] = nullptr;  // consumed by the build (or dropped on failure)
+    TRY(s0);
     fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);
     if (s == FASTH_OK && dV) s = c->dv_notify_whole(n);
     free_tape(t);  // pool reuse is stream ordered

@@ -69,13 +69,13 @@ __host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg) 
     o += (size_t)NR * MT * 128;
     o = (o + 3) & ~size_t(3);
     L.bars = o;
-    o += 2 * (nstg + NSLOTV);
+    o += 2 * (nstg + NSLOTV) + 2;  // + the progress counter of the signal warp
     L.total = o * 4;
     return L;
 }
 
-template <int BS, int TPW>
-__global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(SweepV2Args a) {
+template <int BS, int TPW, bool SIG>
+__global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_kernel(SweepV2Args a) {
     constexpr int MT = BS / 16, KB = BS / 8;
     constexpr int LDW = stage_ldw(BS), LDV = stage_ldv(BS);
     constexpr int WOFF = 0;
@@ -106,6 +106,12 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     const uint32_t stage_bytes = (uint32_t)SF * 4u;
     const uint32_t ex_bytes = (uint32_t)C * MT * 512u;
     const int PW = NR + MT;  // producer warp
+    // pipelined gradient (SIG, a.done set): one more warp, outside the CTA
+    // barriers of the step loop, publishes each finished block (gpu-scope
+    // fence + counter) so that no warp on the step's path pays for the fence
+    const int SW = SIG ? PW + 1 : 1 << 30;
+    const int nmain = (NR + MT + 1) * 32;
+    unsigned* prog = reinterpret_cast<unsigned*>(bars + NSTG + NSLOTV);
     long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
     // prologue / epilogue global-timer stamps in row q: 10 entry, 11 X loaded,
     // 12 cluster synced, 13 prologue partial pushed, 14 loop done, 15 exit
@@ -135,6 +141,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
         for (int s = 0; s < NSTG + NSLOTV; ++s) dev::mbar_init(&bars[s], 1);
         dev::fence_mbar_init();
         for (int s = 0; s < NSLOTV; ++s) mbar_expect_u32(exb_u32 + 8u * s, ex_bytes);
+        *prog = 0u;
     }
     __syncthreads();
     if (warp == PW && lane == 0) {
@@ -261,8 +268,39 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
     GSTAMP(13);
     __syncthreads();  // the combine scratch is reused by step 0's partial
 
+    // the rows and Z' of a step are stored: count the warp in (release at CTA
+    // scope covers the warp's stores, ordered by __syncwarp)
+    // counting starts at step t0 (a.sig_from): earlier steps are covered by
+    // the release of step t0 (program order)
+    const int t0 = a.sig_from < q ? a.sig_from : q - 1;
+    auto step_stored = [&]() {
+        if (SIG) {
+            __syncwarp();
+            if (lane == 0) asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(dev::smem_u32(prog)) : "memory");
+        }
+    };
+    if (SIG && warp == SW) {
+        // block_of(t) is final in this CTA once all NR + MT warps have counted
+        // step t; then one gpu-scope release publishes it to the gradient kernel
+        for (int t = t0; t < q; ++t) {
+            const unsigned target = (unsigned)((t - t0 + 1) * (NR + MT));
+            if (lane == 0) {
+                unsigned v;
+                while (true) {
+                    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(dev::smem_u32(prog)) : "memory");
+                    if (v >= target) break;
+                    __nanosleep(32);
+                }
+                __threadfence();
+                // steps before t0 finish no block of the fused launch early:
+                // they are published together with step t0
+                for (int u = t == t0 ? 0 : t; u <= t; ++u) atomicAdd(a.done + block_of(u), 1u);
+            }
+            __syncwarp();
+        }
+    }
     int st = 0, ph = 0;  // stage ring position of step t
-    for (int t = 0; t < q; ++t) {
+    for (int t = 0; t < q && warp != SW; ++t) {
         const int i = block_of(t);
         if (trc && tid == 0) trc[(size_t)t * 16 + 0] = clock64(), trc[(size_t)t * 16 + 8] = (long long)dev::globaltimer();
         // ---------------- phase 1 ----------------
@@ -290,6 +328,8 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             if (trc && tid == 0) trc[(size_t)t * 16 + 2] = clock64();
         } else if (warp < NR + MT) {
             const int mt = warp - NR;
+            // Z' of step t-1 is stored (a step ago: the release drains nothing new)
+            if (t > t0) step_stored();
             float cm[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f};
             mbar_wait_u32(bar_u32 + 8u * st, (uint32_t)ph);
             if (t > 0) {  // -2 S_t Z_{t-1}: Zn holds -2 Z_{t-1}, pre-split
@@ -350,11 +390,13 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             }
         }
         WSTAMP(0);
-        __syncthreads();
+        if constexpr (SIG) asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
+        else __syncthreads();
         WSTAMP(1);
         if (trc && tid == 0) trc[(size_t)t * 16 + 5] = clock64();
         // ---------------- phase 2: X^(t+1) = X^(t) + V_t (-2 Z_t) ----------------
         if (warp < NR) {
+            if (t > t0) step_stored();  // tape rows of step t-1, stored a step ago
             const float* zc = Zn + (t & 1) * (KB * 128);
             float zh[KB / 2][4], zl[KB / 2][4];
 #pragma unroll
@@ -390,17 +432,14 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
             if (trc && tid == 0) trc[(size_t)t * 16 + 6] = clock64();
         }
         WSTAMP(2);
-        __syncthreads();
+        if constexpr (SIG) asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
+        else __syncthreads();
         WSTAMP(3);
         if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64(), trc[(size_t)t * 16 + 9] = (long long)dev::globaltimer();
-        // block i's tape rows and Z' are stored: signal the gradient kernel
-        if (a.done && warp == PW && lane == 0) {
-            __threadfence();
-            atomicAdd(a.done + i, 1u);
-        }
         if (++st == NSTG) st = 0, ph ^= 1;
     }
 
+    if (warp < NR + MT && q > 0) step_stored();  // the last step's rows and Z'
     if (warp < NR) {
 #pragma unroll
         for (int u = 0; u < TPW; ++u) {
@@ -425,13 +464,13 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1) * 32, 1) sweep2_kernel(S
 template <int BS, int TPW>
 cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
     const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg);
-    auto kern = sweep2_kernel<BS, TPW>;
+    auto kern = a.done ? sweep2_kernel<BS, TPW, true> : sweep2_kernel<BS, TPW, false>;
     if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total, true); e != cudaSuccess) return e;
     const int RT = a.d_pad / a.C / 16;
     const int NR = RT < MAXNR ? RT : MAXNR;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.C * a.ngroups * a.ndir, 1, 1);
-    cfg.blockDim = dim3((NR + BS / 16 + 1) * 32, 1, 1);
+    cfg.blockDim = dim3((NR + BS / 16 + 1 + (a.done ? 1 : 0)) * 32, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];

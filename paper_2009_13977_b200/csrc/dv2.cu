@@ -102,6 +102,12 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     const size_t tstep = (size_t)a.ngroups * a.d_pad * 8;
     const float* tA = a.tapeA + (size_t)i * tstep;
     const float* tG = a.tapeG + (size_t)i * tstep;
+    long long* trc = a.trace && threadIdx.x == 0 ? a.trace + ((size_t)i * gridDim.x + blockIdx.x) * 6 : nullptr;
+    if (trc) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trc[0] = (long long)dev::globaltimer(), trc[5] = smid;
+    }
     if (!a.done && a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // sweep complete
     if (a.done) {  // pipelined step: both sweeps have passed block i
         if (tid == 0) {
@@ -120,6 +126,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
         }
         __syncthreads();
     }
+    if (trc) trc[1] = (long long)dev::globaltimer();
 
     float acc[NT][4], cc[NT][4];
 #pragma unroll
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
         dev::cp_async_commit();
         dev::cp_async_wait_all();
         __syncthreads();
+        if (trc && l0 == 0) trc[2] = (long long)dev::globaltimer();
         // Q += Z'f Z'b^T over the chunk (A = Z'f: rows j, K = l; B = Z'b^T)
 #pragma unroll
         for (int u = 0; u < QN; ++u) {
@@ -236,12 +244,17 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
         }
     }
     __syncthreads();
-    if (!rows_ok) return;
+    if (trc) trc[3] = (long long)dev::globaltimer();
+    if (!rows_ok) {
+        if (trc) trc[4] = (long long)dev::globaltimer();
+        return;
+    }
 #pragma unroll
     for (int ks = 0; ks < KB; ++ks) {
         const AF fV = split4(fv[ks]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
+            if (ks > nt) continue;  // 2K' = 2 striu(Q - Q^T): zero unless k < j
             const int j = nt * 8 + g, k0 = ks * 8 + tq, k1 = k0 + 4;
             const float b0 = k0 < j ? 2.f * (Qs[k0 * (BS + 1) + j] - Qs[j * (BS + 1) + k0]) : 0.f;
             const float b1 = k1 < j ? 2.f * (Qs[k1 * (BS + 1) + j] - Qs[j * (BS + 1) + k1]) : 0.f;
@@ -263,6 +276,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
                 a.dV[(int64_t)col * a.lddv + r] = -2.f * (acc[nt][e] + cc[nt][e]);
             }
         }
+    if (trc) trc[4] = (long long)dev::globaltimer();
 }
 
 template <int BS>

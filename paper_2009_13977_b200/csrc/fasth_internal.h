@@ -62,6 +62,11 @@ struct Plan {
     int nbuild = 0;
     // plain launch: build blocks [blk_lo, blk_hi) only (blk_hi < 0: all q)
     int blk_lo = 0, blk_hi = -1;
+    // column-major activations the next kernel reads first (X, G): the
+    // builder prefetches them into L2 while it works (build4)
+    const float* pf[2] = {nullptr, nullptr};
+    int64_t pf_ld[2] = {0, 0};
+    int pf_rows = 0, pf_cols = 0;
 };
 
 // ---- packed chain stages (chain_v2.cu) ------------------------------------
@@ -112,6 +117,7 @@ struct SweepV2Args {
     // stored (nullptr: plain launch, no waits, no signals)
     const unsigned* ready;
     unsigned* done;
+    int sig_from;         // done counting starts at this step (earlier steps published with it)
     int pdl;              // launched as a programmatic dependent of the builder
 };
 
@@ -133,6 +139,7 @@ struct DvArgs {
     unsigned* dvcnt;
     unsigned done_target;
     size_t min_smem;  // pipelined: dynamic shared memory to request at least
+    long long* trace;  // optional per-CTA global-timer stamps [block][slab][6] (FASTH_STEPTRACE)
     int order;  // blockIdx.y -> block: 0 identity (backward sweep order), 1 middle-out (fused fwd+bwd)
     int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
 };

@@ -68,7 +68,7 @@ __host__ __device__ inline B4Layout b4_layout(int BS, int RB, int C) {
     o += al16((size_t)BS * LD2 * 8);
     L.tts = o;  // T~^T as (hi, lo) pairs
     o += al16((size_t)BS * LD2 * 8);
-    L.gnt = o;  // G_{i,i+1}^T, fp32, pitch BS + 4
+    L.gnt = o;  // G_{i,i+1}^T, fp32, pitch BS + 1 (conflict-free transposed stores)
     o += al16((size_t)BS * (BS + 4) * 4);
     L.gpt = o;  // G_{i,i-1}^T
     o += al16((size_t)BS * (BS + 4) * 4);
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
                                                          int vec_ok, ErrWord* err) {
     constexpr int MT = BS / 16, NT = BS / 8, KB = BS / 8;
     constexpr int E1 = BS * BS;
-    constexpr int LD2 = BS + 4, LDG = BS + 4, LDT = BS + 1;
+    constexpr int LD2 = BS + 4, LDG = BS + 1, LDT = BS + 1;
     constexpr int LDW = stage_ldw(BS), LDV = stage_ldv(BS);
     extern __shared__ __align__(128) unsigned char smem[];
     const int C = p.CB, RB = p.d_pad / C;
@@ -185,6 +185,15 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     const int w = min(p.b, p.n - i * p.b);
     const int nrows = max(0, min(RB, p.d - row0));
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // L2 prefetch of the sweep's first reads (X, G), one 128-byte line per thread
+    if (p.pf_cols > 0) {
+        const int nl = (p.pf_rows + 31) / 32, per_m = nl * p.pf_cols;
+        for (int k = blockIdx.x * NTH4 + tid; k < 2 * per_m; k += gridDim.x * NTH4) {
+            const int mi = k >= per_m, kk = k - mi * per_m, c = kk / nl, l = kk - c * nl;
+            const float* base = p.pf[mi];
+            if (base) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)c * p.pf_ld[mi] + 32 * l));
+        }
+    }
 #define BTRACE(k) \
     if (p.trace && tid == 0) p.trace[((size_t)i * C + rank) * 10 + (k)] = clock64()
     BTRACE(0);
@@ -206,29 +215,44 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     // just before the first push (the loads and the Gram run in between)
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
-    // 1. rows of blocks i (slot 0), i-1 (1), i+1 (2), permuted positions
+    // 1. rows of blocks i (slot 0), i-1 (1), i+1 (2), permuted positions:
+    //    warp w takes columns w, w + 8, ... (six 16-byte loads in flight per
+    //    lane), lane l the 4-row groups 4 l, 4 l + 128, ...
     {
-        const int ngrp = RB / 4;  // 4-row groups per column
-        for (int idx = tid; idx < 3 * BS * ngrp; idx += NTH4) {
-            const int jj = idx / ngrp, r = (idx - jj * ngrp) * 4;
-            const int sl = jj / BS, j = jj - sl * BS;
-            const int blk = sl == 0 ? i : sl == 1 ? i - 1 : i + 1;
-            const int k0 = blk * p.b;
-            const int wb = (blk >= 0 && blk < p.q) ? min(p.b, p.n - k0) : 0;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (j < wb && r < nrows) {
-                const float* src = V + (int64_t)(p.reversed ? p.n - 1 - (k0 + j) : k0 + j) * ldv + row0 + r;
-                if (vec_ok && r + 4 <= nrows) {
-                    v = __ldg(reinterpret_cast<const float4*>(src));
-                } else {
-                    v.x = src[0];
-                    if (r + 1 < nrows) v.y = src[1];
-                    if (r + 2 < nrows) v.z = src[2];
-                    if (r + 3 < nrows) v.w = src[3];
+        constexpr int NB = 6;
+        float* sf = reinterpret_cast<float*>(smem);
+        for (int jb = warp; jb < 3 * BS; jb += NB * (NTH4 / 32)) {
+            for (int r = 4 * lane; r < RB; r += 128) {
+                float4 v[NB];
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    const int jj = jb + u * (NTH4 / 32);
+                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const int sl = jj / BS, j = jj - sl * BS;
+                    const int blk = sl == 0 ? i : sl == 1 ? i - 1 : i + 1;
+                    const int k0 = blk * p.b;
+                    const int wb = (jj < 3 * BS && blk >= 0 && blk < p.q) ? min(p.b, p.n - k0) : 0;
+                    if (j < wb && r < nrows) {
+                        const float* src = V + (int64_t)(p.reversed ? p.n - 1 - (k0 + j) : k0 + j) * ldv + row0 + r;
+                        if (vec_ok && r + 4 <= nrows) {
+                            v[u] = __ldg(reinterpret_cast<const float4*>(src));
+                        } else {
+                            v[u].x = src[0];
+                            if (r + 1 < nrows) v[u].y = src[1];
+                            if (r + 2 < nrows) v[u].z = src[2];
+                            if (r + 3 < nrows) v[u].w = src[3];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    const int jj = jb + u * (NTH4 / 32);
+                    if (jj < 3 * BS) {  // rows r + e -> position + 4 e
+                        float* dst = sf + (jj < BS ? L.vc / 4 + jj * P : L.vpn / 4 + (jj - BS) * P) + b4_pos(r);
+                        dst[0] = v[u].x, dst[4] = v[u].y, dst[8] = v[u].z, dst[12] = v[u].w;
+                    }
                 }
             }
-            float* dst = (jj < BS ? Vc + (size_t)jj * P : Vpn + (size_t)(jj - BS) * P) + b4_pos(r);
-            dst[0] = v.x, dst[4] = v.y, dst[8] = v.z, dst[12] = v.w;  // r + e -> pos + 4e
         }
     }
     __syncthreads();
@@ -353,6 +377,10 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     BTRACE(5);
 
     // 4b. W rows and S into the stage images (fragment-order positions)
+    // the S products are the same for every CTA of the cluster: rank 0 forms
+    // Sf, rank 1 (rank 0 when C == 1) Sb, and stores it into every CTA's
+    // stage slot
+    const bool doSf = rank == 0, doSb = rank == (C > 1 ? 1 : 0);
     float* IWf = IPF;
     float* IVf = IPF + RB * LDW;
     float* ISf = IVf + RB * LDV;
@@ -360,48 +388,72 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     float* IVb = IPB + RB * LDW;
     float* ISb = IVb + RB * LDV;
     {
-        const int mtw = RB / 16;
-        for (int u = warp; u < 2 * mtw + 2 * MT; u += NTH4 / 32) {
-            float acc[NT][3][4];
+        // W^T = T~ V^T (Wf) and T~^T V^T (Wb): A = T~ / T~^T from the pre-split
+        // planes, B[k][n] = V at row position n; unit = (product, m-tile,
+        // group of NPU n-tiles) — 8 units at BS = 32, RB = 80
+        constexpr int NPU = 5;
+        const int ntl = RB / 8, ng = (ntl + NPU - 1) / NPU;
+        const int nW = 2 * MT * ng, nS = (doSf ? MT : 0) + (doSb ? MT : 0);
+        for (int u = warp; u < nW + nS; u += NTH4 / 32) {
+            if (u < nW) {
+                const bool fwd = u < MT * ng;
+                const int uu = fwd ? u : u - MT * ng, mt = uu % MT, nt0 = (uu / MT) * NPU;
+                const float2* Am = fwd ? TfS : TTS;
+                float acc[NPU][3][4];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
+                for (int t = 0; t < NPU; ++t)
 #pragma unroll
-                for (int b = 0; b < 3; ++b)
+                    for (int b = 0; b < 3; ++b)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) acc[nt][b][e] = 0.f;
-            if (u < 2 * mtw) {
-                // Wf = V T~^T: B[k][n] = T~[n][k];  Wb = V T~: B[k][n] = T~^T[n][k]
-                const bool fwd = u < mtw;
-                const int mt = fwd ? u : u - mtw;
-                const float2* Bm = fwd ? TfS : TTS;
+                        for (int e = 0; e < 4; ++e) acc[t][b][e] = 0.f;
 #pragma unroll
                 for (int ks = 0; ks < KB; ++ks) {
-                    const float* a = Vc + (size_t)(ks * 8 + tq) * P + mt * 16 + g;  // A[m][k] = V at position m
-                    const AFrag af = make_a(a[0], a[8], a[4 * P], a[4 * P + 8]);
+                    const float2* a = Am + (mt * 16 + g) * LD2 + ks * 8 + tq;
+                    const float2 a0 = a[0], a1 = a[8 * LD2], a2 = a[4], a3 = a[8 * LD2 + 4];
+                    AFrag af;
+                    af.h[0] = __float_as_uint(a0.x), af.h[1] = __float_as_uint(a1.x);
+                    af.h[2] = __float_as_uint(a2.x), af.h[3] = __float_as_uint(a3.x);
+                    af.l[0] = __float_as_uint(a0.y), af.l[1] = __float_as_uint(a1.y);
+                    af.l[2] = __float_as_uint(a2.y), af.l[3] = __float_as_uint(a3.y);
+                    const float* bv = Vc + (size_t)(ks * 8 + tq) * P + g;
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        const float2 b0 = Bm[(nt * 8 + g) * LD2 + ks * 8 + tq];
-                        const float2 b1 = Bm[(nt * 8 + g) * LD2 + ks * 8 + tq + 4];
-                        mma3s(acc[nt][0], acc[nt][1], acc[nt][2], af, b0.x, b1.x, b0.y, b1.y);
+                    for (int t = 0; t < NPU; ++t) {
+                        if (nt0 + t < ntl) {
+                            const float b0 = bv[(nt0 + t) * 8], b1 = bv[4 * P + (nt0 + t) * 8];
+                            mma3s(acc[t][0], acc[t][1], acc[t][2], af, __uint_as_float(hi_rn(b0)),
+                                  __uint_as_float(hi_rn(b1)), lo_rn(b0), lo_rn(b1));
+                        }
                     }
                 }
+                // C[c][n]: c = 16 mt + g (+8), n = 8 nt + 2 tq (+1) -> W[row(n)][c];
+                // columns c, c + 8 sit side by side in fragment order
                 float* img = fwd ? IWf : IWb;
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const int r = b4_pos(mt * 16 + g + 8 * h);  // true row (b4_pos is an involution)
+                for (int t = 0; t < NPU; ++t) {
+                    if (nt0 + t < ntl) {
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e)
-                            img[r * LDW + perm_w_bs(nt * 8 + 2 * tq + e, BS)] =
-                                acc[nt][0][2 * h + e] + (acc[nt][1][2 * h + e] + acc[nt][2][2 * h + e]);
+                        for (int e = 0; e < 2; ++e) {
+                            const int r = b4_pos((nt0 + t) * 8 + 2 * tq + e);
+                            *reinterpret_cast<float2*>(img + r * LDW + g * 2 * MT + mt * 2) =
+                                make_float2(acc[t][0][e] + (acc[t][1][e] + acc[t][2][e]),
+                                            acc[t][0][2 + e] + (acc[t][1][2 + e] + acc[t][2][2 + e]));
+                        }
+                    }
                 }
             } else {
                 // Sf = T~ G_{i,i+1} (A = T~, B[l][k] = GnT[k][l]);  Sb = T~^T G_{i,i-1} (A = T~^T)
-                const bool fwd = u - 2 * mtw < MT;
-                const int mt = fwd ? u - 2 * mtw : u - 2 * mtw - MT;
+                const int su = u - nW;
+                const bool fwd = doSf && su < MT;
+                const int mt = su % MT;
                 const float2* Am = fwd ? TfS : TTS;
                 const float* Bm = fwd ? GnT : GpT;
+                float acc[NT][3][4];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int b = 0; b < 3; ++b)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) acc[nt][b][e] = 0.f;
 #pragma unroll
                 for (int ks = 0; ks < KB; ++ks) {
                     const float2* a = Am + (mt * 16 + g) * LD2 + ks * 8 + tq;
@@ -433,13 +485,15 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
             }
         }
         // V rows: fragment order for both stages, plain for the gradient kernel
-        for (int idx = tid; idx < RB * BS; idx += NTH4) {
-            const int c = idx / RB, r = idx - c * RB;
-            const float v = Vc[(size_t)c * P + b4_pos(r)];
-            const int pv = perm_v_bs(c, BS);
-            IVf[r * LDV + pv] = v;
-            IVb[r * LDV + pv] = v;
-            IVB[r * LDV + c] = v;
+        for (int r = warp; r < RB; r += NTH4 / 32) {
+            const int pr = b4_pos(r);
+            for (int c = lane; c < BS; c += 32) {
+                const float v = Vc[(size_t)c * P + pr];
+                const int pv = perm_v_bs(c, BS);
+                IVf[r * LDV + pv] = v;
+                IVb[r * LDV + pv] = v;
+                IVB[r * LDV + c] = v;
+            }
         }
     }
     dev::fence_proxy_async_smem();
@@ -452,11 +506,18 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
         float* pf = p.Pf + ((size_t)(p.q - 1 - i) * C + rank) * SF;
         float* pb = p.Pb + ((size_t)i * C + rank) * SF;
         float* vbl = p.Vbl + ((size_t)i * p.d_pad + row0) * LDV;
-        bulk_s2g(pf, dev::smem_u32(IPF), (uint32_t)(SF * 4));
-        bulk_s2g(pb, dev::smem_u32(IPB), (uint32_t)(SF * 4));
+        const uint32_t wv = (uint32_t)(RB * (LDW + LDV) * 4), sb = (uint32_t)(BS * LDV * 4);
+        bulk_s2g(pf, dev::smem_u32(IPF), wv);
+        bulk_s2g(pb, dev::smem_u32(IPB), wv);
         bulk_s2g(vbl, dev::smem_u32(IVB), (uint32_t)(RB * LDV * 4));
+        const int soff = RB * (LDW + LDV);
+        for (int r = 0; r < C; ++r) {  // S into every CTA's slot of this block's stages
+            if (doSf) bulk_s2g(p.Pf + ((size_t)(p.q - 1 - i) * C + r) * SF + soff, dev::smem_u32(ISf), sb);
+            if (doSb) bulk_s2g(p.Pb + ((size_t)i * C + r) * SF + soff, dev::smem_u32(ISb), sb);
+        }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // shared memory may be released once read; the writes complete with the grid
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         BTRACE(7);
         if (p.trace) p.trace[((size_t)i * C + rank) * 10 + 9] = (long long)dev::globaltimer();
     }

@@ -31,6 +31,8 @@ def env_of(v):
 
 
 graphs = {}
+fine = {}
+REP = int(os.environ.get("STEP_REP", 10))
 for v in variants:
     env = env_of(v)
     old = {k: os.environ.get(k) for k in env}
@@ -45,6 +47,8 @@ for v in variants:
             t = fb.fasth_forward(V, X, b, ctx=ctx, out=outs[0])
             r = fb.fasth_backward(t, G)
             return r
+        if env.get("NODV"):  # step option, not a library knob: no gradient kernel
+            return fb.fasth_forward_backward(V, X, G, b, ctx=ctx, out=(outs[0], outs[1], None))
         return fb.fasth_forward_backward(V, X, G, b, ctx=ctx, out=outs)
     try:
         with torch.cuda.stream(s):
@@ -58,6 +62,14 @@ for v in variants:
         torch.cuda.synchronize()
         gr.replay()
         torch.cuda.synchronize()
+        # finer resolution: REP x (flush + step) in one graph, minus REP flushes
+        g10 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g10, stream=s):
+            for _ in range(REP):
+                flush.zero_()
+                keep10 = fn()
+        torch.cuda.synchronize()
+        fine[v] = g10
     except Exception as e:  # noqa: BLE001
         print(json.dumps({"variant": v, "error": str(e)[:200]}), flush=True)
         for k, val in old.items():
@@ -90,7 +102,33 @@ for rnd in range(int(os.environ.get("STEP_ROUNDS", 5))):
                 e.record(s)
                 e.synchronize()
                 times[v].append(a.elapsed_time(e) * 1e3)
+gfl = torch.cuda.CUDAGraph()
+sf = torch.cuda.Stream()
+with torch.cuda.graph(gfl, stream=sf):
+    for _ in range(REP):
+        flush.zero_()
+torch.cuda.synchronize()
+
+
+def time_graph(g, st, n=20):
+    ts = []
+    with torch.cuda.stream(st):
+        for _ in range(n):
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            g.replay()
+            e.record(st)
+            e.synchronize()
+            ts.append(a.elapsed_time(e) * 1e3)
+    return statistics.median(ts)
+
+
+fine_us = {}
+for rnd in range(3):
+    tf = time_graph(gfl, sf)
+    for v in variants:
+        fine_us.setdefault(v, []).append((time_graph(fine[v], graphs[v][1]) - tf) / REP)
 for v in variants:
     ts = sorted(times[v])
     print(json.dumps({"variant": v, "d": d, "m": m, "b": b, "two_call": two_call, "median_us": statistics.median(ts),
-                      "p10_us": ts[len(ts) // 10], "vs_first_variant_maxrel": graphs[v][4]}), flush=True)
+                      "p10_us": ts[len(ts) // 10], "fine_us": round(statistics.median(fine_us[v]), 2), "vs_first_variant_maxrel": graphs[v][4]}), flush=True)
