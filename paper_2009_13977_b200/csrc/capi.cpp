@@ -88,6 +88,9 @@ struct fasth_ctx_s {
     // activations the next build's L2 prefetch covers (set by the entry, consumed by build_plan)
     const float* pf[2] = {nullptr, nullptr};
     int64_t pf_ld[2] = {0, 0};
+    // the host-buffer step writes dV straight into the caller's pinned memory:
+    // there the gradient kernel runs behind the sweep (PCIe writes overlap it)
+    bool dv_pipe_pref = false;
     long long* step_trace = nullptr;
     int cur_m = 0;  // batch of the plan being built (step-trace sizing)
     size_t st_build = 0, st_sweep = 0, st_dv = 0, st_total = 0;
@@ -667,7 +670,7 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
 // warp that issues it, and every warp of the sweep is on the step's path).
 bool dv_pipe_ok(fasth_ctx c, const SweepV2Args& a) {
     const char* e = getenv("FASTH_DV_PIPE");
-    if (!e || atoi(e) == 0) return false;
+    if (e ? atoi(e) == 0 : !c->dv_pipe_pref) return false;
     return a.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) && !getenv("FASTH_TRACE");
 }
 
@@ -1429,21 +1432,37 @@ fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, 
     if ((!zc || atoi(zc) != 0) && nx * 4 <= (1u << 20) && !use_large_batch(d, n, m)) {
         const float *xm = mapped(X), *gm = mapped(G), *ym = mapped(Y), *dxm = mapped(dX);
         if (xm && gm && ym && dxm) {
-            x = const_cast<float*>(xm), g = const_cast<float*>(gm);
+            // Y, dX out: the sweep's 16-byte stores into the pinned buffers' mappings
             y = const_cast<float*>(ym), dx = const_cast<float*>(dxm);
-            // V in: an SM copy kernel over the pinned buffer's mapping (more
-            // PCIe reads in flight than the copy engine keeps: host_io.cu);
+            // V, X, G in: one SM copy kernel over the pinned buffers' mappings
+            // (more PCIe reads in flight than the copy engine keeps:
+            // host_io.cu), so the sweep reads X and G from device memory;
             // FASTH_H2D=dma for cudaMemcpyAsync
             const float* vm = mapped(V);
             const char* h2d = getenv("FASTH_H2D");
-            if (nv && vm && !(h2d && !strcmp(h2d, "dma")))
-                TRY(c->timed([&] { return launch_stream_copy(vm, v, (int64_t)nv, c->num_sms, c->stream); }, "h2d_copy"));
-            else if (nv)
-                CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
-            TRY(fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d, n ? dv : nullptr,
-                                       d));
+            if (nv && vm && !(h2d && !strcmp(h2d, "dma"))) {
+                const float* srcs[3] = {vm, xm, gm};
+                float* dsts[3] = {v, x, g};
+                const int64_t ns[3] = {(int64_t)nv, (int64_t)nx, (int64_t)nx};
+                TRY(c->timed([&] { return launch_stream_copy_n(srcs, dsts, ns, 3, c->num_sms, c->stream); }, "h2d_copy"));
+            } else {
+                if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
+                CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
+                CU(cudaMemcpyAsync(g, G, nx * 4, cudaMemcpyHostToDevice, c->stream));
+            }
+            // dV out: by default the gradient kernel stores straight into the
+            // pinned buffer's mapping (16-byte stores of whole columns), run
+            // behind the sweep so the PCIe writes overlap it; FASTH_D2H=dma
+            // (device buffer + cudaMemcpyAsync) or =kernel (+ SM copy kernel)
             float* dvm = const_cast<float*>(mapped(dV));
             const char* d2h = getenv("FASTH_D2H");
+            const bool direct = nv && dvm && !(d2h && (!strcmp(d2h, "dma") || !strcmp(d2h, "kernel")));
+            c->dv_pipe_pref = direct;
+            const fasth_status fs = fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d,
+                                                           n ? (direct ? dvm : dv) : nullptr, d);
+            c->dv_pipe_pref = false;
+            TRY(fs);
+            if (direct) return FASTH_OK;
             if (nv && dvm && d2h && !strcmp(d2h, "kernel"))
                 TRY(c->timed([&] { return launch_stream_copy(dv, dvm, (int64_t)nv, c->num_sms, c->stream); }, "d2h_copy"));
             else if (nv)

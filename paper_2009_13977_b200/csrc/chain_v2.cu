@@ -440,17 +440,40 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
     }
 
     if (warp < NR + MT && q > 0) step_stored();  // the last step's rows and Z'
+    // x_out: the row warps stage their tiles column-major in the (consumed)
+    // stage ring, then store 16 bytes at a time (whole lines: x_out may be a
+    // caller's pinned host buffer).  With the signal warp, after its last
+    // release, so that fence does not wait for these stores.
+    if (SIG && warp == SW) asm volatile("bar.arrive 2, %0;" ::"r"((NR + 1) * 32) : "memory");
     if (warp < NR) {
+        float* xs = stg;  // [WCV][RC + 4]
+        const int LX = RC + 4;
 #pragma unroll
         for (int u = 0; u < TPW; ++u) {
             const int rt = warp + u * NR;
             if (rt < RT) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int gr = row0 + rt * 16 + g + 8 * (e >> 1), gc = col0 + 2 * tq + (e & 1);
-                    if (gr < a.d && gc < a.m) D.x_out[(int64_t)gc * D.ldo + gr] = x[u][e];
-                    if (u == 0 && e == 0) GSTAMP(14);
-                }
+                for (int e = 0; e < 4; ++e) xs[(2 * tq + (e & 1)) * LX + rt * 16 + g + 8 * (e >> 1)] = x[u][e];
+            }
+        }
+        if (SIG) asm volatile("bar.sync 2, %0;" ::"r"((NR + 1) * 32) : "memory");
+        else dev::named_bar_sync<1>(NR * 32);
+        if (warp == 0 && lane == 0) GSTAMP(14);
+        const bool v4 = ((reinterpret_cast<uintptr_t>(D.x_out) & 15) == 0) && (D.ldo % 4 == 0);
+        const int nr4 = RC / 4;
+        for (int idx = warp * 32 + lane; idx < WCV * nr4; idx += NR * 32) {
+            const int c = idx / nr4, r = (idx - c * nr4) * 4;
+            const int gr = row0 + r, gc = col0 + c;
+            if (gc >= a.m || gr >= a.d) continue;
+            const float4 v = *reinterpret_cast<const float4*>(xs + c * LX + r);
+            float* dst = D.x_out + (int64_t)gc * D.ldo + gr;
+            if (v4 && gr + 4 <= a.d) {
+                *reinterpret_cast<float4*>(dst) = v;
+            } else {
+                dst[0] = v.x;
+                if (gr + 1 < a.d) dst[1] = v.y;
+                if (gr + 2 < a.d) dst[2] = v.z;
+                if (gr + 3 < a.d) dst[3] = v.w;
             }
         }
     }

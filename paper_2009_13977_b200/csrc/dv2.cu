@@ -66,7 +66,9 @@ __device__ __forceinline__ void mma3(float (&m)[4], float (&c)[4], const AF& a, 
 
 template <int BS>
 __host__ __device__ constexpr size_t dv2_smem() {
-    // Zb | Zf chunk (BS x (MCH+4) each), Q (BS x (BS+1))
+    // Zb | Zf chunk (BS x (MCH+4) each; later the dV staging tile,
+    // BS x (DV_ROWS+4) <= that), Q (BS x (BS+1))
+    static_assert(BS * (DV_ROWS + 4) <= 2 * BS * (MCH + 4), "dV staging fits the Z' chunks");
     return 4 * ((size_t)2 * BS * (MCH + 4) + (size_t)BS * (BS + 1));
 }
 
@@ -245,12 +247,8 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     }
     __syncthreads();
     if (trc) trc[3] = (long long)dev::globaltimer();
-    if (!rows_ok) {
-        if (trc) trc[4] = (long long)dev::globaltimer();
-        return;
-    }
 #pragma unroll
-    for (int ks = 0; ks < KB; ++ks) {
+    for (int ks = 0; ks < KB && rows_ok; ++ks) {
         const AF fV = split4(fv[ks]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -263,19 +261,41 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
             mma3(acc[nt], cc[nt], fV, bh, bl);
         }
     }
-    // dV = -2 * result, straight from the accumulators (chain order; the V^T
-    // leg un-reverses, svd_layer.hpp:150-151)
+    // dV = -2 * result (chain order; the V^T leg un-reverses,
+    // svd_layer.hpp:150-151), staged column-major in shared memory (over the
+    // dead Z' chunks) so that each column's 64 rows leave as 16-byte stores:
+    // full lines, which matters when dV is the caller's pinned host buffer
+    constexpr int LDS_ = DV_ROWS + 4;
+    float* stg = dsm;
+    if (rows_ok) {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int j = nt * 8 + 2 * tq + (e & 1), r = r0 + g + 8 * (e >> 1);
+            for (int e = 0; e < 4; ++e)
+                stg[(nt * 8 + 2 * tq + (e & 1)) * LDS_ + warp * 16 + g + 8 * (e >> 1)] = -2.f * (acc[nt][e] + cc[nt][e]);
+    }
+    __syncthreads();
+    {
+        const int rb0 = blockIdx.x * DV_ROWS;
+        const int wb = min(a.b, a.n - i * a.b);
+        const bool v4 = ((reinterpret_cast<uintptr_t>(a.dV) & 15) == 0) && (a.lddv % 4 == 0);
+        for (int idx = tid; idx < BS * (DV_ROWS / 4); idx += DV_WARPS * 32) {
+            const int j = idx / (DV_ROWS / 4), rr = (idx - j * (DV_ROWS / 4)) * 4, row = rb0 + rr;
+            if (j >= wb || row >= a.d) continue;
             const int kc = i * a.b + j;
-            if (j < a.b && kc < a.n && r < a.d) {
-                const int col = a.reversed ? a.n - 1 - kc : kc;
-                a.dV[(int64_t)col * a.lddv + r] = -2.f * (acc[nt][e] + cc[nt][e]);
+            const int col = a.reversed ? a.n - 1 - kc : kc;
+            float* dst = a.dV + (int64_t)col * a.lddv + row;
+            const float4 v = *reinterpret_cast<const float4*>(stg + j * LDS_ + rr);
+            if (v4 && row + 4 <= a.d) {
+                *reinterpret_cast<float4*>(dst) = v;
+            } else {
+                dst[0] = v.x;
+                if (row + 1 < a.d) dst[1] = v.y;
+                if (row + 2 < a.d) dst[2] = v.z;
+                if (row + 3 < a.d) dst[3] = v.w;
             }
         }
+    }
     if (trc) trc[4] = (long long)dev::globaltimer();
 }
 

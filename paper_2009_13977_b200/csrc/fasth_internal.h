@@ -161,6 +161,8 @@ size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg);
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
 // host_io.cu: streaming copy kernel (either side may be a pinned-host mapping)
 cudaError_t launch_stream_copy(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s);
+cudaError_t launch_stream_copy_n(const float* const* src, float* const* dst, const int64_t* n, int nseg, int num_sms,
+                                 cudaStream_t s);
 // wy_api.cu: the reference's WY internals (wy.hpp:56-170) in its own layout
 // W, Y (column-major d x n, block z = columns [z bw, z bw + w_z)); scratch of
 // wy_compact_scratch_doubles(n, bw) doubles; T of b * m doubles for wy_apply

@@ -36,7 +36,70 @@ __global__ void copy1_kernel(const float* __restrict__ src, float* __restrict__ 
         dst[i] = src[i];
 }
 
+struct Segs {
+    const float4* src[4];
+    float4* dst[4];
+    int64_t end[4];  // cumulative float4 counts
+    int n;
+};
+
+// several 16-byte aligned copies in one launch (the host step's V, X, G)
+__global__ void __launch_bounds__(kCopyThreads) copyn_kernel(Segs sg) {
+    const int64_t total = sg.end[sg.n - 1];
+    const int64_t stride = (int64_t)gridDim.x * kCopyThreads;
+    auto at = [&](int64_t k, const float4*& s, float4*& d) {
+        int j = 0;
+        while (j + 1 < sg.n && k >= sg.end[j]) ++j;
+        const int64_t o = k - (j ? sg.end[j - 1] : 0);
+        s = sg.src[j] + o, d = sg.dst[j] + o;
+    };
+    for (int64_t i = (int64_t)blockIdx.x * kCopyThreads + threadIdx.x; i < total; i += kUnroll * stride) {
+        float4 v[kUnroll];
+        float4* dp[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t k = i + u * stride;
+            dp[u] = nullptr;
+            if (k < total) {
+                const float4* sp;
+                at(k, sp, dp[u]);
+                v[u] = __ldcs(sp);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (dp[u]) __stcs(dp[u], v[u]);
+    }
+}
+
 }  // namespace
+
+// dst[j][0..n[j]) = src[j][0..n[j]) for up to 4 segments in one launch when
+// every segment is 16-byte aligned with n % 4 == 0, else one launch each.
+cudaError_t launch_stream_copy_n(const float* const* src, float* const* dst, const int64_t* n, int nseg, int num_sms,
+                                 cudaStream_t s) {
+    Segs sg{};
+    bool vec = nseg <= 4;
+    int64_t tot = 0;
+    for (int j = 0; j < nseg && vec; ++j) {
+        vec = !((reinterpret_cast<uintptr_t>(src[j]) | reinterpret_cast<uintptr_t>(dst[j])) & 15) && n[j] % 4 == 0;
+        if (n[j] <= 0) continue;
+        sg.src[sg.n] = reinterpret_cast<const float4*>(src[j]);
+        sg.dst[sg.n] = reinterpret_cast<float4*>(dst[j]);
+        tot += n[j] / 4;
+        sg.end[sg.n++] = tot;
+    }
+    if (!vec) {
+        for (int j = 0; j < nseg; ++j)
+            if (cudaError_t e = launch_stream_copy(src[j], dst[j], n[j], num_sms, s); e != cudaSuccess) return e;
+        return cudaSuccess;
+    }
+    if (sg.n == 0) return cudaSuccess;
+    const int64_t want = (tot + kCopyThreads * kUnroll - 1) / (kCopyThreads * kUnroll);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms * 4));
+    copyn_kernel<<<grid, kCopyThreads, 0, s>>>(sg);
+    return cudaGetLastError();
+}
 
 // dst[0..n) = src[0..n) where either side may be a device view of pinned
 // host memory; 16-byte aligned buffers take the vector kernel.

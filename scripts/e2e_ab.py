@@ -1,0 +1,53 @@
+"""A/B of the host-buffer step (fasth_forward_backward_host, the e2e number)
+under env-knob variants, each with its own context (its cached graph is built
+under the variant's env): median wall time per call, and agreement of Y, dX,
+dV with the first variant.  usage: e2e_ab.py base FASTH_D2H=dma ..."""
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2009_13977_b200 import fasth as fb  # noqa: E402
+
+d, m, b = (int(os.environ.get(k, v)) for k, v in (("E2E_D", 784), ("E2E_M", 32), ("E2E_B", 32)))
+torch.manual_seed(0)
+Vh, Xh, Gh = torch.randn(d, d).pin_memory(), torch.randn(m, d).pin_memory(), torch.randn(m, d).pin_memory()
+variants = sys.argv[1:] or ["base"]
+ref = None
+rows = {}
+for rnd in range(3):
+    for v in variants:
+        env = {} if v == "base" else dict(kv.split("=", 1) for kv in v.split(","))
+        old = {k: os.environ.get(k) for k in env}
+        os.environ.update(env)
+        try:
+            if v not in rows:
+                ctx = fb.Context(0)
+                out = tuple(torch.empty(s).pin_memory() for s in ((m, d), (m, d), (d, d)))
+                for _ in range(5):
+                    fb.forward_backward_host(Vh, Xh, Gh, b, ctx=ctx, out=out)
+                rows[v] = {"ctx": ctx, "out": out, "t": []}
+            r = rows[v]
+            for _ in range(100):
+                t0 = time.perf_counter()
+                fb.forward_backward_host(Vh, Xh, Gh, b, ctx=r["ctx"], out=r["out"])
+                r["t"].append((time.perf_counter() - t0) * 1e6)
+        finally:
+            for k, val in old.items():
+                if val is None:
+                    os.environ.pop(k, None)
+                else:
+                    os.environ[k] = val
+for v in variants:
+    r = rows[v]
+    o = [t.double() for t in r["out"]]
+    if ref is None:
+        ref = o
+    err = max(float((a - w).norm() / w.norm()) for a, w in zip(o, ref))
+    print(json.dumps({"variant": v, "median_us": round(statistics.median(r["t"]), 1),
+                      "p10_us": round(sorted(r["t"])[len(r["t"]) // 10], 1), "vs_first_maxrel": err}), flush=True)
