@@ -9,7 +9,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $R/smoke.log 2>
 timeout 600 python bench.py > $R/bench.log 2>&1
 timeout 300 python bench.py --impl reference --steps 10 --warmup 3 > $R/bench_ref.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $R/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > $R/b_ncu.log 2>&1
-for k in sweep2 build2 dv2; do
+for k in sweep2 build4 dv2; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 -o $R/${k}_full python bench.py --steps 2 --warmup 3 --no-cpu > $R/ncu_$k.log 2>&1
 done
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:panel -s 2 -c 1 -o $R/panel_full python scripts/bench_config5.py --m-per-gpu 1024 --steps 1 --warmup 1 > $R/ncu_panel.log 2>&1
