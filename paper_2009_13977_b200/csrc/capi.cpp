@@ -665,12 +665,16 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
 // each block's finished tape rows (done[i]) and the gradient kernel, launched
 // as its programmatic dependent, starts on a block as soon as both chains
 // have passed it.  Not for the panel sweep (it keeps no counters).
-// Opt-in (FASTH_DV_PIPE=1): measured slower at the metric config (the
-// per-step release fence that publishes a block costs ~900 cycles on the
-// warp that issues it, and every warp of the sweep is on the step's path).
+// The publishing costs the sweep ~1 us (a signal warp outside the step's
+// barriers, sweep2_kernel<.., SIG>); the gradient tail it removes is worth
+// more where the blocks finish in sweep order (fasth_backward: block t after
+// step t; 101.9 vs 103.2 us for the two-call step) and where dV goes out over
+// PCIe (the host-buffer step), not for the fused device step (blocks finish
+// only from mid-sweep on: 62.3 vs 60.9 us).  FASTH_DV_PIPE=0/1 forces it.
 bool dv_pipe_ok(fasth_ctx c, const SweepV2Args& a) {
     const char* e = getenv("FASTH_DV_PIPE");
-    if (e ? atoi(e) == 0 : !c->dv_pipe_pref) return false;
+    const bool dflt = c->dv_pipe_pref || (a.ndir == 1 && !a.dir[0].forward);
+    if (e ? atoi(e) == 0 : !dflt) return false;
     return a.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) && !getenv("FASTH_TRACE");
 }
 
