@@ -675,7 +675,9 @@ bool dv_pipe_ok(fasth_ctx c, const SweepV2Args& a) {
     const char* e = getenv("FASTH_DV_PIPE");
     const bool dflt = c->dv_pipe_pref || (a.ndir == 1 && !a.dir[0].forward);
     if (e ? atoi(e) == 0 : !dflt) return false;
-    return a.q <= kMaxPipeQ && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) && !getenv("FASTH_TRACE");
+    // (the signal-warp sweep spills at 64-wide blocks: not there)
+    return a.q <= kMaxPipeQ && a.BS <= 32 && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) &&
+           !getenv("FASTH_TRACE");
 }
 
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).

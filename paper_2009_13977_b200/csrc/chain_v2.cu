@@ -74,8 +74,13 @@ __host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg) 
     return L;
 }
 
-template <int BS, int TPW, bool SIG>
-__global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_kernel(SweepV2Args a) {
+// NP > 0: NP "push" warps take the combine of the row warps' partials and
+// the DSMEM pushes off the row warps (which then only run the partial MMAs
+// and the update per step); for NR <= kPushMaxNR row warps.
+constexpr int kPushMaxNR = 6;
+template <int BS, int TPW, bool SIG, int NP>
+__global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP + SIG) * 32, 1)
+    sweep2_kernel(SweepV2Args a) {
     constexpr int MT = BS / 16, KB = BS / 8;
     constexpr int LDW = stage_ldw(BS), LDV = stage_ldv(BS);
     constexpr int WOFF = 0;
@@ -109,8 +114,10 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
     // pipelined gradient (SIG, a.done set): one more warp, outside the CTA
     // barriers of the step loop, publishes each finished block (gpu-scope
     // fence + counter) so that no warp on the step's path pays for the fence
-    const int SW = SIG ? PW + 1 : 1 << 30;
-    const int nmain = (NR + MT + 1) * 32;
+    const int PU0 = PW + 1;  // first push warp (NP > 0)
+    const int SW = SIG ? PW + 1 + NP : 1 << 30;
+    const int nmain = (NR + MT + 1 + NP) * 32;
+    const bool pusher = NP > 0 && warp >= PU0 && warp < PU0 + NP;
     unsigned* prog = reinterpret_cast<unsigned*>(bars + NSTG + NSLOTV);
     long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
     // prologue / epilogue global-timer stamps in row q: 10 entry, 11 X loaded,
@@ -126,7 +133,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
             asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(dummy_) : "r"(bar_u32)); \
             if (dummy_ == 0xdeadbeefu) wtr[0] = 0;                                           \
         }                                                                                     \
-        wtr[((size_t)t * 12 + warp) * 4 + (k)] = clock64();                                  \
+        if (warp < 12) wtr[((size_t)t * 12 + warp) * 4 + (k)] = clock64();                   \
     }
 #define GSTAMP(k) \
     if (trc && tid == 0) trc[(size_t)q * 16 + (k)] = (long long)dev::globaltimer()
@@ -187,6 +194,41 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
     const size_t tape_step = (size_t)a.ngroups * a.d_pad * WCV;
     float* const tape0 = D.tape ? D.tape + ((size_t)group * a.d_pad + row0) * WCV : nullptr;
 
+    // the CTA's sum of the row warps' partials (fixed order; all loads in
+    // flight), pushed to CTAs first, first + step, ... of the cluster
+    auto combine_push = [&](int s, int first, int step) {
+        if (first >= C) return;
+        float sum[MT][4];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
+            float part[MAXNR][4];
+#pragma unroll
+            for (int w = 0; w < MAXNR; ++w)
+                if (w < NR) lds_vec<4>(part[w], red + (w * MT + mt) * 128 + lane * 4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) sum[mt][e] = part[0][e];
+#pragma unroll
+            for (int w = 1; w < MAXNR; ++w)
+                if (w < NR)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) sum[mt][e] += part[w][e];
+        }
+        const int slot = s % NSLOTV;
+        const uint32_t off = zr_u32 + (uint32_t)((((slot * C + (int)rank) * MT) * 128 + lane * 4) * 4);
+        const uint32_t rbar_l = exb_u32 + 8u * slot;
+        if (C == 1) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) dev::put4_local(off + mt * 512u, sum[mt]);
+            dev::complete_tx_local(rbar_l, (uint32_t)MT * 16u);
+        } else {
+            for (int dst = first; dst < C; dst += step) {
+                const uint32_t rz = dev::mapa(off, dst), rb = dev::mapa(rbar_l, dst);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) push4(rz + mt * 512u, sum[mt], rb);
+            }
+        }
+    };
+
     // ---- phase-1 work of the row warps: L partial for step s (stage ss) from X^(cur)
     auto partial_push = [&](int s, int ss) {
         const float* Ws = stg + ss * SF;
@@ -224,47 +266,25 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
                 make_float4(pm[mt][0] + (p1[mt][0] + p2[mt][0]), pm[mt][1] + (p1[mt][1] + p2[mt][1]),
                             pm[mt][2] + (p1[mt][2] + p2[mt][2]), pm[mt][3] + (p1[mt][3] + p2[mt][3]));
         if (trc && tid == 0) trc[(size_t)(s > 0 ? s - 1 : q) * 16 + 1] = clock64();
+        if constexpr (NP > 0) {  // hand the partials to the push warps, go on
+            asm volatile("bar.arrive 4, %0;" ::"r"((NR + NP) * 32) : "memory");
+            return;
+        }
         // every row warp forms the CTA's sum (fixed order over the row warps;
         // all loads in flight) and pushes it to its own destinations
         // (warp, warp + NR, ...): the pushes are spread over the row warps
         dev::named_bar_sync<1>(NR * 32);
-        if (warp < C) {
-            float sum[MT][4];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                float part[MAXNR][4];
-#pragma unroll
-                for (int w = 0; w < MAXNR; ++w)
-                    if (w < NR) lds_vec<4>(part[w], red + (w * MT + mt) * 128 + lane * 4);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) sum[mt][e] = part[0][e];
-#pragma unroll
-                for (int w = 1; w < MAXNR; ++w)
-                    if (w < NR)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) sum[mt][e] += part[w][e];
-            }
-            const int slot = s % NSLOTV;
-            const uint32_t off = zr_u32 + (uint32_t)((((slot * C + (int)rank) * MT) * 128 + lane * 4) * 4);
-            const uint32_t rbar_l = exb_u32 + 8u * slot;
-            if (C == 1) {
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) dev::put4_local(off + mt * 512u, sum[mt]);
-                dev::complete_tx_local(rbar_l, (uint32_t)MT * 16u);
-            } else {
-                for (int dst = warp; dst < C; dst += NR) {
-                    const uint32_t rz = dev::mapa(off, dst), rb = dev::mapa(rbar_l, dst);
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) push4(rz + mt * 512u, sum[mt], rb);
-                }
-            }
-        }
+        combine_push(s, warp, NR);
     };
-
+    auto push_step = [&](int s) {  // push warps: partials of step s -> peers
+        asm volatile("bar.sync 4, %0;" ::"r"((NR + NP) * 32) : "memory");
+        combine_push(s, warp - PU0, NP);
+    };
     if (warp < NR && q > 0) {  // prologue: Z_0's partials from X^(0)
         mbar_wait_u32(bar_u32, 0);
         partial_push(0, 0);
     }
+    if (pusher && q > 0) push_step(0);
     GSTAMP(13);
     __syncthreads();  // the combine scratch is reused by step 0's partial
 
@@ -360,6 +380,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
             for (int e = 0; e < 4; ++e) z[e] = cm[e] + (c1[e] + c2[e]);
             const float* zr = Zr + ((size_t)slot * C * MT + mt) * 128 + lane * 4;
             float zs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
             for (int c = 0; c < C; ++c) {  // fixed order over the source CTAs
                 float p[4];
                 lds_vec<4>(p, zr + c * MT * 128);
@@ -388,10 +409,17 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
                 bulk_u32(dev::smem_u32(stg) + (uint32_t)sp * stage_bytes, gstage(tn), stage_bytes,
                          bar_u32 + 8u * sp);
             }
+        } else if (pusher) {
+            if (t + 1 < q) push_step(t + 1);
         }
         WSTAMP(0);
-        if constexpr (SIG) asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
-        else __syncthreads();
+        if constexpr (NP > 0) {  // barrier 1 without the push warps: Z_t -> the update
+            if (!pusher) asm volatile("bar.sync 2, %0;" ::"r"((NR + MT + 1) * 32) : "memory");
+        } else if constexpr (SIG) {
+            asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
+        } else {
+            __syncthreads();
+        }
         WSTAMP(1);
         if (trc && tid == 0) trc[(size_t)t * 16 + 5] = clock64();
         // ---------------- phase 2: X^(t+1) = X^(t) + V_t (-2 Z_t) ----------------
@@ -432,8 +460,19 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
             if (trc && tid == 0) trc[(size_t)t * 16 + 6] = clock64();
         }
         WSTAMP(2);
-        if constexpr (SIG) asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
-        else __syncthreads();
+        if constexpr (NP > 0) {
+            // barrier 2 without the B warps: they run ahead into Z_{t+1}
+            // (exchange wait, reduce) while the row warps update X.  Safe: B
+            // warps overwrite Zn[t & 1] only in step t+2, after barrier 1 of
+            // step t+1, which the row warps reach after reading it here; their
+            // S reads of a stage precede barrier 1, the refill follows this one
+            if (warp < NR || warp == PW || pusher)
+                asm volatile("bar.sync 3, %0;" ::"r"((NR + 1 + NP) * 32) : "memory");
+        } else if constexpr (SIG) {
+            asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
+        } else {
+            __syncthreads();
+        }
         WSTAMP(3);
         if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64(), trc[(size_t)t * 16 + 9] = (long long)dev::globaltimer();
         if (++st == NSTG) st = 0, ph ^= 1;
@@ -444,7 +483,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
     // stage ring, then store 16 bytes at a time (whole lines: x_out may be a
     // caller's pinned host buffer).  With the signal warp, after its last
     // release, so that fence does not wait for these stores.
-    if (SIG && warp == SW) asm volatile("bar.arrive 2, %0;" ::"r"((NR + 1) * 32) : "memory");
+    if (SIG && warp == SW) asm volatile("bar.arrive 5, %0;" ::"r"((NR + 1) * 32) : "memory");
     if (warp < NR) {
         float* xs = stg;  // [WCV][RC + 4]
         const int LX = RC + 4;
@@ -456,7 +495,7 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
                 for (int e = 0; e < 4; ++e) xs[(2 * tq + (e & 1)) * LX + rt * 16 + g + 8 * (e >> 1)] = x[u][e];
             }
         }
-        if (SIG) asm volatile("bar.sync 2, %0;" ::"r"((NR + 1) * 32) : "memory");
+        if (SIG) asm volatile("bar.sync 5, %0;" ::"r"((NR + 1) * 32) : "memory");
         else dev::named_bar_sync<1>(NR * 32);
         if (warp == 0 && lane == 0) GSTAMP(14);
         const bool v4 = ((reinterpret_cast<uintptr_t>(D.x_out) & 15) == 0) && (D.ldo % 4 == 0);
@@ -484,16 +523,16 @@ __global__ void __launch_bounds__((MAXNR + BS / 16 + 1 + SIG) * 32, 1) sweep2_ke
 #undef WSTAMP
 }
 
-template <int BS, int TPW>
+template <int BS, int TPW, int NP>
 cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
     const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg);
-    auto kern = a.done ? sweep2_kernel<BS, TPW, true> : sweep2_kernel<BS, TPW, false>;
+    auto kern = a.done ? sweep2_kernel<BS, TPW, true, NP> : sweep2_kernel<BS, TPW, false, NP>;
     if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total, true); e != cudaSuccess) return e;
     const int RT = a.d_pad / a.C / 16;
     const int NR = RT < MAXNR ? RT : MAXNR;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.C * a.ngroups * a.ndir, 1, 1);
-    cfg.blockDim = dim3((NR + BS / 16 + 1 + (a.done ? 1 : 0)) * 32, 1, 1);
+    cfg.blockDim = dim3((NR + BS / 16 + 1 + NP + (a.done ? 1 : 0)) * 32, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -508,12 +547,17 @@ cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
+// push warps (NP = 2) where the row-warp count allows them; FASTH_PUSHW=0 off
 template <int TPW>
 cudaError_t launch_bs(const SweepV2Args& a, cudaStream_t s) {
+    const int RT = a.d_pad / a.C / 16;
+    const int NR = RT < MAXNR ? RT : MAXNR;
+    const char* e = getenv("FASTH_PUSHW");
+    const bool push = TPW == 1 && NR <= kPushMaxNR && (!e || atoi(e) != 0);
     switch (a.BS) {
-        case 16: return launch_t<16, TPW>(a, s);
-        case 32: return launch_t<32, TPW>(a, s);
-        case 64: return launch_t<64, TPW>(a, s);
+        case 16: return push ? launch_t<16, TPW, 2>(a, s) : launch_t<16, TPW, 0>(a, s);
+        case 32: return push ? launch_t<32, TPW, 2>(a, s) : launch_t<32, TPW, 0>(a, s);
+        case 64: return launch_t<64, TPW, 0>(a, s);
         default: return cudaErrorInvalidValue;
     }
 }
