@@ -172,15 +172,19 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
 #pragma unroll
             for (int e = 0; e < 4; ++e) x[u][e] = 0.f;
             if (rt < RT) {
+                // all loads in flight before any use (branch-free: a guarded
+                // load per element was four serial L2 round trips, ~1.4 us)
+                float v[4], sc[4];
+                bool ok[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int gr = row0 + rt * 16 + g + 8 * (e >> 1), gc = col0 + 2 * tq + (e & 1);
-                    if (gr < D.n_valid && gc < a.m) {
-                        float v = D.x_in[(int64_t)gc * D.ldx + gr];
-                        if (D.scale) v *= D.scale[gr];
-                        x[u][e] = v;
-                    }
+                    ok[e] = gr < D.n_valid && gc < a.m;
+                    v[e] = D.x_in[ok[e] ? (int64_t)gc * D.ldx + gr : 0];
+                    sc[e] = D.scale ? D.scale[ok[e] ? gr : 0] : 1.f;
                 }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[u][e] = ok[e] ? v[e] * sc[e] : 0.f;
                 scatter_cb(Xn + rt * 256, Xn + rt * 256 + 128, x[u], g, tq, 1.f);
             }
         }
