@@ -1456,6 +1456,9 @@ fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, 
                 CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
                 CU(cudaMemcpyAsync(g, G, nx * 4, cudaMemcpyHostToDevice, c->stream));
             }
+            // the copy is ordered after any cross-stream wait: the step's own
+            // launches may chain programmatically again
+            c->after_stream_wait = false;
             // dV out: by default the gradient kernel stores straight into the
             // pinned buffer's mapping (16-byte stores of whole columns), run
             // behind the sweep so the PCIe writes overlap it; FASTH_D2H=dma
