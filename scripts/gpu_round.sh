@@ -17,3 +17,11 @@ for m in 1024 8192; do timeout 300 python scripts/bench_config5.py --m-per-gpu $
 timeout 900 python scripts/bench_configs.py > $R/configs.log 2>&1
 timeout 300 python tools/fasth_bench_b200.py --d 256:256:4 --reps 20 --algo fasth,ref-fasth > $R/cli_mul.csv 2>&1
 ls -la $R
+mkdir -p gpurun_out/round/st
+FASTH_STEPTRACE=gpurun_out/round/st/t timeout 300 python scripts/step_trace_run.py > gpurun_out/round/timeline.txt 2>&1
+FASTH_STEPTRACE=gpurun_out/round/st/e timeout 300 python scripts/e2e_trace.py >> gpurun_out/round/timeline.txt 2>&1
+FASTH_TRACE=gpurun_out/round/st/f timeout 300 python scripts/trace_fused.py 784 32 32 > /dev/null 2>&1
+python scripts/trace_report.py "gpurun_out/round/st/f.sweep(fwd+bwd).v2.bin" "gpurun_out/round/st/f.sweep(fwd+bwd).warps.bin" > gpurun_out/round/sweep_trace.txt 2>&1
+python scripts/build_timeline.py gpurun_out/round/st/f.build.bin 25 > gpurun_out/round/build_timeline.txt 2>&1
+timeout 300 python scripts/replay_overhead.py > gpurun_out/round/replay_overhead.txt 2>&1
+timeout 300 python scripts/e2e_ab.py base FASTH_D2H=dma > gpurun_out/round/e2e_ab.txt 2>&1
