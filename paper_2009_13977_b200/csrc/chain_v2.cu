@@ -378,7 +378,9 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             const int slot = t % NSLOTV;
             mbar_wait_u32(exb_u32 + 8u * slot, (uint32_t)((t / NSLOTV) & 1));
             if (trc && lane == 0 && mt == 0) trc[(size_t)t * 16 + 3] = clock64();
-            if (lane == 0 && mt == 0) mbar_expect_u32(exb_u32 + 8u * slot, ex_bytes);
+            // re-arm the slot for step t + NSLOTV (relaxed: it publishes nothing
+            // of this thread's, and rank 0's B warp has Z' stores outstanding)
+            if (lane == 0 && mt == 0) mbar_expect_relaxed_u32(exb_u32 + 8u * slot, ex_bytes);
             float z[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) z[e] = cm[e] + (c1[e] + c2[e]);

@@ -107,6 +107,12 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// re-arming a barrier that publishes nothing of this thread's: a relaxed
+// arrive (a release arrive waits for the thread's outstanding global stores)
+__device__ __forceinline__ void mbar_expect_relaxed_u32(uint32_t a, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_expect_u32(uint32_t a, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
                  : "memory");
