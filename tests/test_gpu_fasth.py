@@ -349,10 +349,11 @@ def test_host_buffer_entry(fb, oracle):
 @pytest.mark.parametrize("d,n,m,b", [(784, 784, 32, 32), (200, 200, 17, 6), (64, 64, 32, 8), (300, 45, 8, 16),
                                      (96, 5, 3, 32), (128, 128, 100, 32)])
 def test_host_pipelined_equals_device_bitwise(fb, d, n, m, b):
-    """The host-buffer call overlaps V's chunked upload with the WY builds
-    and the sweeps (readiness counters): same kernels, same arithmetic as the
-    device-resident fasth_forward_backward, so identical bits; repeated to
-    exercise the self-resetting counters."""
+    """The host-buffer call (V, X, G in by one SM copy kernel; dV stored by
+    the gradient kernel straight into the pinned buffer while the sweep still
+    runs, Y / dX by the sweep's 16-byte stores; ragged shapes take the scalar
+    tails): same arithmetic as the device-resident fasth_forward_backward, so
+    identical bits; repeated to exercise the self-resetting block counters."""
     import torch
     rng = np.random.default_rng(d + 7 * n + m)
     V, X, G = rng.standard_normal((n, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
