@@ -548,7 +548,8 @@ fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what)
         return c->timed([&] { return launch_panel(a, c->stream); }, "panel(fwd/bwd)");
     }
     if (!prefix) {
-        const bool st = getenv("FASTH_STEPTRACE") && c->step_trace && c->st_hdr[2] > 0 && a.ndir == 2;
+        const bool st = getenv("FASTH_STEPTRACE") && c->step_trace && c->st_hdr[2] > 0 &&
+                        (a.ndir == 2 || !a.dir[0].forward);  // the fused launch or the backward sweep
         a.trace = st ? c->step_trace + c->st_sweep : nullptr;
         a.wtrace = nullptr;
         if (st) c->st_hdr[3] = a.C * a.ngroups * a.ndir;
@@ -606,6 +607,8 @@ SweepV2Args v2_args(fasth_tape t) {
     a.C = t->C;
     a.nstg = t->v2nstg;
     a.ngroups = t->ngroups;
+    a.pub_ns = 256;
+    if (const char* e = getenv("FASTH_PUB_NS")) a.pub_ns = atoi(e);
     return a;
 }
 
@@ -677,7 +680,7 @@ bool dv_pipe_ok(fasth_ctx c, const SweepV2Args& a) {
     if (e ? atoi(e) == 0 : !dflt) return false;
     // (the signal-warp sweep spills at 64-wide blocks: not there)
     return a.q <= kMaxPipeQ && a.BS <= 32 && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) &&
-           !getenv("FASTH_TRACE");
+           (!getenv("FASTH_TRACE") || e) && sweep2_smem_bytes(a.C, a.BS, a.d_pad, a.nstg, true) <= 227 * 1024;
 }
 
 // Backward (Alg. 2): sweep (step 1) + blocked gradients (step 2).
@@ -729,9 +732,11 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
         v.done_target = (unsigned)(ndir * t->ngroups * t->C);
         v.order = order;
         // keep the gradient CTAs off the sweep's SMs (FASTH_DV_SMEM overrides)
-        const size_t sw = sweep2_smem_bytes(t->C, p.BS, p.d_pad, t->v2nstg);
+        const size_t sw = sweep2_smem_bytes(t->C, p.BS, p.d_pad, t->v2nstg, true);
         v.min_smem = sw < 227 * 1024 ? 227 * 1024 - sw + 1024 : 0;
         if (const char* e = getenv("FASTH_DV_SMEM")) v.min_smem = (size_t)atol(e);
+        v.poll_ns = 128;
+        if (const char* e = getenv("FASTH_DV_POLL")) v.poll_ns = atoi(e);
     }
     v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
     c->after_stream_wait = false;

@@ -52,7 +52,9 @@ struct V2Smem {
     size_t stg, zr, xn, zn, red, bars, total;
 };
 
-__host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg) {
+// sig: the tape-warp variant double-buffers the pre-split X (the tape warp
+// reads X^(t+1) while the row warps already form X^(t+2))
+__host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg, bool sig) {
     const int RC = d_pad / C, RT = RC / 16, MT = BS / 16, KB = BS / 8;
     const int NR = RT < MAXNR ? RT : MAXNR;
     V2Smem L;
@@ -62,14 +64,14 @@ __host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg) 
     L.zr = o;
     o += (size_t)NSLOTV * C * MT * 128;
     L.xn = o;
-    o += (size_t)RT * 256;
+    o += (size_t)RT * 256 * (sig ? 2 : 1);
     L.zn = o;
     o += (size_t)2 * KB * 128;
     L.red = o;
     o += (size_t)NR * MT * 128;
     o = (o + 3) & ~size_t(3);
     L.bars = o;
-    o += 2 * (nstg + NSLOTV) + 2;  // + the progress counter of the signal warp
+    o += 2 * (nstg + NSLOTV) + 6;  // + the tape warp's two mbarriers and step counter
     L.total = o * 4;
     return L;
 }
@@ -79,7 +81,7 @@ __host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg) 
 // and the update per step); for NR <= kPushMaxNR row warps.
 constexpr int kPushMaxNR = 6;
 template <int BS, int TPW, bool SIG, int NP>
-__global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP + SIG) * 32, 1)
+__global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP + (SIG ? (TPW == 1 ? 2 : 1) : 0)) * 32, 1)
     sweep2_kernel(SweepV2Args a) {
     constexpr int MT = BS / 16, KB = BS / 8;
     constexpr int LDW = stage_ldw(BS), LDV = stage_ldv(BS);
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     const int C = a.C, q = a.q, NSTG = a.nstg;
     const int RC = a.d_pad / C, RT = RC / 16;
     const int NR = RT < MAXNR ? RT : MAXNR;
-    const V2Smem L = v2_layout(C, BS, a.d_pad, NSTG);
+    const V2Smem L = v2_layout(C, BS, a.d_pad, NSTG, SIG);
     const int SF = (int)stage_floats(RC, BS);
     const int VOFF = RC * LDW, SOFF = RC * (LDW + LDV);
     float* stg = sm + L.stg;
@@ -111,14 +113,25 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     const uint32_t stage_bytes = (uint32_t)SF * 4u;
     const uint32_t ex_bytes = (uint32_t)C * MT * 512u;
     const int PW = NR + MT;  // producer warp
-    // pipelined gradient (SIG, a.done set): one more warp, outside the CTA
-    // barriers of the step loop, publishes each finished block (gpu-scope
-    // fence + counter) so that no warp on the step's path pays for the fence
+    // pipelined gradient (SIG, a.done set): two more warps outside the CTA
+    // barriers of the step loop.  The "tape" warp copies each step's tape
+    // rows and Z' from the pre-split shared B operands (hi + lo is exact) to
+    // global, so the row and B warps issue no global stores in the loop; the
+    // "publish" warp makes finished blocks visible to the gradient kernel
+    // (gpu-scope fence + counter), as many per fence as are ready, so a slow
+    // fence never holds up the tape warp (and through it the row warps).
+    // Two-tile geometries (longer steps; no registers to spare for a 14th
+    // warp) publish from the tape warp itself.
     const int PU0 = PW + 1;  // first push warp (NP > 0)
-    const int SW = SIG ? PW + 1 + NP : 1 << 30;
+    const int SW = SIG ? PW + 1 + NP : 1 << 30;  // tape warp
+    const int PBW = TPW == 1 ? SW + 1 : SW;       // publish warp
     const int nmain = (NR + MT + 1 + NP) * 32;
     const bool pusher = NP > 0 && warp >= PU0 && warp < PU0 + NP;
-    unsigned* prog = reinterpret_cast<unsigned*>(bars + NSTG + NSLOTV);
+    // tape warp hand-off: xrdy (NR arrivals: X^(t+1) formed in Xn), xfree
+    // (1 arrival: the tape warp has read step t's Xn / Zn)
+    const uint32_t xrdy_u32 = bar_u32 + 8u * (NSTG + NSLOTV), xfree_u32 = xrdy_u32 + 8u;
+    auto xbuf = [&](int k) { return Xn + (SIG ? (k & 1) * RT * 256 : 0); };
+    unsigned* prog = reinterpret_cast<unsigned*>(bars + NSTG + NSLOTV + 2);  // steps copied out
     long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
     // prologue / epilogue global-timer stamps in row q: 10 entry, 11 X loaded,
     // 12 cluster synced, 13 prologue partial pushed, 14 loop done, 15 exit
@@ -146,9 +159,13 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
         for (int s = 0; s < NSTG + NSLOTV; ++s) dev::mbar_init(&bars[s], 1);
+        if (SIG) {
+            dev::mbar_init(&bars[NSTG + NSLOTV], (uint32_t)NR);
+            dev::mbar_init(&bars[NSTG + NSLOTV + 1], 1u);
+            *prog = 0u;
+        }
         dev::fence_mbar_init();
         for (int s = 0; s < NSLOTV; ++s) mbar_expect_u32(exb_u32 + 8u * s, ex_bytes);
-        *prog = 0u;
     }
     __syncthreads();
     if (warp == PW && lane == 0) {
@@ -246,8 +263,9 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             const int rt = warp + u * NR;
             if (rt < RT) {
                 float xh[4], xl[4];
-                lds_vec<4>(xh, Xn + rt * 256 + lane * 4);
-                lds_vec<4>(xl, Xn + rt * 256 + 128 + lane * 4);
+                const float* Xc = xbuf(s > 0 ? s - 1 : 0) + rt * 256;  // X^(s-1)
+                lds_vec<4>(xh, Xc + lane * 4);
+                lds_vec<4>(xl, Xc + 128 + lane * 4);
                 float w0[2][2 * MT], w1[2][2 * MT];
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
@@ -292,39 +310,122 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     GSTAMP(13);
     __syncthreads();  // the combine scratch is reused by step 0's partial
 
-    // the rows and Z' of a step are stored: count the warp in (release at CTA
-    // scope covers the warp's stores, ordered by __syncwarp)
-    // counting starts at step t0 (a.sig_from): earlier steps are covered by
-    // the release of step t0 (program order)
     const int t0 = a.sig_from < q ? a.sig_from : q - 1;
-    auto step_stored = [&]() {
-        if (SIG) {
-            __syncwarp();
-            if (lane == 0) asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(dev::smem_u32(prog)) : "memory");
-        }
-    };
     if (SIG && warp == SW) {
-        // block_of(t) is final in this CTA once all NR + MT warps have counted
-        // step t; then one gpu-scope release publishes it to the gradient kernel
-        for (int t = t0; t < q; ++t) {
-            const unsigned target = (unsigned)((t - t0 + 1) * (NR + MT));
-            if (lane == 0) {
-                unsigned v;
-                while (true) {
-                    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(dev::smem_u32(prog)) : "memory");
-                    if (v >= target) break;
-                    __nanosleep(32);
+        // per step s: X^(s+1) (forward tape) or X^(s) (backward tape) and
+        // -2 Z_s, pre-split in B-fragment order: float4 j of lane l holds rows
+        // (l & 3) + 4 j, column l >> 2 of a 16 x 8 tile (scatter_cb's layout)
+        // (1-tile-per-row-warp geometries hold the whole step in registers and
+        // free the buffers before storing; 2-tile ones stream tile by tile)
+        constexpr int RTM = TPW == 1 ? MAXNR : 1;
+        const int zl = col0 + (lane >> 2);
+        const bool zst = D.zhat && rank == 0 && zl < a.m;
+        for (int s = 0; s < q; ++s) {
+            const int i = block_of(s);
+            mbar_wait_u32(xrdy_u32, (uint32_t)(s & 1));
+            const float* xs = xbuf(D.forward ? s + 1 : s);
+            float* tb = tape0 ? tape0 + (size_t)i * tape_step + (lane & 3) * WCV + (lane >> 2) : nullptr;
+            float* zb = zst ? D.zhat + ((size_t)i * BS + (lane & 3)) * a.m + zl : nullptr;
+            auto ld_tile = [&](const float* p, float (&v)[4], float sc) {
+                float h[4], l[4];
+                lds_vec<4>(h, p + lane * 4);
+                lds_vec<4>(l, p + 128 + lane * 4);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = sc * (h[j] + l[j]);
+            };
+            const float* zs = Zn + (s & 1) * (KB * 128);
+            auto ld_z = [&](int mt, float (&v)[4]) {
+                float h[4], l[4];
+                lds_vec<4>(h, zs + mt * 128 + lane * 4);
+                lds_vec<4>(l, zs + (KB / 2) * 128 + mt * 128 + lane * 4);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = -0.5f * (h[j] + l[j]);
+            };
+            // reads done: the row warps may overwrite this Xn after the next
+            // barrier 1, the B warps this Zn a step later
+            auto free_bufs = [&]() {
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(xfree_u32) : "memory");
+            };
+            if constexpr (TPW == 1) {
+                float tv[RTM][4], zv[MT][4];
+#pragma unroll
+                for (int rt = 0; rt < RTM; ++rt)
+                    if (rt < RT) ld_tile(xs + rt * 256, tv[rt], 1.f);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) ld_z(mt, zv[mt]);
+                free_bufs();
+                // step s-1's rows are out (stored a step ago: the release
+                // waits for nothing); step s is counted after the loop or
+                // with step s+1
+                if (s > 0 && lane == 0)
+                    asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(dev::smem_u32(prog)) : "memory");
+                if (tb) {
+#pragma unroll
+                    for (int rt = 0; rt < RTM; ++rt)
+                        if (rt < RT)
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) tb[(rt * 16 + 4 * j) * WCV] = tv[rt][j];
                 }
-                __threadfence();
-                // steps before t0 finish no block of the fused launch early:
-                // they are published together with step t0
-                for (int u = t == t0 ? 0 : t; u <= t; ++u) atomicAdd(a.done + block_of(u), 1u);
+                if (zb) {
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) zb[(size_t)(mt * 16 + 4 * j) * a.m] = zv[mt][j];
+                }
+            } else {
+                for (int rt = 0; rt < RT; ++rt) {
+                    float v[4];
+                    ld_tile(xs + rt * 256, v, 1.f);
+                    if (tb)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) tb[(rt * 16 + 4 * j) * WCV] = v[j];
+                }
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    float v[4];
+                    ld_z(mt, v);
+                    if (zb)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) zb[(size_t)(mt * 16 + 4 * j) * a.m] = v[j];
+                }
+                free_bufs();
             }
-            __syncwarp();
+            if constexpr (TPW == 2) {
+                __syncwarp();
+                if (lane == 0 && s >= t0) {
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                    for (int u = s == t0 ? 0 : s; u <= s; ++u) atomicAdd(a.done + block_of(u), 1u);
+                }
+            }
+        }
+        // the last step's block (the one the gradient kernel's tail waits on)
+        // goes out from here, without the hand-off; with it every block when
+        // t0 is the last step (the publish warp then has nothing to do)
+        __syncwarp();
+        if (TPW == 1 && lane == 0 && q > 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (int u = t0 >= q - 1 ? 0 : q - 1; u < q; ++u) atomicAdd(a.done + block_of(u), 1u);
         }
     }
+    if (SIG && TPW == 1 && warp == PBW) {
+        // blocks of steps 0 .. q-2; steps before t0 finish no block of the
+        // fused launch early: they are published together with step t0
+        for (int pub = 0; pub < q - 1 && t0 < q - 1 && lane == 0;) {
+            const unsigned need = (unsigned)(pub > t0 ? pub + 1 : t0 + 1);
+            unsigned v;
+            while (true) {
+                asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(dev::smem_u32(prog)) : "memory");
+                if (v >= need) break;
+                __nanosleep(a.pub_ns);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            for (; pub < (int)v; ++pub) atomicAdd(a.done + block_of(pub), 1u);
+        }
+        __syncwarp();
+    }
     int st = 0, ph = 0;  // stage ring position of step t
-    for (int t = 0; t < q && warp != SW; ++t) {
+    for (int t = 0; t < q && warp < SW; ++t) {
         const int i = block_of(t);
         if (trc && tid == 0) trc[(size_t)t * 16 + 0] = clock64(), trc[(size_t)t * 16 + 8] = (long long)dev::globaltimer();
         // ---------------- phase 1 ----------------
@@ -352,8 +453,6 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             if (trc && tid == 0) trc[(size_t)t * 16 + 2] = clock64();
         } else if (warp < NR + MT) {
             const int mt = warp - NR;
-            // Z' of step t-1 is stored (a step ago: the release drains nothing new)
-            if (t > t0) step_stored();
             float cm[4] = {0.f, 0.f, 0.f, 0.f}, c1[4] = {0.f, 0.f, 0.f, 0.f}, c2[4] = {0.f, 0.f, 0.f, 0.f};
             mbar_wait_u32(bar_u32 + 8u * st, (uint32_t)ph);
             if (t > 0) {  // -2 S_t Z_{t-1}: Zn holds -2 Z_{t-1}, pre-split
@@ -397,7 +496,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             for (int e = 0; e < 4; ++e) z[e] += zs[e];
             float* zc = Zn + (t & 1) * (KB * 128) + mt * 128;
             scatter_cb(zc, zc + (KB / 2) * 128, z, g, tq, -2.f);
-            if (D.zhat && rank == 0) {
+            if (!SIG && D.zhat && rank == 0) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int j = mt * 16 + g + 8 * (e >> 1), l = col0 + 2 * tq + (e & 1);
@@ -418,6 +517,8 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         } else if (pusher) {
             if (t + 1 < q) push_step(t + 1);
         }
+        // the tape warp has read step t-1's Xn / Zn before either is reused
+        if (SIG && warp < NR && t > 0) mbar_wait_u32(xfree_u32, (uint32_t)((t - 1) & 1));
         WSTAMP(0);
         if constexpr (NP > 0) {  // barrier 1 without the push warps: Z_t -> the update
             if (!pusher) asm volatile("bar.sync 2, %0;" ::"r"((NR + MT + 1) * 32) : "memory");
@@ -430,7 +531,6 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         if (trc && tid == 0) trc[(size_t)t * 16 + 5] = clock64();
         // ---------------- phase 2: X^(t+1) = X^(t) + V_t (-2 Z_t) ----------------
         if (warp < NR) {
-            if (t > t0) step_stored();  // tape rows of step t-1, stored a step ago
             const float* zc = Zn + (t & 1) * (KB * 128);
             float zh[KB / 2][4], zl[KB / 2][4];
 #pragma unroll
@@ -438,7 +538,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
                 lds_vec<4>(zh[h2], zc + h2 * 128 + lane * 4);
                 lds_vec<4>(zl[h2], zc + (KB / 2) * 128 + h2 * 128 + lane * 4);
             }
-            float* tblk = tape0 ? tape0 + (size_t)i * tape_step : nullptr;
+            float* tblk = tape0 && !SIG ? tape0 + (size_t)i * tape_step : nullptr;
 #pragma unroll
             for (int u = 0; u < TPW; ++u) {
                 const int rt = warp + u * NR;
@@ -459,10 +559,11 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
                         *reinterpret_cast<float2*>(tp) = make_float2(x[u][0], x[u][1]);
                         *reinterpret_cast<float2*>(tp + 8 * WCV) = make_float2(x[u][2], x[u][3]);
                     }
-                    if (t + 2 < q) scatter_cb(Xn + rt * 256, Xn + rt * 256 + 128, x[u], g, tq, 1.f);
+                    if (SIG || t + 2 < q) scatter_cb(xbuf(t + 1) + rt * 256, xbuf(t + 1) + rt * 256 + 128, x[u], g, tq, 1.f);
                 }
             }
             __syncwarp();
+            if (SIG && lane == 0) asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(xrdy_u32) : "memory");
             if (trc && tid == 0) trc[(size_t)t * 16 + 6] = clock64();
         }
         WSTAMP(2);
@@ -484,12 +585,11 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         if (++st == NSTG) st = 0, ph ^= 1;
     }
 
-    if (warp < NR + MT && q > 0) step_stored();  // the last step's rows and Z'
     // x_out: the row warps stage their tiles column-major in the (consumed)
     // stage ring, then store 16 bytes at a time (whole lines: x_out may be a
-    // caller's pinned host buffer).  With the signal warp, after its last
-    // release, so that fence does not wait for these stores.
-    if (SIG && warp == SW) asm volatile("bar.arrive 5, %0;" ::"r"((NR + 1) * 32) : "memory");
+    // caller's pinned host buffer).  With the publish warp, after its last
+    // fence, so that fence does not wait for these stores.
+    if (SIG && warp == PBW) asm volatile("bar.arrive 5, %0;" ::"r"((NR + 1) * 32) : "memory");
     if (warp < NR) {
         float* xs = stg;  // [WCV][RC + 4]
         const int LX = RC + 4;
@@ -531,14 +631,14 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
 
 template <int BS, int TPW, int NP>
 cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
-    const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg);
+    const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg, a.done != nullptr);
     auto kern = a.done ? sweep2_kernel<BS, TPW, true, NP> : sweep2_kernel<BS, TPW, false, NP>;
     if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total, true); e != cudaSuccess) return e;
     const int RT = a.d_pad / a.C / 16;
     const int NR = RT < MAXNR ? RT : MAXNR;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(a.C * a.ngroups * a.ndir, 1, 1);
-    cfg.blockDim = dim3((NR + BS / 16 + 1 + NP + (a.done ? 1 : 0)) * 32, 1, 1);
+    cfg.blockDim = dim3((NR + BS / 16 + 1 + NP + (a.done ? (TPW == 1 ? 2 : 1) : 0)) * 32, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
@@ -570,7 +670,9 @@ cudaError_t launch_bs(const SweepV2Args& a, cudaStream_t s) {
 
 }  // namespace
 
-size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg) { return v2_layout(C, BS, d_pad, nstg).total; }
+size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg, bool sig) {
+    return v2_layout(C, BS, d_pad, nstg, sig).total;
+}
 
 int sweep2_nstg(int C, int BS, int d_pad) {
     if (C < 1 || C > 16 || d_pad % C) return 0;
@@ -579,7 +681,7 @@ int sweep2_nstg(int C, int BS, int d_pad) {
     if (BS != 16 && BS != 32 && BS != 64) return 0;
     int best = 0;
     for (int n = 2; n <= 4; ++n)
-        if (sweep2_smem_bytes(C, BS, d_pad, n) <= 227 * 1024) best = n;
+        if (sweep2_smem_bytes(C, BS, d_pad, n, false) <= 227 * 1024) best = n;
     return best;
 }
 

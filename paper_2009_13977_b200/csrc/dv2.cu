@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
             while (true) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.done + i) : "memory");
                 if (v >= a.done_target) break;
-                __nanosleep(128);
+                __nanosleep(a.poll_ns);
             }
             // the last CTA of block i to get here resets the block's counters
             if (atomicAdd(a.dvcnt + i, 1u) == gridDim.x - 1) {

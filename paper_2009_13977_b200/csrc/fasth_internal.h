@@ -118,6 +118,7 @@ struct SweepV2Args {
     const unsigned* ready;
     unsigned* done;
     int sig_from;         // done counting starts at this step (earlier steps published with it)
+    int pub_ns;           // publish warp's back-off between polls of the tape warp's count
     int pdl;              // launched as a programmatic dependent of the builder
 };
 
@@ -141,6 +142,7 @@ struct DvArgs {
     size_t min_smem;  // pipelined: dynamic shared memory to request at least
     long long* trace;  // optional per-CTA global-timer stamps [block][slab][6] (FASTH_STEPTRACE)
     int order;  // blockIdx.y -> block: 0 identity (backward sweep order), 1 middle-out (fused fwd+bwd)
+    int poll_ns;  // pipelined: back-off between polls of the block's counter
     int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
 };
 
@@ -157,7 +159,7 @@ struct SweepGeom {
 };
 SweepGeom pick_geometry(int d, int m, int BS, int num_sms);
 int sweep2_nstg(int C, int BS, int d_pad);  // 0 = geometry not supported by the v2 kernel
-size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg);
+size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg, bool sig);  // sig: tape-warp variant
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
 // host_io.cu: streaming copy kernel (either side may be a pinned-host mapping)
 cudaError_t launch_stream_copy(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s);

@@ -1,5 +1,7 @@
 """Run the metric-config fused step a few times as a CUDA graph (L2 flushed)
-with FASTH_STEPTRACE set, then dump the last replay's timeline."""
+with FASTH_STEPTRACE set, then dump the last replay's timeline.
+STEP_TWO_CALL=1: the fasth_forward + fasth_backward step instead (the trace
+then shows the backward sweep and the gradient kernel)."""
 import os
 import subprocess
 import sys
@@ -19,13 +21,23 @@ flush = torch.empty(64 * 1024 * 1024, device="cuda")
 ctx = fb.Context(0, deferred=True)
 outs = (torch.empty(m, d, device="cuda").t(), torch.empty(m, d, device="cuda").t(), torch.empty(d, d, device="cuda"))
 s = torch.cuda.Stream()
+two_call = os.environ.get("STEP_TWO_CALL", "0") == "1"
+
+
+def step():
+    if two_call:
+        t = fb.fasth_forward(V, X, b, ctx=ctx, out=outs[0])
+        return fb.fasth_backward(t, G)
+    return fb.fasth_forward_backward(V, X, G, b, ctx=ctx, out=outs)
+
+
 with torch.cuda.stream(s):
     for _ in range(3):
-        fb.fasth_forward_backward(V, X, G, b, ctx=ctx, out=outs)
+        step()
 torch.cuda.synchronize()
 gr = torch.cuda.CUDAGraph()
 with torch.cuda.graph(gr, stream=s):
-    fb.fasth_forward_backward(V, X, G, b, ctx=ctx, out=outs)
+    step()
 with torch.cuda.stream(s):
     for _ in range(5):
         flush.zero_()
