@@ -91,6 +91,7 @@ struct fasth_ctx_s {
     // the host-buffer step writes dV straight into the caller's pinned memory:
     // there the gradient kernel runs behind the sweep (PCIe writes overlap it)
     bool dv_pipe_pref = false;
+    bool dv_v_pre = false;  // the last sweep launched released its dependents after the builder
     long long* step_trace = nullptr;
     int cur_m = 0;  // batch of the plan being built (step-trace sizing)
     size_t st_build = 0, st_sweep = 0, st_dv = 0, st_total = 0;
@@ -543,6 +544,10 @@ bool use_panel(const SweepV2Args& a) {
 
 fasth_status launch_traced_sweep2(fasth_ctx c, SweepV2Args& a, const char* what) {
     const char* prefix = getenv("FASTH_TRACE");
+    // a gradient kernel launched behind this sweep may read the WY blocks
+    // before its own wait once the sweep releases it only after the builder
+    a.late_trigger = a.pdl && !a.ready && !getenv("FASTH_EARLY_TRIGGER");
+    c->dv_v_pre = !a.ready && (a.late_trigger || !a.pdl) && !use_panel(a);
     if (use_panel(a)) {
         a.trace = nullptr;
         return c->timed([&] { return launch_panel(a, c->stream); }, "panel(fwd/bwd)");
@@ -739,6 +744,7 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
         if (const char* e = getenv("FASTH_DV_POLL")) v.poll_ns = atoi(e);
     }
     v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
+    v.v_pre = c->dv_v_pre || !v.pdl;
     c->after_stream_wait = false;
     if (getenv("FASTH_STEPTRACE") && c->step_trace && c->st_hdr[3] > 0) {
         v.trace = c->step_trace + c->st_dv;

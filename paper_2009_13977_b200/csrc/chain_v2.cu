@@ -155,8 +155,10 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     auto block_of = [&](int t) { return D.forward ? q - 1 - t : t; };
     auto gstage = [&](int t) { return D.stage + ((size_t)t * C + rank) * SF; };
 
-    // the gradient kernel may launch now; it waits on the per-block counters
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // the gradient kernel may launch now (it waits on the sweep or on the
+    // per-block counters); with late_trigger once the builder is complete, so
+    // that it may read the builder's outputs before its wait
+    if (!a.late_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (tid == 0) {
         for (int s = 0; s < NSTG + NSLOTV; ++s) dev::mbar_init(&bars[s], 1);
         if (SIG) {
@@ -172,7 +174,10 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         const uint32_t stg_u32 = dev::smem_u32(stg);
         // launched as a programmatic dependent of the builder: everything up
         // to here overlapped its tail; its stages are read only from now on
-        if (!a.ready && a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (!a.ready && a.pdl) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (a.late_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        }
         for (int t = 0; t < NSTG && t < q; ++t) {
             if (a.ready) wait_counter(a.ready + block_of(t), (unsigned)C);
             mbar_expect_u32(bar_u32 + 8u * t, stage_bytes);

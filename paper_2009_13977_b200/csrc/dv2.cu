@@ -67,9 +67,10 @@ __device__ __forceinline__ void mma3(float (&m)[4], float (&c)[4], const AF& a, 
 template <int BS>
 __host__ __device__ constexpr size_t dv2_smem() {
     // Zb | Zf chunk (BS x (MCH+4) each; later the dV staging tile,
-    // BS x (DV_ROWS+4) <= that), Q (BS x (BS+1))
+    // BS x (DV_ROWS+4) <= that), Q (BS x (BS+1)), the slab's V rows
+    // (DV_ROWS x (BS+4), the builder's layout)
     static_assert(BS * (DV_ROWS + 4) <= 2 * BS * (MCH + 4), "dV staging fits the Z' chunks");
-    return 4 * ((size_t)2 * BS * (MCH + 4) + (size_t)BS * (BS + 1));
+    return 4 * ((size_t)2 * BS * (MCH + 4) + (size_t)BS * (BS + 1) + (size_t)DV_ROWS * (BS + 4));
 }
 
 // Phases per CTA (one per 64-row slab of block i): every global load of a
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     float* Zb = dsm;
     float* Zf = dsm + BS * LDZ;
     float* Qs = dsm + 2 * BS * LDZ;
+    float* Vs = Qs + BS * (BS + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
     // blocks in the order the sweeps finish them (pipelined step: the CTAs
@@ -110,6 +112,17 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         trc[0] = (long long)dev::globaltimer(), trc[5] = smid;
     }
+    // the slab's V rows of the block (K = BS; the builder's output, rows
+    // < d_pad) into shared memory: before the wait on the sweep when the
+    // builder is known complete (a.v_pre), else with the first Z' chunk
+    auto stage_v = [&]() {
+        const int rb = blockIdx.x * DV_ROWS, nr = min(DV_ROWS, a.d_pad - rb);
+        const float* src = a.Vbl + ((size_t)i * a.d_pad + rb) * LDV;
+        for (int idx = tid; idx < nr * LDV / 4; idx += DV_WARPS * 32)
+            dev::cp_async16(Vs + 4 * idx, src + 4 * idx, true);
+        dev::cp_async_commit();
+    };
+    if (a.v_pre) stage_v();
     if (!a.done && a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // sweep complete
     if (a.done) {  // pipelined step: both sweeps have passed block i
         if (tid == 0) {
@@ -164,6 +177,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
             }
         }
         if (l0 > 0) __syncthreads();  // previous chunk's Zb / Zf readers are done
+        if (l0 == 0 && !a.v_pre) stage_v();
         if (vec && mc == MCH) {
             for (int idx = tid; idx < BS * MCH / 4; idx += DV_WARPS * 32) {
                 const int j = idx / (MCH / 4), l4 = (idx - j * (MCH / 4)) * 4;
@@ -219,10 +233,14 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
             }
         }
     }
-    // V fragments of the block (rows r0.., K = BS): issued before the Q hand-off
-    float fv[KB][4];
+    if (m <= 0) {  // no chunk loop ran
+        if (!a.v_pre) stage_v();
+        dev::cp_async_wait_all();
+        __syncthreads();
+    }
+    float fv[KB][4];  // V fragments (the staged rows are visible: the chunk loop synced)
     {
-        const float* vb = a.Vbl + ((size_t)i * a.d_pad + (rows_ok ? r0 : 0) + g) * LDV + tq;
+        const float* vb = Vs + (warp * 16 + g) * LDV + tq;
 #pragma unroll
         for (int ks = 0; ks < KB; ++ks) {
             fv[ks][0] = vb[ks * 8];

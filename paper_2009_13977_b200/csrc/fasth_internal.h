@@ -119,6 +119,8 @@ struct SweepV2Args {
     unsigned* done;
     int sig_from;         // done counting starts at this step (earlier steps published with it)
     int pub_ns;           // publish warp's back-off between polls of the tape warp's count
+    int late_trigger;     // release programmatic dependents only once the previous grid
+                          // (the builder) is complete, not at entry
     int pdl;              // launched as a programmatic dependent of the builder
 };
 
@@ -144,6 +146,8 @@ struct DvArgs {
     int order;  // blockIdx.y -> block: 0 identity (backward sweep order), 1 middle-out (fused fwd+bwd)
     int poll_ns;  // pipelined: back-off between polls of the block's counter
     int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
+    int v_pre;  // Vbl is complete at launch (the sweep released its dependents after the
+                // builder): V fragments load before the wait on the sweep
 };
 
 // wy_build2.cu (packed stages for chain_v2.cu)

@@ -203,6 +203,53 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     const int per = L.per;
     const int mylo = min(E, rank * per), myhi = min(E, mylo + per), mylen = myhi - mylo;
     const uint32_t barA = dev::smem_u32(&bars[0]), barB = dev::smem_u32(&bars[1]);
+    // 1. rows of blocks i (slot 0), i-1 (1), i+1 (2), permuted positions:
+    //    thread k takes 4-row group k % RG of column k / RG (consecutive
+    //    threads walk down a column: whole lines), eight 16-byte loads in
+    //    flight per thread (one round trip at b = 32, 80-row slabs).  The
+    //    phase is issue-bound at two CTAs per SM: (column, group) advance
+    //    incrementally, no division per element
+    {
+        constexpr int NB = 8;
+        const int RG = RB / 4, NTOT = 3 * BS * RG;
+        const int dq = NTH4 / RG, dr = NTH4 - dq * RG;
+        float* sf = reinterpret_cast<float*>(smem);
+        int jj = tid / RG, rg = tid - jj * RG;
+        for (int kb = tid; kb < NTOT; kb += NB * NTH4) {
+            float4 v[NB];
+            int dofs[NB];
+#pragma unroll
+            for (int u = 0; u < NB; ++u) {
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                const int r = 4 * rg;
+                const int sl = jj / BS, j = jj - sl * BS;
+                const int blk = sl == 0 ? i : sl == 1 ? i - 1 : i + 1;
+                const int k0 = blk * p.b;
+                const bool in = jj < 3 * BS;
+                const int wb = (in && blk >= 0 && blk < p.q) ? min(p.b, p.n - k0) : 0;
+                dofs[u] = in ? (jj < BS ? L.vc / 4 + jj * P : L.vpn / 4 + (jj - BS) * P) + b4_pos(r) : -1;
+                if (j < wb && r < nrows) {
+                    const float* src = V + (int64_t)(p.reversed ? p.n - 1 - (k0 + j) : k0 + j) * ldv + row0 + r;
+                    if (vec_ok && r + 4 <= nrows) {
+                        v[u] = __ldg(reinterpret_cast<const float4*>(src));
+                    } else {
+                        v[u].x = src[0];
+                        if (r + 1 < nrows) v[u].y = src[1];
+                        if (r + 2 < nrows) v[u].z = src[2];
+                        if (r + 3 < nrows) v[u].w = src[3];
+                    }
+                }
+                jj += dq, rg += dr;
+                if (rg >= RG) rg -= RG, ++jj;
+            }
+#pragma unroll
+            for (int u = 0; u < NB; ++u)
+                if (dofs[u] >= 0) {  // rows r + e -> position + 4 e
+                    float* dst = sf + dofs[u];
+                    dst[0] = v[u].x, dst[4] = v[u].y, dst[8] = v[u].z, dst[12] = v[u].w;
+                }
+        }
+    }
     if (tid == 0) {
         dev::mbar_init(&bars[0], 1);
         dev::mbar_init(&bars[1], 1);
@@ -215,47 +262,6 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     // just before the first push (the loads and the Gram run in between)
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
-    // 1. rows of blocks i (slot 0), i-1 (1), i+1 (2), permuted positions:
-    //    warp w takes columns w, w + 8, ... (six 16-byte loads in flight per
-    //    lane), lane l the 4-row groups 4 l, 4 l + 128, ...
-    {
-        constexpr int NB = 6;
-        float* sf = reinterpret_cast<float*>(smem);
-        for (int jb = warp; jb < 3 * BS; jb += NB * (NTH4 / 32)) {
-            for (int r = 4 * lane; r < RB; r += 128) {
-                float4 v[NB];
-#pragma unroll
-                for (int u = 0; u < NB; ++u) {
-                    const int jj = jb + u * (NTH4 / 32);
-                    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    const int sl = jj / BS, j = jj - sl * BS;
-                    const int blk = sl == 0 ? i : sl == 1 ? i - 1 : i + 1;
-                    const int k0 = blk * p.b;
-                    const int wb = (jj < 3 * BS && blk >= 0 && blk < p.q) ? min(p.b, p.n - k0) : 0;
-                    if (j < wb && r < nrows) {
-                        const float* src = V + (int64_t)(p.reversed ? p.n - 1 - (k0 + j) : k0 + j) * ldv + row0 + r;
-                        if (vec_ok && r + 4 <= nrows) {
-                            v[u] = __ldg(reinterpret_cast<const float4*>(src));
-                        } else {
-                            v[u].x = src[0];
-                            if (r + 1 < nrows) v[u].y = src[1];
-                            if (r + 2 < nrows) v[u].z = src[2];
-                            if (r + 3 < nrows) v[u].w = src[3];
-                        }
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < NB; ++u) {
-                    const int jj = jb + u * (NTH4 / 32);
-                    if (jj < 3 * BS) {  // rows r + e -> position + 4 e
-                        float* dst = sf + (jj < BS ? L.vc / 4 + jj * P : L.vpn / 4 + (jj - BS) * P) + b4_pos(r);
-                        dst[0] = v[u].x, dst[4] = v[u].y, dst[8] = v[u].z, dst[12] = v[u].w;
-                    }
-                }
-            }
-        }
-    }
-    __syncthreads();
     BTRACE(1);
 
     // 2. partial band: warp w -> m-tile (w & 1) of V_i^T, n-tile (w >> 1) of
