@@ -51,6 +51,8 @@ fasth_status fail(fasth_status s, const char* fmt, ...) {
     } while (0)
 
 constexpr int kMaxPipeQ = 4096;  // WY blocks the pipelined step supports
+constexpr int kCounterWords = 4 * kMaxPipeQ + 64;
+constexpr int kUploadChunks = 4;  // chunks per upload unit (streamed host step)
 
 size_t size_class(size_t bytes) {
     size_t c = 512;
@@ -92,6 +94,25 @@ struct fasth_ctx_s {
     // there the gradient kernel runs behind the sweep (PCIe writes overlap it)
     bool dv_pipe_pref = false;
     bool dv_v_pre = false;  // the last sweep launched released its dependents after the builder
+    // streamed host step: the upload the next build_plan launches (before its
+    // builder), whether the tape geometry allows it to stream, and whether the
+    // step in flight streams (consumed by the sweep and the gradient kernel)
+    struct UploadReq {
+        const float *v_src, *x_src, *g_src;
+        float *v, *x, *g;
+        int64_t nv, nx;
+    } up{};
+    bool up_pending = false, up_geom_ok = false, up_active = false;
+    // streamed: the builder is launched after the sweep (the sweep's 80 CTAs
+    // take their SMs first and wait per block; builders waiting for V's
+    // columns would otherwise hold the SMs the sweep needs)
+    bool build_deferred = false;
+    Plan deferred_plan{};
+    const float* deferred_V = nullptr;
+    int64_t deferred_ldv = 0;
+    unsigned* up_counts() { return counters + 3 * kMaxPipeQ; }      // [q] per block
+    unsigned* up_xg() { return counters + 4 * kMaxPipeQ; }          // X and G
+    unsigned* up_xg_seen() { return counters + 4 * kMaxPipeQ + 1; }  // sweep CTAs past it
     long long* step_trace = nullptr;
     int cur_m = 0;  // batch of the plan being built (step-trace sizing)
     size_t st_build = 0, st_sweep = 0, st_dv = 0, st_total = 0;
@@ -448,6 +469,7 @@ int internal_b(int d, int n, int b_user) {
 // padding d_pad the chain geometry asks for.
 fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_pad, int cb, int n,
                         int b_user, int reversed, int tag, bool* pipelined, Plan* out) {
+    const bool dv_wanted = pipelined && *pipelined;
     Plan p;
     p.d = d;
     p.n = n;
@@ -499,11 +521,65 @@ fasth_status build_plan(fasth_ctx c, const float* V, int64_t ldv, int d, int d_p
         }
         // build4 unless the persistent (pipelined) builder is asked for, it
         // does not fit shared memory, or FASTH_BUILD2=1 (A/B knob)
-        const bool v4 = !p.ready && p.nbuild == 0 && build4_smem_bytes(p.BS, p.d_pad / p.CB, p.CB) <= 227 * 1024 &&
-                        !(getenv("FASTH_BUILD2") && atoi(getenv("FASTH_BUILD2")) != 0);
-        fasth_status bs = c->timed([&] {
-            return v4 ? launch_build4(p, V, ldv, c->err_d, c->stream) : launch_build2(p, V, ldv, c->err_d, c->stream);
-        }, "wy_build");
+        const bool b4fits = build4_smem_bytes(p.BS, p.d_pad / p.CB, p.CB) <= 227 * 1024 &&
+                            !(getenv("FASTH_BUILD2") && atoi(getenv("FASTH_BUILD2")) != 0);
+        // the host step's upload goes first: streamed (the builder, the sweep
+        // and the gradient kernel start per block as V's columns land) where
+        // the whole pipelined chain applies, else one plain SM copy
+        if (c->up_pending) {
+            c->up_pending = false;
+            const auto& u = c->up;
+            const char* se = getenv("FASTH_UPLOAD_STREAM");
+            const bool stream = (!se || atoi(se) != 0) && c->up_geom_ok && dv_wanted && b4fits && !p.ready &&
+                                p.nbuild == 0 && !reversed && p.q <= kMaxPipeQ && u.nv == (int64_t)d * n &&
+                                ((int64_t)p.b * d) % 4 == 0 && u.nx % 4 == 0 &&
+                                !((reinterpret_cast<uintptr_t>(u.v_src) | reinterpret_cast<uintptr_t>(u.x_src) |
+                                   reinterpret_cast<uintptr_t>(u.g_src) | reinterpret_cast<uintptr_t>(u.v) |
+                                   reinterpret_cast<uintptr_t>(u.x) | reinterpret_cast<uintptr_t>(u.g)) & 15) &&
+                                ldv == d;
+            if (stream) {
+                UploadArgs ua{};
+                ua.x_src = reinterpret_cast<const float4*>(u.x_src);
+                ua.g_src = reinterpret_cast<const float4*>(u.g_src);
+                ua.v_src = reinterpret_cast<const float4*>(u.v_src);
+                ua.x_dst = reinterpret_cast<float4*>(u.x);
+                ua.g_dst = reinterpret_cast<float4*>(u.g);
+                ua.v_dst = reinterpret_cast<float4*>(u.v);
+                ua.x4 = u.nx / 4, ua.v4 = u.nv / 4, ua.blk4 = (int64_t)p.b * d / 4;
+                ua.q = p.q, ua.ncb = kUploadChunks;
+                ua.upc = c->up_counts(), ua.xg_cnt = c->up_xg();
+                const char* ce = getenv("FASTH_UPLOAD_CTAS");
+                const int ctas = ce ? std::max(1, atoi(ce)) : 16;
+                TRY(c->timed([&] { return launch_upload(ua, ctas, c->stream); }, "h2d_copy"));
+                p.upc = c->up_counts();
+                p.upc_target = kUploadChunks;
+                p.ready = c->counters;
+                // a few persistent builder clusters (blocks in upload order):
+                // the sweep's clusters find their SMs free and start as soon
+                // as the first blocks are built
+                const char* nb = getenv("FASTH_BUILDERS");
+                p.nbuild = nb ? std::max(1, atoi(nb)) : 10;
+                *pipelined = true;
+                c->up_active = true;
+            } else {
+                const float* srcs[3] = {u.v_src, u.x_src, u.g_src};
+                float* dsts[3] = {u.v, u.x, u.g};
+                const int64_t ns[3] = {u.nv, u.nx, u.nx};
+                TRY(c->timed([&] { return launch_stream_copy_n(srcs, dsts, ns, 3, c->num_sms, c->stream); }, "h2d_copy"));
+            }
+        }
+        const bool v4 = c->up_active ? b4fits : !p.ready && p.nbuild == 0 && b4fits;
+        fasth_status bs = FASTH_OK;
+        if (c->up_active && getenv("FASTH_BUILD_AFTER_SWEEP")) {  // launched by run_forward_backward
+            c->build_deferred = true;
+            c->deferred_plan = p;
+            c->deferred_V = V;
+            c->deferred_ldv = ldv;
+        } else {
+            bs = c->timed([&] {
+                return v4 ? launch_build4(p, V, ldv, c->err_d, c->stream) : launch_build2(p, V, ldv, c->err_d, c->stream);
+            }, "wy_build");
+        }
         if (prefix) {
             c->build_trace = p.trace;
             c->build_trace_n = ntr;
@@ -734,6 +810,7 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
         v.ready = c->counters;
         v.done = c->counters + kMaxPipeQ;
         v.dvcnt = c->counters + 2 * kMaxPipeQ;
+        if (c->up_active) v.upc = c->up_counts();  // streamed host step
         v.done_target = (unsigned)(ndir * t->ngroups * t->C);
         v.order = order;
         // keep the gradient CTAs off the sweep's SMs (FASTH_DV_SMEM overrides)
@@ -743,6 +820,7 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
         v.poll_ns = 128;
         if (const char* e = getenv("FASTH_DV_POLL")) v.poll_ns = atoi(e);
     }
+    c->up_active = false;
     v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
     v.v_pre = c->dv_v_pre || !v.pdl;
     c->after_stream_wait = false;
@@ -800,16 +878,28 @@ fasth_status run_forward_backward(fasth_ctx c, fasth_tape t, const float* X, int
         a.ready = c->counters;
         a.done = c->counters + kMaxPipeQ;
     }
+    if (pipe && c->up_active) {  // streamed host step: X / G are still landing
+        a.xg_ready = c->up_xg();
+        a.xg_target = 2 * kUploadChunks;
+        a.xg_seen = c->up_xg_seen();
+    }
     const bool dvpipe = want_dv && !pipe && dv_pipe_ok(c, a);
     if (dvpipe) {
         a.done = c->counters + kMaxPipeQ;
         a.sig_from = (p.q - 1) / 2;  // no block is final in both chains before this step
     }
     fasth_status s = launch_traced_sweep2(c, a, "sweep(fwd+bwd)");
+    if (s == FASTH_OK && c->build_deferred) {  // streamed host step: builder behind the sweep
+        c->build_deferred = false;
+        s = c->timed([&] {
+            return launch_build4(c->deferred_plan, c->deferred_V, c->deferred_ldv, c->err_d, c->stream);
+        }, "wy_build");
+    }
+    c->build_deferred = false;
     if (dx != dX) c->release(dx);
     TRY(s);
     if (!want_dv) return FASTH_OK;
-    return run_dv(c, t, dV, lddv, pipe || dvpipe, 2, dvpipe ? 1 : 0);
+    return run_dv(c, t, dV, lddv, pipe || dvpipe, 2, (pipe || dvpipe) ? 1 : 0);
 }
 
 fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, int m, int b,
@@ -831,6 +921,9 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
         return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for the chain kernels at block width %d", d, BS);
     }
     t->pipelined = pipelined;
+    // the streamed host step needs the pipelined gradient (signal-warp sweep)
+    c->up_geom_ok = BS <= 32 && m >= 1 && m <= 64 && !getenv("FASTH_PANEL") && c->counters_len >= 3 * kMaxPipeQ &&
+                    sweep2_smem_bytes(G.C, BS, G.d_pad, t->v2nstg, true) <= 227 * 1024;
     fasth_status s = build_plan(c, V, ldv, d, G.d_pad, G.C, n, b, reversed, tag, &t->pipelined, &t->plan);
     if (s != FASTH_OK) {
         delete t;
@@ -919,9 +1012,10 @@ fasth_status fasth_ctx_create(int device, void* stream, fasth_ctx* out) {
     c->err_h->chain = 0;
     cudaHostGetDevicePointer(&c->err_d, c->err_h, 0);
     cudaMalloc(&c->logdet_d, sizeof(double));
-    // pipelined-step counters (ready | done | dvcnt per block), zero, self-resetting
-    if (cudaMalloc(&c->counters, 3 * kMaxPipeQ * sizeof(unsigned)) == cudaSuccess &&
-        cudaMemset(c->counters, 0, 3 * kMaxPipeQ * sizeof(unsigned)) == cudaSuccess)
+    // pipelined-step counters (ready | done | dvcnt | uploaded per block, then
+    // X/G uploaded and its reader count), zero, self-resetting
+    if (cudaMalloc(&c->counters, kCounterWords * sizeof(unsigned)) == cudaSuccess &&
+        cudaMemset(c->counters, 0, kCounterWords * sizeof(unsigned)) == cudaSuccess)
         c->counters_len = 3 * kMaxPipeQ;
     *out = c;
     return FASTH_OK;
@@ -1455,13 +1549,16 @@ fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, 
             // (more PCIe reads in flight than the copy engine keeps:
             // host_io.cu), so the sweep reads X and G from device memory;
             // FASTH_H2D=dma for cudaMemcpyAsync
+            // The copy is launched by build_plan, right before the builder:
+            // streamed when the pipelined chain applies (host_io.cu
+            // upload_kernel: blocks in the order the chains need them,
+            // counted per block), else as one plain copy kernel
             const float* vm = mapped(V);
             const char* h2d = getenv("FASTH_H2D");
+            c->up_active = c->up_pending = c->build_deferred = false;
             if (nv && vm && !(h2d && !strcmp(h2d, "dma"))) {
-                const float* srcs[3] = {vm, xm, gm};
-                float* dsts[3] = {v, x, g};
-                const int64_t ns[3] = {(int64_t)nv, (int64_t)nx, (int64_t)nx};
-                TRY(c->timed([&] { return launch_stream_copy_n(srcs, dsts, ns, 3, c->num_sms, c->stream); }, "h2d_copy"));
+                c->up = {vm, xm, gm, v, x, g, (int64_t)nv, (int64_t)nx};
+                c->up_pending = true;
             } else {
                 if (nv) CU(cudaMemcpyAsync(v, V, nv * 4, cudaMemcpyHostToDevice, c->stream));
                 CU(cudaMemcpyAsync(x, X, nx * 4, cudaMemcpyHostToDevice, c->stream));
@@ -1481,7 +1578,10 @@ fasth_status enqueue_host_step(fasth_ctx c, float* const* bufs, const float* V, 
             const fasth_status fs = fasth_forward_backward(c, v, d, d, n, x, d, g, d, m, block_width, y, d, dx, d,
                                                            n ? (direct ? dvm : dv) : nullptr, d);
             c->dv_pipe_pref = false;
+            const bool lost = c->up_pending || c->build_deferred;  // every chain path builds and sweeps
+            c->up_active = c->up_pending = c->build_deferred = false;
             TRY(fs);
+            if (lost) return fail(FASTH_ERR_INVALID, "host step: the input upload was not issued");
             if (direct) return FASTH_OK;
             if (nv && dvm && d2h && !strcmp(d2h, "kernel"))
                 TRY(c->timed([&] { return launch_stream_copy(dv, dvm, (int64_t)nv, c->num_sms, c->stream); }, "d2h_copy"));

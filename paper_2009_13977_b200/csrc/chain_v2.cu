@@ -170,6 +170,10 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         for (int s = 0; s < NSLOTV; ++s) mbar_expect_u32(exb_u32 + 8u * s, ex_bytes);
     }
     __syncthreads();
+    if (a.xg_ready) {  // streamed host step: X / G still landing
+        if (tid == 0) wait_counter_bounded(a.xg_ready, a.xg_target);
+        __syncthreads();
+    }
     if (warp == PW && lane == 0) {
         const uint32_t stg_u32 = dev::smem_u32(stg);
         // launched as a programmatic dependent of the builder: everything up
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             if (a.late_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         }
         for (int t = 0; t < NSTG && t < q; ++t) {
-            if (a.ready) wait_counter(a.ready + block_of(t), (unsigned)C);
+            if (a.ready) wait_counter_bounded(a.ready + block_of(t), (unsigned)C);
             mbar_expect_u32(bar_u32 + 8u * t, stage_bytes);
             bulk_u32(stg_u32 + (uint32_t)t * stage_bytes, gstage(t), stage_bytes, bar_u32 + 8u * t);
         }
@@ -214,6 +218,11 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     GSTAMP(11);
     // peers' barriers armed before anyone pushes; Xn visible
     dev::cluster_sync();
+    // every CTA has read X / G: the last one re-arms the streamed-upload count
+    if (a.xg_ready && tid == 0 && atomicAdd(a.xg_seen, 1u) == gridDim.x - 1) {
+        *a.xg_ready = 0u;
+        *a.xg_seen = 0u;
+    }
     GSTAMP(12);
 
     const uint32_t zr_u32 = dev::smem_u32(Zr);
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             const int tn = t - 1 + NSTG;
             if (t > 0 && tn < q) {
                 const int sp = st == 0 ? NSTG - 1 : st - 1;
-                if (a.ready) wait_counter(a.ready + block_of(tn), (unsigned)C);
+                if (a.ready) wait_counter_bounded(a.ready + block_of(tn), (unsigned)C);
                 mbar_expect_u32(bar_u32 + 8u * sp, stage_bytes);
                 bulk_u32(dev::smem_u32(stg) + (uint32_t)sp * stage_bytes, gstage(tn), stage_bytes,
                          bar_u32 + 8u * sp);

@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
                 a.ready[i] = 0u;
                 a.done[i] = 0u;
                 a.dvcnt[i] = 0u;
+                if (a.upc) a.upc[i] = 0u;
             }
         }
         __syncthreads();

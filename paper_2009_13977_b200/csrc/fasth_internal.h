@@ -60,6 +60,10 @@ struct Plan {
     // the order the two sweeps need them).  nullptr / 0: plain launch.
     unsigned* ready = nullptr;
     int nbuild = 0;
+    // streamed host step (build4): V's columns land while the builder runs;
+    // block k is in once upc[k] >= upc_target (host_io.cu upload_kernel)
+    const unsigned* upc = nullptr;
+    unsigned upc_target = 0;
     // plain launch: build blocks [blk_lo, blk_hi) only (blk_hi < 0: all q)
     int blk_lo = 0, blk_hi = -1;
     // column-major activations the next kernel reads first (X, G): the
@@ -119,6 +123,11 @@ struct SweepV2Args {
     unsigned* done;
     int sig_from;         // done counting starts at this step (earlier steps published with it)
     int pub_ns;           // publish warp's back-off between polls of the tape warp's count
+    // streamed host step: X / G land while the kernel runs (wait for
+    // xg_ready >= xg_target before loading them; the last CTA resets both)
+    unsigned* xg_ready;
+    unsigned xg_target;
+    unsigned* xg_seen;
     int late_trigger;     // release programmatic dependents only once the previous grid
                           // (the builder) is complete, not at entry
     int pdl;              // launched as a programmatic dependent of the builder
@@ -141,6 +150,7 @@ struct DvArgs {
     unsigned* done;
     unsigned* dvcnt;
     unsigned done_target;
+    unsigned* upc;  // streamed host step: block i's upload count, reset with the others
     size_t min_smem;  // pipelined: dynamic shared memory to request at least
     long long* trace;  // optional per-CTA global-timer stamps [block][slab][6] (FASTH_STEPTRACE)
     int order;  // blockIdx.y -> block: 0 identity (backward sweep order), 1 middle-out (fused fwd+bwd)
@@ -167,6 +177,18 @@ size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg, bool sig);  // sig:
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
 // host_io.cu: streaming copy kernel (either side may be a pinned-host mapping)
 cudaError_t launch_stream_copy(const float* src, float* dst, int64_t n, int num_sms, cudaStream_t s);
+// streamed upload of the host step (host_io.cu): X, G, then V's blocks
+// outside-in, each unit counted per landed chunk (target ncb per counter
+// entry: upc[k] per block, xg_cnt for X and G together 2 * ncb)
+struct UploadArgs {
+    const float4 *x_src, *g_src, *v_src;  // device views of the pinned inputs
+    float4 *x_dst, *g_dst, *v_dst;
+    int64_t x4, v4, blk4;  // float4 counts: X (= G), V, one block of columns
+    int q, ncb;
+    unsigned* upc;     // [q]
+    unsigned* xg_cnt;  // X and G
+};
+cudaError_t launch_upload(const UploadArgs& u, int ctas, cudaStream_t s);
 cudaError_t launch_stream_copy_n(const float* const* src, float* const* dst, const int64_t* n, int nseg, int num_sms,
                                  cudaStream_t s);
 // wy_api.cu: the reference's WY internals (wy.hpp:56-170) in its own layout

@@ -96,6 +96,19 @@ __device__ __forceinline__ void wait_counter(const unsigned* c, unsigned target)
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// wait_counter for producers in other grids that may not run yet: gives up
+// after ~2^24 polls (seconds) instead of hanging the GPU if a count is
+// never reached; the results are then wrong and the parity tests say so
+__device__ __forceinline__ void wait_counter_bounded(const unsigned* c, unsigned target) {
+    unsigned v;
+    for (unsigned it = 0; it < (1u << 24); ++it) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_u32(uint32_t a, uint32_t parity) {
     asm volatile(
         "{\n"

@@ -72,7 +72,65 @@ __global__ void __launch_bounds__(kCopyThreads) copyn_kernel(Segs sg) {
     }
 }
 
+// Streamed upload of the host step (fasth_forward_backward_host): X and G,
+// then V's WY blocks in the order the two chains need them (0, q-1, 1, q-2,
+// ...).  Each unit (X, G, one block of b columns) is ncb chunks; the CTAs take
+// chunks in that order with few in flight per CTA, so units land in order,
+// and count every landed chunk (gpu-scope release) in the unit's counter:
+// the builder of block i starts once blocks i-1..i+1 are in, the sweep once
+// X and G are.  Releases its dependents (the builder) at entry.
+__global__ void __launch_bounds__(kCopyThreads) upload_kernel(UploadArgs u) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int nunits = 2 + u.q, nchunks = nunits * u.ncb;
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const int unit = c / u.ncb, part = c - unit * u.ncb;
+        const float4* src;
+        float4* dst;
+        int64_t len;
+        unsigned* cnt;
+        if (unit < 2) {
+            src = unit == 0 ? u.x_src : u.g_src;
+            dst = unit == 0 ? u.x_dst : u.g_dst;
+            len = u.x4;
+            cnt = u.xg_cnt;
+        } else {
+            const int j = unit - 2;  // outside-in: 0, q-1, 1, q-2, ...
+            const int k = (j & 1) ? u.q - 1 - (j >> 1) : (j >> 1);
+            const int64_t lo = (int64_t)k * u.blk4, hi = min(lo + u.blk4, u.v4);
+            src = u.v_src + lo;
+            dst = u.v_dst + lo;
+            len = hi - lo;
+            cnt = u.upc + k;
+        }
+        const int64_t per = (len + u.ncb - 1) / u.ncb;
+        const int64_t b0 = part * per, b1 = min(b0 + per, len);
+        float4 v[kUnroll];
+        for (int64_t i0 = b0 + threadIdx.x; i0 < b1; i0 += kUnroll * kCopyThreads) {
+#pragma unroll
+            for (int e = 0; e < kUnroll; ++e) {
+                const int64_t i = i0 + e * kCopyThreads;
+                if (i < b1) v[e] = __ldcs(src + i);
+            }
+#pragma unroll
+            for (int e = 0; e < kUnroll; ++e) {
+                const int64_t i = i0 + e * kCopyThreads;
+                if (i < b1) dst[i] = v[e];
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) atomicAdd(cnt, 1u);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_upload(const UploadArgs& u, int ctas, cudaStream_t s) {
+    if (u.ncb < 1 || u.q < 1 || !u.upc || !u.xg_cnt) return cudaErrorInvalidValue;
+    const int nchunks = (2 + u.q) * u.ncb;
+    upload_kernel<<<std::max(1, std::min(ctas, nchunks)), kCopyThreads, 0, s>>>(u);
+    return cudaGetLastError();
+}
 
 // dst[j][0..n[j]) = src[j][0..n[j]) for up to 4 segments in one launch when
 // every segment is 16-byte aligned with n % 4 == 0, else one launch each.

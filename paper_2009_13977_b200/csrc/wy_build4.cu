@@ -181,8 +181,6 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
     const int rank = (int)dev::cluster_ctarank();
     const int row0 = rank * RB;
-    const int i = p.blk_lo + (int)dev::cluster_id_x();
-    const int w = min(p.b, p.n - i * p.b);
     const int nrows = max(0, min(RB, p.d - row0));
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // L2 prefetch of the sweep's first reads (X, G), one 128-byte line per thread
@@ -194,21 +192,37 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
             if (base) asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)c * p.pf_ld[mi] + 32 * l));
         }
     }
-#define BTRACE(k) \
-    if (p.trace && tid == 0) p.trace[((size_t)i * C + rank) * 10 + (k)] = clock64()
-    BTRACE(0);
-    if (p.trace && tid == 0) p.trace[((size_t)i * C + rank) * 10 + 8] = (long long)dev::globaltimer();
-
     constexpr int E = 3 * E1;
     const int per = L.per;
     const int mylo = min(E, rank * per), myhi = min(E, mylo + per), mylen = myhi - mylo;
     const uint32_t barA = dev::smem_u32(&bars[0]), barB = dev::smem_u32(&bars[1]);
+
+    // One block per cluster, or (p.nbuild > 0) persistent clusters taking
+    // blocks cj, cj + nclusters, ...: the streamed host step builds on a few
+    // clusters so that the sweep finds its SMs free.  Streamed, blocks go in
+    // the upload's (and the two chains') order 0, q-1, 1, q-2, ...
+    const int ncl = (int)gridDim.x / C;
+    for (int cj = (int)dev::cluster_id_x(), it = 0; p.nbuild > 0 ? cj < p.q : it == 0; cj += ncl, ++it) {
+    const int i = p.upc ? ((cj & 1) ? p.q - 1 - (cj >> 1) : (cj >> 1)) : p.blk_lo + cj;
+    const int w = min(p.b, p.n - i * p.b);
+    if (it > 0) __syncthreads();  // the previous block's shared-memory readers are done
+#define BTRACE(k) \
+    if (p.trace && tid == 0) p.trace[((size_t)i * C + rank) * 10 + (k)] = clock64()
+    BTRACE(0);
+    if (p.trace && tid == 0) p.trace[((size_t)i * C + rank) * 10 + 8] = (long long)dev::globaltimer();
     // 1. rows of blocks i (slot 0), i-1 (1), i+1 (2), permuted positions:
     //    thread k takes 4-row group k % RG of column k / RG (consecutive
     //    threads walk down a column: whole lines), eight 16-byte loads in
     //    flight per thread (one round trip at b = 32, 80-row slabs).  The
     //    phase is issue-bound at two CTAs per SM: (column, group) advance
     //    incrementally, no division per element
+    //    Streamed host step (p.upc): V's columns arrive while the builder
+    //    runs; wait until blocks i-1..i+1 have landed (L2-coherent loads)
+    if (p.upc) {
+        if (tid == 0)
+            for (int k = max(i - 1, 0); k <= min(i + 1, p.q - 1); ++k) wait_counter_bounded(p.upc + k, p.upc_target);
+        __syncthreads();
+    }
     {
         constexpr int NB = 8;
         const int RG = RB / 4, NTOT = 3 * BS * RG;
@@ -231,12 +245,12 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
                 if (j < wb && r < nrows) {
                     const float* src = V + (int64_t)(p.reversed ? p.n - 1 - (k0 + j) : k0 + j) * ldv + row0 + r;
                     if (vec_ok && r + 4 <= nrows) {
-                        v[u] = __ldg(reinterpret_cast<const float4*>(src));
+                        v[u] = __ldcg(reinterpret_cast<const float4*>(src));
                     } else {
-                        v[u].x = src[0];
-                        if (r + 1 < nrows) v[u].y = src[1];
-                        if (r + 2 < nrows) v[u].z = src[2];
-                        if (r + 3 < nrows) v[u].w = src[3];
+                        v[u].x = __ldcg(src);
+                        if (r + 1 < nrows) v[u].y = __ldcg(src + 1);
+                        if (r + 2 < nrows) v[u].z = __ldcg(src + 2);
+                        if (r + 3 < nrows) v[u].w = __ldcg(src + 3);
                     }
                 }
                 jj += dq, rg += dr;
@@ -251,9 +265,11 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
         }
     }
     if (tid == 0) {
-        dev::mbar_init(&bars[0], 1);
-        dev::mbar_init(&bars[1], 1);
-        dev::fence_mbar_init();
+        if (it == 0) {
+            dev::mbar_init(&bars[0], 1);
+            dev::mbar_init(&bars[1], 1);
+            dev::fence_mbar_init();
+        }
         mbar_expect_u32(barA, (uint32_t)((C - 1) * mylen * 4));
         mbar_expect_u32(barB, (uint32_t)((E - mylen) * 4));
     }
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
         }
     }
     // 3b. my slice: sum the C partials in source order (f64), push the result
-    mbar_wait_acq_cluster(barA, 0);
+    mbar_wait_acq_cluster(barA, (uint32_t)(it & 1));
     {
         const uint32_t gr_u32 = dev::smem_u32(Gr);
         for (int q4 = tid; 4 * q4 < mylen; q4 += NTH4) {
@@ -343,7 +359,7 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
         }
     }
     BTRACE(3);
-    mbar_wait_acq_cluster(barB, 0);
+    mbar_wait_acq_cluster(barB, (uint32_t)(it & 1));
     __syncthreads();
     BTRACE(4);
 
@@ -522,12 +538,22 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
             if (doSb) bulk_s2g(p.Pb + ((size_t)i * C + r) * SF + soff, dev::smem_u32(ISb), sb);
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        // shared memory may be released once read; the writes complete with the grid
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (p.ready) {
+            // pipelined step: block i's rows are published once written
+            // (the sweep bulk-loads the stages after acquiring the counter)
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __threadfence();
+            atomicAdd(p.ready + i, 1u);
+        } else {
+            // shared memory may be released once read; the writes complete with the grid
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         BTRACE(7);
         if (p.trace) p.trace[((size_t)i * C + rank) * 10 + 9] = (long long)dev::globaltimer();
     }
 #undef BTRACE
+    }  // blocks of this cluster
 }
 
 template <int BS>
@@ -535,7 +561,7 @@ cudaError_t launch_build4_t(const Plan& p, const float* V, int64_t ldv, ErrWord*
     const B4Layout L = b4_layout(BS, p.d_pad / p.CB, p.CB);
     if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(build4_kernel<BS>), L.total, true); e != cudaSuccess)
         return e;
-    const int nclu = (p.blk_hi < 0 ? p.q : p.blk_hi) - p.blk_lo;
+    const int nclu = p.nbuild > 0 ? (p.nbuild < p.q ? p.nbuild : p.q) : (p.blk_hi < 0 ? p.q : p.blk_hi) - p.blk_lo;
     if (nclu <= 0) return cudaSuccess;
     // 16-byte row groups need 16-byte aligned columns
     const int vec_ok = ((reinterpret_cast<uintptr_t>(V) & 15) == 0) && (ldv % 4 == 0);
@@ -544,13 +570,16 @@ cudaError_t launch_build4_t(const Plan& p, const float* V, int64_t ldv, ErrWord*
     cfg.blockDim = dim3(NTH4, 1, 1);
     cfg.dynamicSmemBytes = L.total;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = p.CB;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // streamed host step: a programmatic dependent of the upload kernel
+    cfg.numAttrs = p.upc ? 2 : 1;
     return cudaLaunchKernelEx(&cfg, build4_kernel<BS>, p, V, ldv, vec_ok, err);
 }
 
@@ -559,8 +588,8 @@ cudaError_t launch_build4_t(const Plan& p, const float* V, int64_t ldv, ErrWord*
 size_t build4_smem_bytes(int BS, int RB, int C) { return b4_layout(BS, RB, C).total; }
 
 cudaError_t launch_build4(const Plan& p, const float* V, int64_t ldv, ErrWord* err, cudaStream_t s) {
-    if (!p.Pf || !p.Pb || p.CB < 1 || p.CB > 16 || p.d_pad % p.CB || (p.d_pad / p.CB) % 16 || p.ready ||
-        p.nbuild > 0)
+    if (!p.Pf || !p.Pb || p.CB < 1 || p.CB > 16 || p.d_pad % p.CB || (p.d_pad / p.CB) % 16 ||
+        (p.nbuild > 0 && (p.blk_lo != 0 || p.blk_hi >= 0)))
         return cudaErrorInvalidValue;
     switch (p.BS) {
         case 16: return launch_build4_t<16>(p, V, ldv, err, s);

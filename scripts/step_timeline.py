@@ -17,6 +17,9 @@ t0 = b[:, 8].min()
 us = lambda x: (x - t0) / 1e3  # noqa: E731
 print(f"q={q} C={C}: {brows} builder CTAs, {sctas} sweep CTAs, {dctas} gradient CTAs (us from first builder start)")
 print(f"  builder : start {us(b[:, 8].min()):6.2f}..{us(b[:, 8].max()):6.2f}  end {us(b[:, 9].min()):6.2f}..{us(b[:, 9].max()):6.2f}")
+if brows % q == 0:
+    be = b[:, 9].reshape(q, brows // q).max(axis=1)
+    print("  builder end per block: " + " ".join(f"{x:5.1f}" for x in us(be)))
 r = s[:, q, :]
 for k, nm in ((10, "entry"), (11, "X loaded"), (12, "cluster synced"), (13, "prologue pushed"), (14, "loop done"), (15, "exit")):
     v = r[:, k]
@@ -37,3 +40,6 @@ if dctas:
     print(f"  dv V-term  {us(d[:, 3].min()):6.2f}..{us(d[:, 3].max()):6.2f}  (loaded->V mean {np.mean(d[:, 3] - d[:, 2]) / 1e3:.2f} us)")
     print(f"  dv end     {us(d[:, 4].min()):6.2f}..{us(d[:, 4].max()):6.2f}  (V->end mean {np.mean(d[:, 4] - d[:, 3]) / 1e3:.2f} us)")
     print(f"  dv SMs used {len(set(d[:, 5].astype(int)))}")
+    if dctas % q == 0 and (dv[:, 4] > 0).all():
+        de = dv[:, 4].reshape(q, dctas // q).max(axis=1)
+        print("  dv end per block: " + " ".join(f"{x:5.1f}" for x in us(de)))

@@ -349,7 +349,7 @@ def test_host_buffer_entry(fb, oracle):
 @pytest.mark.parametrize("d,n,m,b", [(784, 784, 32, 32), (200, 200, 17, 6), (64, 64, 32, 8), (300, 45, 8, 16),
                                      (96, 5, 3, 32), (128, 128, 100, 32)])
 def test_host_pipelined_equals_device_bitwise(fb, d, n, m, b):
-    """The host-buffer call (V, X, G in by one SM copy kernel; dV stored by
+    """The host-buffer call (V, X, G in by the streamed SM upload kernel; dV stored by
     the gradient kernel straight into the pinned buffer while the sweep still
     runs, Y / dX by the sweep's 16-byte stores; ragged shapes take the scalar
     tails): same arithmetic as the device-resident fasth_forward_backward, so
@@ -364,6 +364,33 @@ def test_host_pipelined_equals_device_bitwise(fb, d, n, m, b):
     want = (host(Yd).T, host(back.grad_input).T, host(back.grad_vectors))
     for _ in range(3):
         got = fb.forward_backward_host(Vh, Xh, Gh, b)
+        for u, w in zip(got, want):
+            assert np.array_equal(u.double().numpy(), w)
+
+
+@pytest.mark.parametrize("env", [{"FASTH_UPLOAD_STREAM": "0"}, {"FASTH_BUILDERS": "3"}, {"FASTH_UPLOAD_CTAS": "1"},
+                                 {"FASTH_BUILDERS": "40", "FASTH_UPLOAD_CTAS": "64"}])
+@pytest.mark.parametrize("d,n,m,b", [(784, 784, 32, 32), (200, 200, 17, 6), (300, 45, 8, 16), (2048, 2048, 32, 32)])
+def test_host_streamed_upload_variants(fb, monkeypatch, env, d, n, m, b):
+    """The streamed host step (host_io.cu upload_kernel: X, G, then V's blocks
+    outside-in, counted per block; build4 on persistent clusters waiting per
+    block; the sweep and the gradient kernel on the pipelined counters) under
+    its knobs — plain upload, 3 builder clusters (8+ blocks each), one upload
+    CTA (strict order), more clusters than blocks — gives the device step's
+    bits, call after call (the upload counters re-arm themselves)."""
+    import torch
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(d + 3 * n + m)
+    V, X, G = rng.standard_normal((n, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    Vh = torch.tensor(V, dtype=torch.float32).pin_memory()
+    Xh = torch.tensor(X.T.copy(), dtype=torch.float32).pin_memory()
+    Gh = torch.tensor(G.T.copy(), dtype=torch.float32).pin_memory()
+    Yd, back = fb.fasth_forward_backward(Vh.cuda(), Xh.cuda().t(), Gh.cuda().t(), b)
+    want = (host(Yd).T, host(back.grad_input).T, host(back.grad_vectors))
+    ctx = fb.Context(0)  # the host graph is cached per context: a fresh one per variant
+    for _ in range(3):
+        got = fb.forward_backward_host(Vh, Xh, Gh, b, ctx=ctx)
         for u, w in zip(got, want):
             assert np.array_equal(u.double().numpy(), w)
 
