@@ -94,6 +94,7 @@ struct fasth_ctx_s {
     // there the gradient kernel runs behind the sweep (PCIe writes overlap it)
     bool dv_pipe_pref = false;
     bool dv_v_pre = false;  // the last sweep launched released its dependents after the builder
+    int dv_chain = 0;       // run_dv: 1 first / 2 later of independent kernels after a sweep
     // streamed host step: the upload the next build_plan launches (before its
     // builder), whether the tape geometry allows it to stream, and whether the
     // step in flight streams (consumed by the sweep and the gradient kernel)
@@ -824,6 +825,11 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
     v.pdl = !getenv("FASTH_NO_PDL") && !c->after_stream_wait;  // the sweep was the previous launch
     v.v_pre = c->dv_v_pre || !v.pdl;
     c->after_stream_wait = false;
+    if (c->dv_chain == 1) {  // first of independent kernels reading complete inputs
+        v.pdl = 0, v.v_pre = 1, v.trigger = 1;
+    } else if (c->dv_chain == 2) {  // behind such a kernel: start early, nothing to wait for
+        v.pdl = 1, v.nowait = 1, v.v_pre = 1, v.trigger = 1;
+    }
     if (getenv("FASTH_STEPTRACE") && c->step_trace && c->st_hdr[3] > 0) {
         v.trace = c->step_trace + c->st_dv;
         c->st_hdr[4] = ((p.d_pad + 63) / 64) * p.q;
@@ -916,6 +922,8 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     t->WC = G.WC;
     t->ngroups = (m + t->WC - 1) / t->WC;
     t->v2nstg = G.C > 0 ? sweep2_nstg(G.C, BS, G.d_pad) : 0;
+    if (const char* e = getenv("FASTH_NSTG"))  // A/B knob: fewer stage buffers (less shared memory)
+        if (t->v2nstg >= 2) t->v2nstg = std::max(2, std::min(t->v2nstg, atoi(e)));
     if (t->v2nstg < 2) {
         delete t;
         return fail(FASTH_ERR_INVALID, "fasth: dimension %d too large for the chain kernels at block width %d", d, BS);
@@ -2168,23 +2176,35 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
                 if (s) break;
             }
             a.dir[1] = v2_backward_dir(tv, dT2, d, k, p->sigma, dx, dX ? lddx : d, want_dv);
-            a.pdl = 0;
+            // launched early (its prologue overlaps launch 1's tail); the row
+            // warps wait for launch 1 before loading T1 / dT2
+            a.pdl = !getenv("FASTH_NO_PDL");
+            a.x_wait = 1;
             s = launch_traced_sweep2(c, a, "sweep(svd 2)");
             if (dx != dX) c->release(dx);
             if (s) break;
         }
-        if (dsigma) {
-            s = c->timed([&] { return launch_dsigma(dT2, d, T1, d, k, m, dsigma, c->stream); }, "dsigma");
-            if (s) break;
-        }
-        c->after_stream_wait = true;  // the gradient kernels read both launches' tapes
+        // the two gradient kernels and dSigma read only finished tapes and
+        // T1 / dT2: the first waits for launch 2, the others run beside it
+        int nind = 0;
         if (want_du) {
+            c->dv_chain = 1;
             s = run_dv(c, tu, dU, lddu);
+            c->dv_chain = 0;
             if (s) break;
+            ++nind;
         }
         if (want_dv) {
-            c->after_stream_wait = true;
+            c->after_stream_wait = nind == 0;
+            c->dv_chain = nind == 0 ? 1 : 2;
             s = run_dv(c, tv, dV, lddv);
+            c->dv_chain = 0;
+            if (s) break;
+            ++nind;
+        }
+        if (dsigma) {
+            const bool early = nind > 0 && !getenv("FASTH_NO_PDL");
+            s = c->timed([&] { return launch_dsigma(dT2, d, T1, d, k, m, dsigma, c->stream, early); }, "dsigma");
             if (s) break;
         }
     } while (0);

@@ -189,8 +189,10 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         }
     }
 
-    // row warps: X^(0) tiles into registers and B-fragment order
+    // row warps: X^(0) tiles into registers and B-fragment order (x_wait: X
+    // is the previous grid's output, the launch only started early)
     float x[TPW][4];
+    if (warp < NR && a.x_wait) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (warp < NR) {
 #pragma unroll
         for (int u = 0; u < TPW; ++u) {

@@ -122,8 +122,9 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
             dev::cp_async16(Vs + 4 * idx, src + 4 * idx, true);
         dev::cp_async_commit();
     };
+    if (a.trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (a.v_pre) stage_v();
-    if (!a.done && a.pdl) asm volatile("griddepcontrol.wait;" ::: "memory");  // sweep complete
+    if (!a.done && a.pdl && !a.nowait) asm volatile("griddepcontrol.wait;" ::: "memory");  // sweep complete
     if (a.done) {  // pipelined step: both sweeps have passed block i
         if (tid == 0) {
             unsigned v;

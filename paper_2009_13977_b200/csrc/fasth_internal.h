@@ -128,6 +128,8 @@ struct SweepV2Args {
     unsigned* xg_ready;
     unsigned xg_target;
     unsigned* xg_seen;
+    int x_wait;           // X / G are the previous grid's outputs: the row warps wait for it
+                          // before loading them (so the launch may still start early)
     int late_trigger;     // release programmatic dependents only once the previous grid
                           // (the builder) is complete, not at entry
     int pdl;              // launched as a programmatic dependent of the builder
@@ -158,6 +160,8 @@ struct DvArgs {
     int pdl;  // launched as a programmatic dependent of the sweep (griddepcontrol.wait first)
     int v_pre;  // Vbl is complete at launch (the sweep released its dependents after the
                 // builder): V fragments load before the wait on the sweep
+    int trigger;  // release programmatic dependents at entry (independent kernels after it)
+    int nowait;   // launched behind an independent kernel: its inputs are complete, no wait
 };
 
 // wy_build2.cu (packed stages for chain_v2.cu)
@@ -210,7 +214,7 @@ cudaError_t launch_scale_rows(const float* x, int64_t ldx, int n_valid, const fl
                               int rows, int m, float* y, int64_t ldy, int mode,
                               cudaStream_t s);
 cudaError_t launch_dsigma(const float* dT2, int64_t ld2, const float* T1, int64_t ld1, int k,
-                          int m, float* dsigma, cudaStream_t s);
+                          int m, float* dsigma, cudaStream_t s, bool pdl_nowait = false);
 cudaError_t launch_step(const float* P, int64_t ldp, const float* dP, int64_t lddp, int dim,
                         int n, float eta, float* out, int64_t ldo, ErrWord* err, int tag,
                         cudaStream_t s);

@@ -33,12 +33,23 @@ __global__ void scale_rows_kernel(const float* __restrict__ x, int64_t ldx, int 
 __global__ void dsigma_kernel(const float* __restrict__ dT2, int64_t ld2,
                               const float* __restrict__ T1, int64_t ld1, int k, int m,
                               float* dsigma) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= k) return;
-    // 8 columns' loads in flight per round trip (the loop was latency bound);
-    // the batch sum stays in f64, in the same column order
+    // 32 columns' loads in flight per round trip (the loop is latency bound:
+    // one round trip at batch 32); the batch sum stays in f64, in column order
     double acc = 0.0;
     int l = 0;
+    for (; l + 32 <= m; l += 32) {
+        float a[32], b[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            a[u] = __ldg(dT2 + (int64_t)(l + u) * ld2 + i);
+            b[u] = __ldg(T1 + (int64_t)(l + u) * ld1 + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) acc += (double)a[u] * b[u];
+    }
     for (; l + 8 <= m; l += 8) {
         float a[8], b[8];
 #pragma unroll
@@ -183,14 +194,26 @@ cudaError_t launch_scale_rows(const float* x, int64_t ldx, int n_valid, const fl
     return cudaGetLastError();
 }
 
+// pdl_nowait: launched as a programmatic dependent of a kernel it does not
+// depend on (its inputs were complete when that one started): starts early
 cudaError_t launch_dsigma(const float* dT2, int64_t ld2, const float* T1, int64_t ld1, int k,
-                          int m, float* dsigma, cudaStream_t s) {
+                          int m, float* dsigma, cudaStream_t s, bool pdl_nowait) {
     if (k == 0) return cudaSuccess;
-    if (m >= 512)  // one thread per row would leave most SMs idle for a long sequential sum
-        dsigma_wide_kernel<<<(k + 31) / 32, 32 * DSW, 0, s>>>(dT2, ld2, T1, ld1, k, m, dsigma);
-    else
-        dsigma_kernel<<<(k + 127) / 128, 128, 0, s>>>(dT2, ld2, T1, ld1, k, m, dsigma);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_nowait ? 1 : 0;
+    if (m >= 512) {  // one thread per row would leave most SMs idle for a long sequential sum
+        cfg.gridDim = dim3((k + 31) / 32);
+        cfg.blockDim = dim3(32 * DSW);
+        return cudaLaunchKernelEx(&cfg, dsigma_wide_kernel, dT2, ld2, T1, ld1, k, m, dsigma);
+    }
+    cfg.gridDim = dim3((k + 127) / 128);
+    cfg.blockDim = dim3(128);
+    return cudaLaunchKernelEx(&cfg, dsigma_kernel, dT2, ld2, T1, ld1, k, m, dsigma);
 }
 
 cudaError_t launch_step(const float* P, int64_t ldp, const float* dP, int64_t lddp, int dim,
