@@ -95,6 +95,7 @@ struct fasth_ctx_s {
     bool dv_pipe_pref = false;
     bool dv_v_pre = false;  // the last sweep launched released its dependents after the builder
     int dv_chain = 0;       // run_dv: 1 first / 2 later of independent kernels after a sweep
+    bool geom_fused = false;  // new_tape: the chain runs as fused fwd | bwd launches
     // streamed host step: the upload the next build_plan launches (before its
     // builder), whether the tape geometry allows it to stream, and whether the
     // step in flight streams (consumed by the sweep and the gradient kernel)
@@ -460,10 +461,12 @@ int internal_b(int d, int n, int b_user) {
     if (const char* e = getenv("FASTH_INTERNAL_BS"))
         return std::max(1, std::min({atoi(e), kMaxBS, std::max(n, 1)}));
     const int b = std::min(std::max(b_user, 1), n);
-    // 64-wide blocks only at d <= 512, 16-wide beyond d = 2048: past those
-    // sizes the chain kernel's stages and exchange slots no longer fit shared
-    // memory (the same product either way)
-    return std::min(b, d > 2048 ? 16 : d > 512 ? 32 : kMaxBS);
+    // at most 32 wide (64-wide blocks measured 2-3.5x slower at every d they
+    // fit, d <= 512: the 64-wide sweep spills and its builder is build2),
+    // 16-wide beyond d = 2048 (the stages and exchange slots no longer fit
+    // shared memory); the same product either way.  FASTH_INTERNAL_BS=64
+    // still reaches the 64-wide kernels.
+    return std::min(b, d > 2048 ? 16 : 32);
 }
 
 // Build the compacted chain (Alg. 1 step 1) on the device, in the row
@@ -917,7 +920,7 @@ fasth_status new_tape(fasth_ctx c, const float* V, int64_t ldv, int d, int n, in
     t->b_user = b;
     t->n_valid = d;
     const int BS = next_pow2_min16(internal_b(d, n, b));
-    const SweepGeom G = pick_geometry(d, m, BS, c->num_sms);
+    const SweepGeom G = pick_geometry(d, m, BS, c->num_sms, c->geom_fused);
     t->C = G.C;
     t->WC = G.WC;
     t->ngroups = (m + t->WC - 1) / t->WC;
@@ -1504,7 +1507,9 @@ fasth_status fasth_forward_backward(fasth_ctx c, const float* V, int64_t ldv, in
         return run_large_batch(c, V, ldv, d, n, X, ldx, G, ldg, m, Y, ldy, dX, lddx, dV, lddv);
     fasth_tape t = nullptr;
     c->pf[0] = X, c->pf_ld[0] = ldx, c->pf[1] = G, c->pf_ld[1] = ldg;
+    c->geom_fused = true;  // both sweeps in one launch: its cluster count picks the geometry
     const fasth_status s0 = new_tape(c, V, ldv, d, n, m, block_width, 0, 0, &t, dV != nullptr);
+    c->geom_fused = false;
     c->pf[0] = c->pf[1] = nullptr;  // consumed by the build (or dropped on failure)
     TRY(s0);
     fasth_status s = run_forward_backward(c, t, X, ldx, Y, ldy, G, ldg, dX, lddx, dV, lddv);
@@ -2108,6 +2113,7 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
     float *T1 = nullptr, *dT2 = nullptr;
     fasth_status s = FASTH_OK;
     const fasthb::lb::Streams* side = c->svd_streams();
+    c->geom_fused = true;  // paired sweeps: two chains per launch
     do {
         // builds: U on the side stream, V on the main stream
         if (side) {
@@ -2124,6 +2130,7 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
             if (s) break;
         }
         s = new_tape(c, p->V, p->ldv, d, p->nv, m, block_width, 1, 1, &tv);
+        c->geom_fused = false;
         if (s) break;
         if (side) {
             CU(cudaStreamWaitEvent(c->stream, side->ev[9], 0));
@@ -2208,6 +2215,7 @@ fasth_status fasth_svd_forward_backward(fasth_ctx c, const fasth_svd_param* p, c
             if (s) break;
         }
     } while (0);
+    c->geom_fused = false;
     free_tape(tu);
     free_tape(tv);
     c->release(T1);

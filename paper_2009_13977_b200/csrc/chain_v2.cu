@@ -30,6 +30,7 @@
 //             cluster (st.async + remote mbarrier complete_tx)
 //             B warps:   Z_t = sum_c L_t^c (fixed order) + (-2 S_t Z_{t-1})
 //   phase 2   row warps: X^(t+1) = X^(t) + V_t (-2 Z_t) in their accumulators
+#include <algorithm>
 #include <cstdlib>
 
 #include "device_prims.cuh"
@@ -704,14 +705,22 @@ int sweep2_nstg(int C, int BS, int d_pad) {
 // Chain geometry: C CTAs per cluster split the rows into RC (a multiple of
 // 16) each; 8 batch columns per cluster.  ~80-row slabs up to 10 CTAs per
 // cluster (measured on B200 at d = 784: 10 x 80 beats 7 x 112 by ~4% per
-// fwd+bwd step; 12+ CTA clusters no longer fit the fused launch's 8 clusters
-// on the GPCs at once), else ~112-row slabs, widened until the packed-stage
-// sweep fits shared memory.  FASTH_CLUSTER overrides C.
-SweepGeom pick_geometry(int d, int m, int BS, int num_sms) {
-    (void)m;
+// fwd+bwd step).  Past d = 800: clusters of 12+ CTAs fit the GPCs only ~7 at
+// a time, so a launch of 8+ clusters (the fused fwd+bwd at batch 32) runs a
+// second wave; there 10-CTA clusters with up to 256-row slabs win (d = 1280
+// / 1536 / 2048 / 2560: 245 -> 151, 299 -> 223, 434 -> 373, 683 -> 549 us per
+// fused step), and up to d = 1536 for every launch (the builder's 10-CTA
+// clusters pack better too: two-call d = 1280 242 -> 221 us), else ~112-row
+// slabs (two-call d = 2048: 418 vs 546 us at C = 10; fused at batch <= 24
+// too).  Widened until the packed-stage sweep fits shared memory.
+// FASTH_CLUSTER overrides C.
+SweepGeom pick_geometry(int d, int m, int BS, int num_sms, bool fused) {
     (void)num_sms;
     int C = (d + 79) / 80;
-    if (C > 10) C = (d + 111) / 112;
+    if (C > 10) {
+        const int clusters = (fused ? 2 : 1) * ((std::max(m, 1) + 7) / 8);
+        C = d <= 1536 || (clusters >= 8 && d <= 2560) ? 10 : (d + 111) / 112;
+    }
     C = C < 1 ? 1 : C > 16 ? 16 : C;
     if (const char* e = getenv("FASTH_CLUSTER")) C = atoi(e);
     if (C < 1 || C > 16) C = 8;

@@ -175,7 +175,7 @@ size_t build4_smem_bytes(int BS, int RB, int C);
 struct SweepGeom {
     int C = 0, RC = 16, d_pad = 16, WC = 8;  // C == 0: no geometry fits
 };
-SweepGeom pick_geometry(int d, int m, int BS, int num_sms);
+SweepGeom pick_geometry(int d, int m, int BS, int num_sms, bool fused);  // fused: fwd | bwd in one launch
 int sweep2_nstg(int C, int BS, int d_pad);  // 0 = geometry not supported by the v2 kernel
 size_t sweep2_smem_bytes(int C, int BS, int d_pad, int nstg, bool sig);  // sig: tape-warp variant
 cudaError_t launch_sweep2(const SweepV2Args& a, cudaStream_t s);
