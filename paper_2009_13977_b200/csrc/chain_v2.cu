@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+    const int ls4 = swz4(lane) * 4;  // this lane's 16-byte group of a swizzled B-fragment tile
     const uint32_t rank = dev::cluster_ctarank();
     const int cid = (int)dev::cluster_id_x();
     const int dirn = cid / a.ngroups, group = cid - dirn * a.ngroups;
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
                 }
 #pragma unroll
                 for (int e = 0; e < 4; ++e) x[u][e] = ok[e] ? v[e] * sc[e] : 0.f;
-                scatter_cb(Xn + rt * 256, Xn + rt * 256 + 128, x[u], g, tq, 1.f);
+                scatter_cb_swz(Xn + rt * 256, Xn + rt * 256 + 128, x[u], g, tq, 1.f);
             }
         }
     }
@@ -281,8 +282,8 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             if (rt < RT) {
                 float xh[4], xl[4];
                 const float* Xc = xbuf(s > 0 ? s - 1 : 0) + rt * 256;  // X^(s-1)
-                lds_vec<4>(xh, Xc + lane * 4);
-                lds_vec<4>(xl, Xc + 128 + lane * 4);
+                lds_vec<4>(xh, Xc + ls4);
+                lds_vec<4>(xl, Xc + 128 + ls4);
                 float w0[2][2 * MT], w1[2][2 * MT];
 #pragma unroll
                 for (int ks = 0; ks < 2; ++ks) {
@@ -345,16 +346,16 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             float* zb = zst ? D.zhat + ((size_t)i * BS + (lane & 3)) * a.m + zl : nullptr;
             auto ld_tile = [&](const float* p, float (&v)[4], float sc) {
                 float h[4], l[4];
-                lds_vec<4>(h, p + lane * 4);
-                lds_vec<4>(l, p + 128 + lane * 4);
+                lds_vec<4>(h, p + ls4);
+                lds_vec<4>(l, p + 128 + ls4);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) v[j] = sc * (h[j] + l[j]);
             };
             const float* zs = Zn + (s & 1) * (KB * 128);
             auto ld_z = [&](int mt, float (&v)[4]) {
                 float h[4], l[4];
-                lds_vec<4>(h, zs + mt * 128 + lane * 4);
-                lds_vec<4>(l, zs + (KB / 2) * 128 + mt * 128 + lane * 4);
+                lds_vec<4>(h, zs + mt * 128 + ls4);
+                lds_vec<4>(l, zs + (KB / 2) * 128 + mt * 128 + ls4);
 #pragma unroll
                 for (int j = 0; j < 4; ++j) v[j] = -0.5f * (h[j] + l[j]);
             };
@@ -481,8 +482,8 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
 #pragma unroll
                 for (int h2 = 0; h2 < KB / 2; ++h2) {
                     float zh[4], zl[4];
-                    lds_vec<4>(zh, zp + h2 * 128 + lane * 4);
-                    lds_vec<4>(zl, zp + (KB / 2) * 128 + h2 * 128 + lane * 4);
+                    lds_vec<4>(zh, zp + h2 * 128 + ls4);
+                    lds_vec<4>(zl, zp + (KB / 2) * 128 + h2 * 128 + ls4);
 #pragma unroll
                     for (int kk = 0; kk < 2; ++kk) {
                         const int ks = 2 * h2 + kk;
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
 #pragma unroll
             for (int e = 0; e < 4; ++e) z[e] += zs[e];
             float* zc = Zn + (t & 1) * (KB * 128) + mt * 128;
-            scatter_cb(zc, zc + (KB / 2) * 128, z, g, tq, -2.f);
+            scatter_cb_swz(zc, zc + (KB / 2) * 128, z, g, tq, -2.f);
             if (!SIG && D.zhat && rank == 0) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
@@ -552,8 +553,8 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             float zh[KB / 2][4], zl[KB / 2][4];
 #pragma unroll
             for (int h2 = 0; h2 < KB / 2; ++h2) {
-                lds_vec<4>(zh[h2], zc + h2 * 128 + lane * 4);
-                lds_vec<4>(zl[h2], zc + (KB / 2) * 128 + h2 * 128 + lane * 4);
+                lds_vec<4>(zh[h2], zc + h2 * 128 + ls4);
+                lds_vec<4>(zl[h2], zc + (KB / 2) * 128 + h2 * 128 + ls4);
             }
             float* tblk = tape0 && !SIG ? tape0 + (size_t)i * tape_step : nullptr;
 #pragma unroll
@@ -576,7 +577,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
                         *reinterpret_cast<float2*>(tp) = make_float2(x[u][0], x[u][1]);
                         *reinterpret_cast<float2*>(tp + 8 * WCV) = make_float2(x[u][2], x[u][3]);
                     }
-                    if (SIG || t + 2 < q) scatter_cb(xbuf(t + 1) + rt * 256, xbuf(t + 1) + rt * 256 + 128, x[u], g, tq, 1.f);
+                    if (SIG || t + 2 < q) scatter_cb_swz(xbuf(t + 1) + rt * 256, xbuf(t + 1) + rt * 256 + 128, x[u], g, tq, 1.f);
                 }
             }
             __syncwarp();

@@ -84,6 +84,27 @@ __device__ __forceinline__ void scatter_cb(float* hi, float* lo, const float (&v
         }
 }
 
+// The same B-fragment buffer with its 16-byte groups swizzled: group f lives
+// at f ^ (((f >> 3) & 1) << 2).  The producer's four tq lanes of a row then
+// cover 8 bank groups instead of 4 (2-way instead of 4-way conflicts on every
+// store); the consumer reads group swz4(lane) (an involution) with one
+// 16-byte load as before.
+__device__ __forceinline__ int swz4(int f) { return f ^ (((f >> 3) & 1) << 2); }
+__device__ __forceinline__ void scatter_cb_swz(float* hi, float* lo, const float (&v)[4], int g, int tq,
+                                               float s) {
+#pragma unroll
+    for (int e2 = 0; e2 < 2; ++e2)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int c = 2 * tq + e;
+            const int o = swz4(4 * c + (g & 3)) * 4 + 2 * e2 + (g >> 2);
+            const float x = s * v[e2 * 2 + e];
+            const uint32_t h = hi_rn(x);
+            hi[o] = __uint_as_float(h);
+            lo[o] = x - __uint_as_float(h);
+        }
+}
+
 // pipelined step: spin until counter >= target (acquire, gpu scope), then make
 // the generic-proxy writes it published visible to the bulk-copy engine
 __device__ __forceinline__ void wait_counter(const unsigned* c, unsigned target) {
