@@ -501,10 +501,15 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             float z[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) z[e] = cm[e] + (c1[e] + c2[e]);
+            if (trc && lane == 0 && mt == 0) trc[(size_t)t * 16 + 10] = clock64() + (long long)(z[0] != z[0]);
             const float* zr = Zr + ((size_t)slot * C * MT + mt) * 128 + lane * 4;
             float zs[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-            for (int c = 0; c < C; ++c) {  // fixed order over the source CTAs
+            // fixed order over the source CTAs; five 16-byte loads in flight
+            // per round (all ten spill the register budget; two-tile
+            // geometries keep two)
+            constexpr int ZU = TPW == 1 ? 5 : 2;
+#pragma unroll ZU
+            for (int c = 0; c < C; ++c) {
                 float p[4];
                 lds_vec<4>(p, zr + c * MT * 128);
 #pragma unroll
@@ -512,6 +517,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             }
 #pragma unroll
             for (int e = 0; e < 4; ++e) z[e] += zs[e];
+            if (trc && lane == 0 && mt == 0) trc[(size_t)t * 16 + 11] = clock64() + (long long)(z[0] != z[0]);
             float* zc = Zn + (t & 1) * (KB * 128) + mt * 128;
             scatter_cb_swz(zc, zc + (KB / 2) * 128, z, g, tq, -2.f);
             if (!SIG && D.zhat && rank == 0) {

@@ -78,6 +78,9 @@ def report(path):
                 ("B: exch wait (from top)", 3, 0, slice(0, q)), ("B: reduce+scatter", 4, 3, slice(0, q)),
                 ("barrier1 (from row done)", 5, 2, slice(0, q)), ("barrier1 (from B done)", 5, 4, slice(0, q)),
                 ("update", 6, 5, slice(0, q)), ("barrier2", 7, 6, slice(0, q))]
+        if (s[:, :, 10] != 0).any():  # B-warp detail stamps (chain_v2.cu slots 10, 11)
+            rows[4:4] = [("  B: re-arm + S.Z result", 10, 3, slice(0, q)), ("  B: sum of C partials", 11, 10, slice(0, q)),
+                         ("  B: scatter (+ Z' stores)", 4, 11, slice(0, q))]
     else:
         rows = [("A load wait", 1, 0, slice(0, q - 1)), ("A partial+push", 2, 1, slice(0, q - 1)),
                 ("B exch wait (from top)", 3, 0, slice(1, q)), ("B reduce+corr", 4, 3, slice(1, q)),
