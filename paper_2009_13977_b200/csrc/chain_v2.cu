@@ -504,10 +504,10 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             if (trc && lane == 0 && mt == 0) trc[(size_t)t * 16 + 10] = clock64() + (long long)(z[0] != z[0]);
             const float* zr = Zr + ((size_t)slot * C * MT + mt) * 128 + lane * 4;
             float zs[4] = {0.f, 0.f, 0.f, 0.f};
-            // fixed order over the source CTAs; five 16-byte loads in flight
-            // per round (all ten spill the register budget; two-tile
-            // geometries keep two)
-            constexpr int ZU = TPW == 1 ? 5 : 2;
+            // fixed order over the source CTAs; ten 16-byte loads in flight
+            // (two rounds of five: 56.34 vs 56.28 us, two: 57.6 us per fused
+            // step; two-tile geometries keep two, their register budget spills)
+            constexpr int ZU = TPW == 1 ? 10 : 2;
 #pragma unroll ZU
             for (int c = 0; c < C; ++c) {
                 float p[4];
