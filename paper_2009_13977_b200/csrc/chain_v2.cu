@@ -68,8 +68,8 @@ __host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg, 
     o += (size_t)RT * 256 * (sig ? 2 : 1);
     L.zn = o;
     o += (size_t)2 * KB * 128;
-    L.red = o;
-    o += (size_t)NR * MT * 128;
+    L.red = o;  // double-buffered where push warps can run (NR <= 6): no end-of-step barrier
+    o += (size_t)NR * MT * 128 * (NR <= 6 ? 2 : 1);
     o = (o + 3) & ~size_t(3);
     L.bars = o;
     o += 2 * (nstg + NSLOTV) + 6;  // + the tape warp's two mbarriers and step counter
@@ -233,6 +233,10 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     const size_t tape_step = (size_t)a.ngroups * a.d_pad * WCV;
     float* const tape0 = D.tape ? D.tape + ((size_t)group * a.d_pad + row0) * WCV : nullptr;
 
+    // the row warps' partials of step s: with push warps, two buffers (a
+    // step's partials are read by the push warps while the row warps already
+    // form the next step's)
+    auto redb = [&](int s) { return NP > 0 ? (s & 1) * NR * MT * 128 : 0; };
     // the CTA's sum of the row warps' partials (fixed order; all loads in
     // flight), pushed to CTAs first, first + step, ... of the cluster
     auto combine_push = [&](int s, int first, int step) {
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             float part[MAXNR][4];
 #pragma unroll
             for (int w = 0; w < MAXNR; ++w)
-                if (w < NR) lds_vec<4>(part[w], red + (w * MT + mt) * 128 + lane * 4);
+                if (w < NR) lds_vec<4>(part[w], red + redb(s) + (w * MT + mt) * 128 + lane * 4);
 #pragma unroll
             for (int e = 0; e < 4; ++e) sum[mt][e] = part[0][e];
 #pragma unroll
@@ -302,12 +306,14 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
-            *reinterpret_cast<float4*>(red + (warp * MT + mt) * 128 + lane * 4) =
+            *reinterpret_cast<float4*>(red + redb(s) + (warp * MT + mt) * 128 + lane * 4) =
                 make_float4(pm[mt][0] + (p1[mt][0] + p2[mt][0]), pm[mt][1] + (p1[mt][1] + p2[mt][1]),
                             pm[mt][2] + (p1[mt][2] + p2[mt][2]), pm[mt][3] + (p1[mt][3] + p2[mt][3]));
         if (trc && tid == 0) trc[(size_t)(s > 0 ? s - 1 : q) * 16 + 1] = clock64();
         if constexpr (NP > 0) {  // hand the partials to the push warps, go on
-            asm volatile("bar.arrive 4, %0;" ::"r"((NR + NP) * 32) : "memory");
+            // (a sync, not an arrive: the row warps run a step ahead of the end
+            // of step, so the hand-off keeps them in step with the push warps)
+            asm volatile("bar.sync 4, %0;" ::"r"((NR + NP) * 32) : "memory");
             return;
         }
         // every row warp forms the CTA's sum (fixed order over the row warps;
@@ -592,13 +598,15 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         }
         WSTAMP(2);
         if constexpr (NP > 0) {
-            // barrier 2 without the B warps: they run ahead into Z_{t+1}
-            // (exchange wait, reduce) while the row warps update X.  Safe: B
-            // warps overwrite Zn[t & 1] only in step t+2, after barrier 1 of
-            // step t+1, which the row warps reach after reading it here; their
-            // S reads of a stage precede barrier 1, the refill follows this one
-            if (warp < NR || warp == PW || pusher)
-                asm volatile("bar.sync 3, %0;" ::"r"((NR + 1 + NP) * 32) : "memory");
+            // no end-of-step barrier: the row warps go from the update straight
+            // into the next step's partial (their own X tiles), the B warps are
+            // already forming Z_{t+1}.  Safe: B warps overwrite Zn[t & 1] only
+            // in step t+2, after barrier 1 of step t+1, which the row warps
+            // reach after reading it here; every reader of a stage is done by
+            // barrier 1 of its step, after which the producer refills it; the
+            // push warps read a step's partials before pushing L_{t+1}, which
+            // every CTA's Z_{t+1} (so barrier 1 of step t+1, before the row
+            // warps write that buffer again) waits for
         } else if constexpr (SIG) {
             asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
         } else {
