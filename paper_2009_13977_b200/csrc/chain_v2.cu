@@ -607,10 +607,9 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
             // push warps read a step's partials before pushing L_{t+1}, which
             // every CTA's Z_{t+1} (so barrier 1 of step t+1, before the row
             // warps write that buffer again) waits for
-        } else if constexpr (SIG) {
-            asm volatile("bar.sync 0, %0;" ::"r"(nmain) : "memory");
         } else {
-            __syncthreads();
+            // none either: the row warps read the partials buffer (their own
+            // combine) before barrier 1, and write it again after it
         }
         WSTAMP(3);
         if (trc && tid == 0) trc[(size_t)t * 16 + 7] = clock64(), trc[(size_t)t * 16 + 9] = (long long)dev::globaltimer();
