@@ -753,15 +753,16 @@ fasth_status run_dv(fasth_ctx c, fasth_tape t, float* dV, int64_t lddv, bool pip
 // each block's finished tape rows (done[i]) and the gradient kernel, launched
 // as its programmatic dependent, starts on a block as soon as both chains
 // have passed it.  Not for the panel sweep (it keeps no counters).
-// The publishing costs the sweep ~1 us (a signal warp outside the step's
-// barriers, sweep2_kernel<.., SIG>); the gradient tail it removes is worth
-// more where the blocks finish in sweep order (fasth_backward: block t after
-// step t; 101.9 vs 103.2 us for the two-call step) and where dV goes out over
-// PCIe (the host-buffer step), not for the fused device step (blocks finish
-// only from mid-sweep on: 62.3 vs 60.9 us).  FASTH_DV_PIPE=0/1 forces it.
+// The publishing costs the sweep (tape and publish warps outside the step's
+// barrier, sweep2_kernel<.., SIG>) about what the gradient tail it removes is
+// worth on the device (fused 57.4 vs 55.1 us, two-call 84.7 vs 83.1 us back
+// to back): default only where dV goes out over PCIe (the host-buffer step,
+// and the streamed one always).  FASTH_DV_PIPE=0/1 forces it.
 bool dv_pipe_ok(fasth_ctx c, const SweepV2Args& a) {
     const char* e = getenv("FASTH_DV_PIPE");
-    const bool dflt = c->dv_pipe_pref || (a.ndir == 1 && !a.dir[0].forward);
+    // (the two-call backward defaulted to it until the sweep lost its
+    // end-of-step barrier: now 88.1 vs 90.1 us serial vs pipelined)
+    const bool dflt = c->dv_pipe_pref;
     if (e ? atoi(e) == 0 : !dflt) return false;
     // (the signal-warp sweep spills at 64-wide blocks: not there)
     return a.q <= kMaxPipeQ && a.BS <= 32 && c->counters_len >= 3 * kMaxPipeQ && !use_panel(a) &&
