@@ -24,12 +24,13 @@
 //     fragments) and do both the partial (A) and the update (C) on them; two
 //     B warps form Z; one producer warp only issues the stage copies;
 //   * shared addresses are computed once; ring indices are counters.
-// Per step (two CTA barriers):
+// Per step (one CTA barrier, between the phases):
 //   phase 1   row warps: L_{t+1} partial from X^(t) and W_{t+1}, combined over
 //             the row warps in fixed order, pushed to every CTA of the
 //             cluster (st.async + remote mbarrier complete_tx)
 //             B warps:   Z_t = sum_c L_t^c (fixed order) + (-2 S_t Z_{t-1})
-//   phase 2   row warps: X^(t+1) = X^(t) + V_t (-2 Z_t) in their accumulators
+//   phase 2   row warps: X^(t+1) = X^(t) + V_t (-2 Z_t) in their accumulators,
+//             then straight on into the next step's phase 1
 #include <algorithm>
 #include <cstdlib>
 
