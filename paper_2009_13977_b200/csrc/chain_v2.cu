@@ -82,7 +82,10 @@ __host__ __device__ inline V2Smem v2_layout(int C, int BS, int d_pad, int nstg, 
 // the DSMEM pushes off the row warps (which then only run the partial MMAs
 // and the update per step); for NR <= kPushMaxNR row warps.
 constexpr int kPushMaxNR = 6;
-template <int BS, int TPW, bool SIG, int NP>
+// TR: the trace stamps (FASTH_TRACE / FASTH_STEPTRACE) are compiled in; the
+// production instantiations carry none of their code (the loop is latency
+// bound and sensitive to its code layout)
+template <int BS, int TPW, bool SIG, int NP, bool TR>
 __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP + (SIG ? (TPW == 1 ? 2 : 1) : 0)) * 32, 1)
     sweep2_kernel(SweepV2Args a) {
     constexpr int MT = BS / 16, KB = BS / 8;
@@ -135,13 +138,13 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     const uint32_t xrdy_u32 = bar_u32 + 8u * (NSTG + NSLOTV), xfree_u32 = xrdy_u32 + 8u;
     auto xbuf = [&](int k) { return Xn + (SIG ? (k & 1) * RT * 256 : 0); };
     unsigned* prog = reinterpret_cast<unsigned*>(bars + NSTG + NSLOTV + 2);  // steps copied out
-    long long* trc = a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
+    long long* const trc = TR && a.trace ? a.trace + (size_t)blockIdx.x * (q + 1) * 16 : nullptr;
     // prologue / epilogue global-timer stamps in row q: 10 entry, 11 X loaded,
     // 12 cluster synced, 13 prologue partial pushed, 14 loop done, 15 exit
     // per-warp barrier stamps (FASTH_TRACE): [CTA][step][warp < 12][arrive S1,
     // release S1, arrive S2, release S2]; the release stamp sits behind a
     // volatile shared load, which cannot issue before the barrier resolves
-    long long* wtr = a.wtrace ? a.wtrace + (size_t)blockIdx.x * q * 48 : nullptr;
+    long long* const wtr = TR && a.wtrace ? a.wtrace + (size_t)blockIdx.x * q * 48 : nullptr;
 #define WSTAMP(k)                                                                             \
     if (wtr && lane == 0) {                                                                   \
         if ((k) & 1) {                                                                        \
@@ -664,7 +667,9 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
 template <int BS, int TPW, int NP>
 cudaError_t launch_t(const SweepV2Args& a, cudaStream_t s) {
     const V2Smem L = v2_layout(a.C, BS, a.d_pad, a.nstg, a.done != nullptr);
-    auto kern = a.done ? sweep2_kernel<BS, TPW, true, NP> : sweep2_kernel<BS, TPW, false, NP>;
+    const bool tr = a.trace || a.wtrace;
+    auto kern = a.done ? (tr ? sweep2_kernel<BS, TPW, true, NP, true> : sweep2_kernel<BS, TPW, true, NP, false>)
+                       : (tr ? sweep2_kernel<BS, TPW, false, NP, true> : sweep2_kernel<BS, TPW, false, NP, false>);
     if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), L.total, true); e != cudaSuccess) return e;
     const int RT = a.d_pad / a.C / 16;
     const int NR = RT < MAXNR ? RT : MAXNR;
