@@ -180,21 +180,6 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
         if (tid == 0) wait_counter_bounded(a.xg_ready, a.xg_target);
         __syncthreads();
     }
-    if (warp == PW && lane == 0) {
-        const uint32_t stg_u32 = dev::smem_u32(stg);
-        // launched as a programmatic dependent of the builder: everything up
-        // to here overlapped its tail; its stages are read only from now on
-        if (!a.ready && a.pdl) {
-            asm volatile("griddepcontrol.wait;" ::: "memory");
-            if (a.late_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        }
-        for (int t = 0; t < NSTG && t < q; ++t) {
-            if (a.ready) wait_counter_bounded(a.ready + block_of(t), (unsigned)C);
-            mbar_expect_u32(bar_u32 + 8u * t, stage_bytes);
-            bulk_u32(stg_u32 + (uint32_t)t * stage_bytes, gstage(t), stage_bytes, bar_u32 + 8u * t);
-        }
-    }
-
     // row warps: X^(0) tiles into registers and B-fragment order (x_wait: X
     // is the previous grid's output, the launch only started early)
     float x[TPW][4];
@@ -230,6 +215,21 @@ __global__ void __launch_bounds__(((NP ? kPushMaxNR : MAXNR) + BS / 16 + 1 + NP 
     if (a.xg_ready && tid == 0 && atomicAdd(a.xg_seen, 1u) == gridDim.x - 1) {
         *a.xg_ready = 0u;
         *a.xg_seen = 0u;
+    }
+    if (warp == PW && lane == 0) {
+        const uint32_t stg_u32 = dev::smem_u32(stg);
+        // launched as a programmatic dependent of the builder: everything up
+        // to here (X loaded, the cluster synced) overlapped its tail; its
+        // stages are read only from now on
+        if (!a.ready && a.pdl) {
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (a.late_trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        }
+        for (int t = 0; t < NSTG && t < q; ++t) {
+            if (a.ready) wait_counter_bounded(a.ready + block_of(t), (unsigned)C);
+            mbar_expect_u32(bar_u32 + 8u * t, stage_bytes);
+            bulk_u32(stg_u32 + (uint32_t)t * stage_bytes, gstage(t), stage_bytes, bar_u32 + 8u * t);
+        }
     }
     GSTAMP(12);
 
