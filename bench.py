@@ -539,10 +539,14 @@ def main():
     hout = (torch.empty((M, D), dtype=torch.float32).pin_memory(),
             torch.empty((M, D), dtype=torch.float32).pin_memory(),
             torch.empty((D, D), dtype=torch.float32).pin_memory())
-    # the first ~15 calls after the device-resident runs ramp down from ~200
-    # us (PCIe / host clocks waking up): at least 50 untimed calls
-    for _ in range(max(args.warmup, 50)):
+    # after the device-resident runs the first calls ramp down from ~190 us
+    # over ~15 ms (the PCIe link and host waking up; BENCH_E2E_DUMP): untimed
+    # calls for at least 0.2 s and W steps
+    t_w = time.perf_counter() + 0.2
+    n_w = 0
+    while n_w < args.warmup or time.perf_counter() < t_w:
         fb.forward_backward_host(Vh, Xh, Gh, B, ctx=hctx, out=hout)
+        n_w += 1
     e2e_steps = max(20, min(args.steps, 200))
     if world > 1:
         dist.barrier()
