@@ -78,7 +78,8 @@ __host__ __device__ constexpr size_t dv2_smem() {
 // Z'b / Z'f chunk into shared memory), then Q = Z'f Z'b^T, then the main
 // product with B fragments read and split by the consumer; dV written from
 // the accumulators (8 consecutive rows per column per store instruction).
-template <int BS>
+// TR: timeline stamps compiled in (FASTH_STEPTRACE runs only)
+template <int BS, bool TR>
 __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     constexpr int NT = BS / 8, MT = BS / 16, KB = BS / 8;
     constexpr int LDZ = MCH + 4;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
     const size_t tstep = (size_t)a.ngroups * a.d_pad * 8;
     const float* tA = a.tapeA + (size_t)i * tstep;
     const float* tG = a.tapeG + (size_t)i * tstep;
-    long long* trc = a.trace && threadIdx.x == 0 ? a.trace + ((size_t)i * gridDim.x + blockIdx.x) * 6 : nullptr;
+    long long* const trc = TR && a.trace && threadIdx.x == 0 ? a.trace + ((size_t)i * gridDim.x + blockIdx.x) * 6 : nullptr;
     if (trc) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(DV_WARPS * 32, 3) dv2_kernel(DvArgs a) {
 
 template <int BS>
 cudaError_t launch_dv2_t(const DvArgs& a, cudaStream_t s) {
+    auto kern = a.trace ? dv2_kernel<BS, true> : dv2_kernel<BS, false>;
     const dim3 grid((a.d_pad + DV_ROWS - 1) / DV_ROWS, a.q);
     size_t smem = dv2_smem<BS>();
     // pipelined behind the sweep: claim enough shared memory that no CTA
@@ -328,7 +330,7 @@ cudaError_t launch_dv2_t(const DvArgs& a, cudaStream_t s) {
     // the latency-bound chain steps more than the overlap gains)
     if (a.done && a.min_smem > smem) smem = a.min_smem;
     if (smem > 48 * 1024)
-        if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(dv2_kernel<BS>), smem); e != cudaSuccess) return e;
+        if (cudaError_t e = ensure_smem(reinterpret_cast<const void*>(kern), smem); e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(DV_WARPS * 32, 1, 1);
@@ -339,7 +341,7 @@ cudaError_t launch_dv2_t(const DvArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = (a.done || a.pdl) ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, dv2_kernel<BS>, a);
+    return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 }  // namespace
