@@ -415,7 +415,10 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
         // group of NPU n-tiles) — 8 units at BS = 32, RB = 80
         constexpr int NPU = 5;
         const int ntl = RB / 8, ng = (ntl + NPU - 1) / NPU;
-        const int nW = 2 * MT * ng, nS = (doSf ? MT : 0) + (doSb ? MT : 0);
+        // S units in n-tile halves: the ranks forming S give their extra
+        // work to half their warps in two small pieces, not one large one
+        constexpr int NTH = NT / 2;
+        const int nW = 2 * MT * ng, nS = 2 * ((doSf ? MT : 0) + (doSb ? MT : 0));
         for (int u = warp; u < nW + nS; u += NTH4 / 32) {
             if (u < nW) {
                 const bool fwd = u < MT * ng;
@@ -464,14 +467,14 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
                 }
             } else {
                 // Sf = T~ G_{i,i+1} (A = T~, B[l][k] = GnT[k][l]);  Sb = T~^T G_{i,i-1} (A = T~^T)
-                const int su = u - nW;
+                const int su = (u - nW) >> 1, nt0 = ((u - nW) & 1) * NTH;
                 const bool fwd = doSf && su < MT;
                 const int mt = su % MT;
                 const float2* Am = fwd ? TfS : TTS;
                 const float* Bm = fwd ? GnT : GpT;
-                float acc[NT][3][4];
+                float acc[NTH][3][4];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt)
+                for (int nt = 0; nt < NTH; ++nt)
 #pragma unroll
                     for (int b = 0; b < 3; ++b)
 #pragma unroll
@@ -486,10 +489,11 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
                     af.l[0] = __float_as_uint(a0.y), af.l[1] = __float_as_uint(a1.y);
                     af.l[2] = __float_as_uint(a2.y), af.l[3] = __float_as_uint(a3.y);
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
+                    for (int nn = 0; nn < NTH; ++nn) {
+                        const int nt = nt0 + nn;
                         const float b0 = Bm[(nt * 8 + g) * LDG + ks * 8 + tq];
                         const float b1 = Bm[(nt * 8 + g) * LDG + ks * 8 + tq + 4];
-                        mma3s(acc[nt][0], acc[nt][1], acc[nt][2], af, __uint_as_float(hi_rn(b0)),
+                        mma3s(acc[nn][0], acc[nn][1], acc[nn][2], af, __uint_as_float(hi_rn(b0)),
                               __uint_as_float(hi_rn(b1)), lo_rn(b0), lo_rn(b1));
                     }
                 }
@@ -498,11 +502,11 @@ __global__ void __launch_bounds__(NTH4, BS == 64 ? 1 : 2) build4_kernel(Plan p, 
                 for (int h = 0; h < 2; ++h) {
                     const int j = mt * 16 + g + 8 * h;
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
+                    for (int nn = 0; nn < NTH; ++nn)
 #pragma unroll
                         for (int e = 0; e < 2; ++e)
-                            img[j * LDV + perm_v_bs(nt * 8 + 2 * tq + e, BS)] =
-                                acc[nt][0][2 * h + e] + (acc[nt][1][2 * h + e] + acc[nt][2][2 * h + e]);
+                            img[j * LDV + perm_v_bs((nt0 + nn) * 8 + 2 * tq + e, BS)] =
+                                acc[nn][0][2 * h + e] + (acc[nn][1][2 * h + e] + acc[nn][2][2 * h + e]);
                 }
             }
         }
