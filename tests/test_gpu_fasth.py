@@ -76,6 +76,30 @@ def test_fused_forward_backward_matches_reference_golden(fb, golden, case):
     assert max(errs) <= TOL, errs
 
 
+def test_traced_instantiations_same_bits(fb, monkeypatch, tmp_path):
+    """The traced kernel instantiations (FASTH_STEPTRACE: the fused step's
+    timeline; FASTH_TRACE: per-phase stamps of the sweeps) compute the same
+    bits as the production ones, whose stamps are compiled out, and write
+    their dumps."""
+    import glob
+    rng = np.random.default_rng(7)
+    d, b, m = 784, 32, 32
+    V, X, G = rng.standard_normal((d, d)), rng.standard_normal((d, m)), rng.standard_normal((d, m))
+    want = [host(t) for t in run_chain(fb, V, X, G, b, fused=True)]
+    monkeypatch.setenv("FASTH_STEPTRACE", str(tmp_path / "st"))
+    ctx = fb.Context(0)
+    Y, back = fb.fasth_forward_backward(dev(V), dev(X), dev(G), b, ctx=ctx)
+    ctx.check()
+    for u, w in zip((Y, back.grad_input, back.grad_vectors), want):
+        assert np.array_equal(host(u), w)
+    assert (tmp_path / "st.bin").exists()
+    monkeypatch.delenv("FASTH_STEPTRACE")
+    monkeypatch.setenv("FASTH_TRACE", str(tmp_path / "tr"))
+    for u, w in zip(run_chain(fb, V, X, G, b, fused=True), want):
+        assert np.array_equal(host(u), w)
+    assert glob.glob(str(tmp_path / "tr*.v2.bin"))
+
+
 @pytest.mark.parametrize("d,b,m", [(784, 32, 32), (64, 8, 32), (2048, 32, 32), (200, 17, 33), (96, 8, 100)])
 def test_fused_equals_two_calls_bitwise(fb, monkeypatch, d, b, m):
     """Same kernels, same per-column arithmetic: the one-launch fwd+bwd must
